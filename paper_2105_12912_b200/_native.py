@@ -1,0 +1,162 @@
+"""ctypes binding of liblzb.so (the sm_100a kernels behind include/lzb.h).
+
+This is the ONLY way the package reaches compute: there is no CPU fallback.
+Importing a compute entry point without a CUDA device or without the built
+library raises ``RuntimeError`` -- loudly, by design.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import CompressionError, CorruptArchiveError, DataError, QuantOverflowError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "liblzb.so")
+
+LZB_OK, LZB_E_ARG, LZB_E_DATA, LZB_E_OVERFLOW = 0, 1, 2, 3
+LZB_E_CORRUPT, LZB_E_CUDA, LZB_E_ASSERT, LZB_E_CAPACITY = 4, 5, 6, 7
+
+STATUS_BYTES = 64
+
+
+class Geom(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_uint64), ("ny", ctypes.c_uint64), ("nz", ctypes.c_uint64),
+                ("cx", ctypes.c_uint64), ("cy", ctypes.c_uint64), ("cz", ctypes.c_uint64),
+                ("ndim", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+# name -> (restype, argtypes); every entry is declared in include/lzb.h
+_P, _U64, _I, _U32, _D, _SZ = (ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32,
+                               ctypes.c_double, ctypes.c_size_t)
+_GP = ctypes.POINTER(Geom)
+SIGNATURES = {
+    "lzb_version": (ctypes.c_char_p, []),
+    "lzb_strerror": (ctypes.c_char_p, [_I]),
+    "lzb_field_range": (_I, [_P, _I, _U64, _P, _P]),
+    "lzb_prequantize": (_I, [_P, _I, _U64, _D, _P, _P, _P]),
+    "lzb_quantize_scratch_bytes": (_SZ, [_GP, _U64]),
+    "lzb_quantize": (_I, [_P, _I, _GP, _D, _U32, _P, _I, _P, _P, _U64, _P, _P, _SZ, _P]),
+    "lzb_histogram": (_I, [_P, _I, _U64, _U32, _P, _P, _P]),
+    "lzb_codebook_scratch_bytes": (_SZ, [_U32]),
+    "lzb_codebook": (_I, [_P, _U32, _P, _P, _P, _P, _SZ, _P]),
+    "lzb_codebook_from_lengths": (_I, [_P, _U32, _P, _P, _P, _SZ, _P]),
+    "lzb_huff_encode_scratch_bytes": (_SZ, [_U64]),
+    "lzb_huff_encode": (_I, [_P, _I, _U64, _P, _P, _U32, _P, _U64, _P, _P, _SZ, _P]),
+    "lzb_huff_encode_at": (_I, [_P, _I, _U64, _P, _P, _U32, _U64, _P, _U64, _P, _P, _SZ, _P]),
+    "lzb_huff_decode_scratch_bytes": (_SZ, [_U64, _U32, _U32]),
+    "lzb_huff_decode": (_I, [_P, _U64, _U64, _P, _U32, _U32, _P, _I, _P, _P, _SZ, _P]),
+    "lzb_rle_encode_scratch_bytes": (_SZ, [_U64]),
+    "lzb_rle_encode": (_I, [_P, _I, _U64, _P, _P, _U64, _U64, _P, _P, _SZ, _P]),
+    "lzb_rle_decode_scratch_bytes": (_SZ, [_U64]),
+    "lzb_rle_decode": (_I, [_P, _P, _U64, _U32, _P, _I, _U64, _P, _P, _SZ, _P]),
+    "lzb_reconstruct_scratch_bytes": (_SZ, [_GP, _U64]),
+    "lzb_reconstruct": (_I, [_P, _I, _P, _U64, _GP, _D, _U32, _P, _I, _P, _P, _P, _SZ, _P]),
+    "lzb_dequantize": (_I, [_P, _U64, _D, _P, _I, _P, _P]),
+    "lzb_chunk_major": (_I, [_P, _P, _I, _GP, _I, _P]),
+    "lzb_quality_scratch_bytes": (_SZ, [_U64]),
+    "lzb_quality": (_I, [_P, _P, _I, _U64, _P, _P, _SZ, _P]),
+}
+# not in the C header but exported for the RLE sizing path
+EXTRA = {"lzb_rle_encode_scratch_bytes_runs": (_SZ, [_U64, _U64])}
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load liblzb.so and declare every entry point (no GPU needed)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"liblzb.so not built ({path}); run `python -c 'import __graft_entry__ as g; g.build()'`"
+            " -- there is no CPU fallback")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in {**SIGNATURES, **EXTRA}.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2105_12912_b200 requires a CUDA (sm_100a) device; "
+                           "there is no CPU fallback")
+    return load_library()
+
+
+def geom(dims, chunk) -> Geom:
+    nx, ny, nz, ndim = dims
+    cx, cy, cz = chunk
+    return Geom(nx, ny, nz, cx, cy, cz, ndim, 0)
+
+
+def check_rc(rc: int, what: str) -> None:
+    if rc != LZB_OK:
+        msg = load_library().lzb_strerror(rc).decode()
+        raise CompressionError(f"{what}: liblzb returned {rc} ({msg})")
+
+
+class Status:
+    """A host view of one lzb_dstatus block read back from the device."""
+
+    __slots__ = ("code", "detail", "u")
+
+    def __init__(self, raw: np.ndarray):
+        self.code = int(raw[:4].view(np.int32)[0])
+        self.detail = int(raw[4:8].view(np.int32)[0])
+        self.u = [int(v) for v in raw[8:56].view(np.uint64)]
+
+    def f64(self, i: int) -> float:
+        return float(np.array([self.u[i]], np.uint64).view(np.float64)[0])
+
+
+def read_status(block) -> list[Status]:
+    """One device->host read of a (k x 64)-byte status tensor (synchronises)."""
+    raw = block.cpu().numpy().reshape(-1, STATUS_BYTES)
+    return [Status(r) for r in raw]
+
+
+def raise_for(st: Status, stage: str, corrupt_msg: str | None = None) -> None:
+    c = st.code
+    if c == LZB_OK or c == LZB_E_CAPACITY:
+        return
+    if c == LZB_E_OVERFLOW:
+        if stage == "reconstruct":
+            raise QuantOverflowError("prefix-sum magnitude bound exceeded; use a larger error "
+                                     "bound or smaller chunks")
+        raise QuantOverflowError("prequantized magnitude exceeds the integer range; "
+                                 "use a larger error bound")
+    if c == LZB_E_ASSERT:
+        raise AssertionError("prequantization error-bound invariant violated")
+    if c == LZB_E_CORRUPT:
+        raise CorruptArchiveError(corrupt_msg or f"{stage}: archive is corrupt")
+    if c == LZB_E_DATA:
+        if stage in ("reconstruct", "dequantize", "range"):
+            raise DataError(f"non-finite value at element offset {st.u[2]}")
+        raise DataError(f"{stage}: invalid data")
+    raise CompressionError(f"{stage}: device status {c}")
+
+
+def stream_ptr() -> int:
+    import torch
+
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int:
+    return t.data_ptr() if t is not None else 0
+
+
+def empty_bytes(n: int, device="cuda"):
+    import torch
+
+    return torch.empty(max(int(n), 1), dtype=torch.uint8, device=device)

@@ -1,0 +1,846 @@
+// K3 Huffman bit packing and K5 self-synchronising parallel Huffman decode.
+//
+// Reference semantics (P = /root/reference/pkg/src/lzebc):
+//   encode            P/huffman.py:46-61   MSB-first concatenation of code words,
+//                                          last byte zero padded, NO per-chunk
+//                                          offsets anywhere (dense stream)
+//   _decode_tables    P/huffman.py:64-82   canonical first/limit/offset tables
+//   _decode_kernel    P/huffman.py:85-106  bit-serial; -1 code > 64 bits,
+//                                          -2 too many code words, -3 stream ends
+//                                          mid code word
+//   decode            P/huffman.py:109-122 count mismatch -> CorruptArchiveError
+//
+// K3: tiles of 4096 symbols; per-thread bit counts -> block scan ->
+// decoupled look-back gives the tile's u64 bit offset in ONE pass over the
+// symbols.  Code words are OR-ed into a shared-memory word buffer; words fully
+// inside the tile are stored directly (big-endian byte order), the <= 2 partial
+// boundary words per tile go through a tiny fix-up pass.
+//
+// K5: the stream is cut into subsequences of S bits.  For every
+// possible entry phase p in [0, maxlen) a thread decodes its subsequence and
+// records a transfer map p -> (exit phase, code words started); phases merge
+// as soon as they hit a code-word boundary of an already decoded path, so the
+// common case costs ~one decode.  A hierarchical composition of the maps gives
+// every subsequence's true entry phase and symbol offset with bounded work
+// even for non-synchronising (e.g. fixed-length) code books.  A final pass
+// decodes from the true entries, staging 32 symbols per lane in shared memory
+// so each warp writes coalesced runs.
+#include "lzb_common.cuh"
+
+namespace lzb {
+
+// ============================================================================
+// K3 encode
+// ============================================================================
+constexpr int kEThreads = 256;
+constexpr int kESyms = 16;
+constexpr int kETile = kEThreads * kESyms;
+
+struct EncParams {
+    const void *sym;
+    uint64_t n;
+    const uint8_t *lengths;
+    const uint64_t *codes;
+    uint32_t cap;
+    uint8_t *out;
+    uint64_t out_bytes;
+    uint64_t bit_offset;  // phase of the first bit inside out[0] (0..7)
+    lzb_dstatus *st;
+    uint64_t *lb;
+    unsigned int *ticket;
+    uint64_t ntiles;
+    uint64_t *frag;  // per tile: [head word, head bits, tail word, tail bits] (word = ~0 none)
+    uint32_t maxlen;
+    int table_smem;
+};
+
+__device__ __forceinline__ void store_word_bytes(uint8_t *out, uint64_t byte0, uint32_t be_word,
+                                                 uint64_t limit) {
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+        if (byte0 + k < limit) out[byte0 + k] = (uint8_t)(be_word >> (24 - 8 * k));
+}
+
+template <typename SymT>
+__global__ void __launch_bounds__(kEThreads) k_huff_encode(EncParams p) {
+    extern __shared__ __align__(16) unsigned char e_smem[];
+    uint64_t *s_codes = reinterpret_cast<uint64_t *>(e_smem);
+    uint8_t *s_lens = reinterpret_cast<uint8_t *>(s_codes + (p.table_smem ? p.cap : 0));
+    uint32_t *s_words = reinterpret_cast<uint32_t *>(
+        e_smem + (((p.table_smem ? p.cap * 9u : 0u) + 15u) & ~15u));
+    __shared__ uint32_t s_scan[33];
+    __shared__ uint64_t s_tile, s_excl;
+    const uint64_t *g_codes = p.table_smem ? s_codes : p.codes;
+    const uint8_t *g_lens = p.table_smem ? s_lens : p.lengths;
+    if (p.table_smem) {
+        for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) {
+            s_codes[i] = p.codes[i];
+            s_lens[i] = p.lengths[i];
+        }
+    }
+    const uint32_t tid = threadIdx.x;
+    bool bad = false;
+    while (true) {
+        if (tid == 0) s_tile = atomicAdd(p.ticket, 1u);
+        __syncthreads();
+        const uint64_t t = s_tile;
+        if (t >= p.ntiles) break;
+        const uint64_t base = t * kETile + (uint64_t)tid * kESyms;
+        uint32_t s[kESyms];
+        const SymT *sp = static_cast<const SymT *>(p.sym) + base;
+        if (base + kESyms <= p.n && sizeof(SymT) == 2 &&
+            (reinterpret_cast<uintptr_t>(sp) & 15) == 0) {
+            uint4 a = reinterpret_cast<const uint4 *>(sp)[0];
+            uint4 b = reinterpret_cast<const uint4 *>(sp)[1];
+            uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                s[2 * k] = w[k] & 0xFFFFu;
+                s[2 * k + 1] = w[k] >> 16;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kESyms; k++) s[k] = base + k < p.n ? (uint32_t)sp[k] : 0xFFFFFFFFu;
+        }
+        uint32_t nb = 0;
+#pragma unroll
+        for (int k = 0; k < kESyms; k++) {
+            if (s[k] != 0xFFFFFFFFu) {
+                uint32_t L = s[k] < p.cap ? g_lens[s[k]] : 0u;
+                if (L == 0) bad = true;
+                nb += L;
+            }
+        }
+        uint32_t tile_bits;
+        uint32_t off = block_exclusive_scan<uint32_t>(nb, s_scan, &tile_bits);
+        if ((tid >> 5) == 0) {
+            uint64_t ex = lookback_warp(p.lb, t, tile_bits);
+            if (lane_id() == 0) s_excl = ex;
+        }
+        __syncthreads();
+        const uint64_t G = s_excl + p.bit_offset;  // absolute bit position of the tile
+        const uint32_t lead = (uint32_t)(G & 31);
+        const uint64_t wbase = G >> 5;
+        const uint32_t nwords = (lead + tile_bits + 31) >> 5;
+        for (uint32_t i = tid; i < nwords; i += kEThreads) s_words[i] = 0;
+        __syncthreads();
+        uint32_t pos = lead + off;
+#pragma unroll
+        for (int k = 0; k < kESyms; k++) {
+            if (s[k] == 0xFFFFFFFFu || s[k] >= p.cap) continue;
+            uint32_t L = g_lens[s[k]];
+            uint64_t c = g_codes[s[k]];
+            while (L > 0) {
+                uint32_t w = pos >> 5, b = pos & 31;
+                uint32_t room = 32 - b;
+                uint32_t take = L < room ? L : room;
+                uint32_t piece = (uint32_t)((c >> (L - take)) & ((1ull << take) - 1ull));
+                atomicOr(&s_words[w], piece << (room - take));
+                L -= take;
+                pos += take;
+            }
+        }
+        __syncthreads();
+        // words fully inside [G, G + tile_bits) are stored directly
+        const uint64_t endbit = G + tile_bits;
+        const bool aligned = (reinterpret_cast<uintptr_t>(p.out) & 3) == 0;
+        for (uint32_t i = tid; i < nwords; i += kEThreads) {
+            uint64_t gw = wbase + i;
+            bool full = (gw * 32 >= G) && (gw * 32 + 32 <= endbit);
+            if (!full) continue;
+            uint32_t v = s_words[i];
+            if (aligned)
+                reinterpret_cast<uint32_t *>(p.out)[gw] = bswap32(v);
+            else
+                store_word_bytes(p.out, gw * 4, v, ~0ull);
+        }
+        if (tid == 0) {
+            uint64_t hw = ~0ull, hb = 0, tw = ~0ull, tb = 0;
+            if (tile_bits > 0) {
+                if (lead != 0) {
+                    hw = wbase;
+                    hb = s_words[0];
+                }
+                if ((endbit & 31) != 0) {
+                    uint64_t last = (endbit - 1) >> 5;
+                    if (last != hw) {
+                        tw = last;
+                        tb = s_words[nwords - 1];
+                    }
+                }
+            }
+            p.frag[4 * t + 0] = hw;
+            p.frag[4 * t + 1] = hb;
+            p.frag[4 * t + 2] = tw;
+            p.frag[4 * t + 3] = tb;
+            if (t == p.ntiles - 1) p.st->u[0] = s_excl + tile_bits;
+        }
+        __syncthreads();
+    }
+    if (__any_sync(0xffffffffu, bad) && lane_id() == 0) set_status(p.st, LZB_E_DATA);
+}
+
+// Boundary words: each partial word is shared by at most the tail of tile t
+// and the head of tile t+1 (every tile but the last spans >= 4096 bits).
+__global__ void k_huff_fixup(EncParams p) {
+    const uint64_t nbytes = umin64(p.out_bytes, (p.bit_offset + p.st->u[0] + 7) / 8);
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < p.ntiles;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t hw = p.frag[4 * t], hb = p.frag[4 * t + 1];
+        const uint64_t tw = p.frag[4 * t + 2], tb = p.frag[4 * t + 3];
+        if (hw != ~0ull) {
+            uint32_t v = (uint32_t)hb;
+            if (t > 0) {
+                if (p.frag[4 * (t - 1) + 2] == hw) v |= (uint32_t)p.frag[4 * (t - 1) + 3];
+                else if (p.frag[4 * (t - 1)] == hw) v |= (uint32_t)p.frag[4 * (t - 1) + 1];
+            }
+            store_word_bytes(p.out, hw * 4, v, nbytes);
+        }
+        if (tw != ~0ull) {
+            bool shared = t + 1 < p.ntiles && p.frag[4 * (t + 1)] == tw;
+            if (!shared) store_word_bytes(p.out, tw * 4, (uint32_t)tb, nbytes);
+        }
+    }
+}
+
+// ============================================================================
+// K5 decode
+// ============================================================================
+constexpr int kLutBits = 12;
+constexpr uint32_t kLutSize = 1u << kLutBits;
+constexpr uint8_t kExitInvalid = 0xFF;
+constexpr uint8_t kExitEnd = 0xFE;
+constexpr int kMaxPaths = 4;
+constexpr uint32_t kMergeWin = 128;  // bits in which phases look for a merge
+
+struct DecTables {
+    uint32_t lut[kLutSize];  // (len << 20) | sym ; 0 = long code or invalid prefix
+    uint64_t first[65];
+    uint64_t cnt[65];
+    uint32_t off[65];
+    uint32_t maxlen;
+    uint32_t nsym;
+};
+
+struct DecParams {
+    const uint32_t *words;  // 4-byte aligned base covering the stream
+    uint32_t head;          // bit offset of the stream inside words[0]
+    uint64_t nwords;
+    uint64_t bit_len;
+    uint64_t count;
+    const DecTables *tab;
+    const uint32_t *syms;  // symbols sorted by (length, symbol)
+    uint32_t S;            // subsequence length in bits (multiple of 32)
+    uint64_t T;            // subsequences
+    uint32_t P;            // phases per subsequence (= maxlen)
+    uint32_t *maps;        // T * P entries: (count << 8) | exit
+    lzb_dstatus *st;
+    void *out;
+    // resolution
+    uint32_t G;        // group size
+    uint64_t ng1, ng2;
+    uint64_t *g1;      // ng1 * P : (count << 8) | exit
+    uint64_t *g2;      // ng2 * P
+    uint8_t *ent2;     // per level-2 group: entry phase
+    uint64_t *off2;    // per level-2 group: symbol offset
+    uint8_t *ent1;
+    uint64_t *off1;
+    uint8_t *ent0;     // per subsequence
+    uint64_t *off0;
+};
+
+__device__ __forceinline__ uint32_t bswap_load(const DecParams &p, uint64_t w) {
+    return w < p.nwords ? bswap32(__ldg(&p.words[w])) : 0u;
+}
+
+// 64 bits starting at absolute stream bit q (MSB aligned)
+__device__ __forceinline__ uint64_t peek64(const DecParams &p, uint64_t q) {
+    uint64_t a = q + p.head;
+    uint64_t w = a >> 5;
+    uint32_t b = a & 31;
+    uint64_t hi = ((uint64_t)bswap_load(p, w) << 32) | bswap_load(p, w + 1);
+    if (b == 0) return hi;
+    uint64_t nx = bswap_load(p, w + 2);
+    return (hi << b) | (nx >> (32 - b));
+}
+
+struct BitReader {
+    uint64_t buf;  // MSB aligned
+    int nb;        // valid bits in buf (>= 32 after refill)
+    uint64_t nextw;
+    uint64_t pos;  // absolute stream bit of buf's MSB
+
+    __device__ __forceinline__ void init(const DecParams &p, uint64_t q) {
+        uint64_t a = q + p.head;
+        uint64_t w = a >> 5;
+        uint32_t b = a & 31;
+        buf = (((uint64_t)bswap_load(p, w) << 32) | bswap_load(p, w + 1)) << b;
+        nb = 64 - b;
+        nextw = w + 2;
+        pos = q;
+    }
+    __device__ __forceinline__ void consume(const DecParams &p, uint32_t L) {
+        buf <<= L;
+        nb -= L;
+        pos += L;
+        if (nb < 32) {
+            buf |= (uint64_t)bswap_load(p, nextw++) << (32 - nb);
+            nb += 32;
+        }
+    }
+};
+
+// Decode one code word at the reader.  Returns len (0 = invalid), *sym.
+__device__ __forceinline__ uint32_t decode_one(const DecParams &p, const uint32_t *lut,
+                                               const DecTables *tab, BitReader &r, uint32_t &sym) {
+    uint32_t e = lut[r.buf >> (64 - kLutBits)];
+    if (e) {
+        sym = e & 0xFFFFFu;
+        return e >> 20;
+    }
+    // long code (or invalid prefix): canonical tables, reading 64 bits directly
+    uint64_t v = (r.nb >= 64) ? r.buf : peek64(p, r.pos);
+    for (uint32_t L = kLutBits + 1; L <= tab->maxlen; L++) {
+        uint64_t c = v >> (64 - L);
+        uint64_t f = tab->first[L], k = tab->cnt[L];
+        if (k && c >= f && c - f < k) {
+            sym = p.syms[tab->off[L] + (uint32_t)(c - f)];
+            return L;
+        }
+    }
+    return 0;
+}
+
+__global__ void k_dec_tables(const uint8_t *lengths, uint32_t cap, uint32_t maxlen_hint,
+                             DecTables *tab, uint32_t *syms, lzb_dstatus *st) {
+    __shared__ uint32_t s_cnt[65];
+    __shared__ uint32_t s_off[65];
+    __shared__ uint32_t s_bad, s_max;
+    for (uint32_t i = threadIdx.x; i < 65; i += blockDim.x) s_cnt[i] = 0;
+    if (threadIdx.x == 0) {
+        s_bad = 0;
+        s_max = 0;
+    }
+    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) tab->lut[i] = 0;
+    __syncthreads();
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
+        uint32_t L = lengths[s];
+        if (L > 64) s_bad = 1;
+        else if (L) {
+            atomicAdd(&s_cnt[L], 1u);
+            atomicMax(&s_max, L);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // Codebook.from_lengths validation (P/codebook.py:125-140)
+        uint32_t used = 0;
+        for (int L = 1; L <= 64; L++) used += s_cnt[L];
+        int rc = 0;
+        if (s_bad || used == 0) rc = 1;
+        else if (used == 1) rc = (s_max != 1);
+        else {
+            int64_t avail = 1;
+            for (int L = 1; L <= 64 && !rc; L++) {
+                avail = 2 * avail - (int64_t)s_cnt[L];
+                if (avail < 0 || avail > (int64_t)cap) rc = 1;
+            }
+            if (!rc && avail != 0) rc = 1;
+        }
+        if (rc) {
+            set_status(st, LZB_E_CORRUPT);
+            s_bad = 1;
+        }
+        uint64_t f = 0;
+        uint32_t o = 0;
+        for (int L = 1; L <= 64; L++) {
+            f = (L == 1) ? 0 : (f + s_cnt[L - 1]) << 1;
+            tab->first[L] = f;
+            tab->cnt[L] = s_cnt[L];
+            tab->off[L] = o;
+            s_off[L] = o;
+            o += s_cnt[L];
+        }
+        tab->first[0] = 0;
+        tab->cnt[0] = 0;
+        tab->off[0] = 0;
+        tab->maxlen = s_max;
+        tab->nsym = used;
+        if (s_max > maxlen_hint) {
+            set_status(st, LZB_E_CORRUPT);
+            s_bad = 1;
+        }
+    }
+    __syncthreads();
+    if (s_bad) return;
+    // symbols in (length, symbol) order + LUT fill; warp 0 ranks 32 symbols at a time
+    if (threadIdx.x < 32) {
+        const uint32_t lane = threadIdx.x;
+        for (uint32_t s0 = 0; s0 < cap; s0 += 32) {
+            uint32_t s = s0 + lane;
+            uint32_t L = s < cap ? lengths[s] : 0u;
+            uint32_t peers = __match_any_sync(0xffffffffu, L);
+            uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+            uint32_t o = s_off[L];
+            if (s < cap && L) {
+                uint32_t idx = o + rank;
+                syms[idx] = s;
+                if (L <= (uint32_t)kLutBits) {
+                    uint64_t code = tab->first[L] + (idx - tab->off[L]);
+                    uint32_t lo = (uint32_t)(code << (kLutBits - L));
+                    uint32_t hi = lo + (1u << (kLutBits - L));
+                    for (uint32_t v = lo; v < hi; v++) tab->lut[v] = (L << 20) | s;
+                }
+            }
+            __syncwarp();
+            if (L && lane == (uint32_t)(__ffs(peers) - 1)) s_off[L] = o + __popc(peers);
+            __syncwarp();
+        }
+    }
+}
+
+struct Path {
+    uint64_t bm[kMergeWin / 64];
+    uint32_t exit;  // packed exit code
+    uint32_t count;
+};
+
+__device__ __forceinline__ bool bm_test(const uint64_t *bm, uint32_t q) {
+    return (bm[q >> 6] >> (q & 63)) & 1ull;
+}
+__device__ __forceinline__ uint32_t bm_rank(const uint64_t *bm, uint32_t q) {  // set bits < q
+    uint32_t r = 0;
+#pragma unroll
+    for (uint32_t i = 0; i < kMergeWin / 64; i++) {
+        if (q >= 64 * (i + 1)) r += __popcll(bm[i]);
+        else if (q > 64 * i) r += __popcll(bm[i] & ((1ull << (q - 64 * i)) - 1ull));
+    }
+    return r;
+}
+
+// Phase maps: thread per subsequence.
+__global__ void __launch_bounds__(128) k_dec_maps(DecParams p) {
+    __shared__ uint32_t s_lut[kLutSize];
+    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) s_lut[i] = p.tab->lut[i];
+    __syncthreads();
+    const DecTables *tab = p.tab;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < p.T;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t0 = t * p.S;
+        const bool last = (t == p.T - 1);
+        const uint64_t stop = last ? p.bit_len : t0 + p.S;  // decode while pos < stop
+        Path paths[kMaxPaths];
+        int npaths = 0;
+        for (uint32_t ph = 0; ph < p.P; ph++) {
+            uint32_t out;
+            const uint64_t q0 = t0 + ph;
+            if (ph >= p.S || q0 > p.bit_len) {
+                out = kExitInvalid;
+            } else {
+                // immediate merge?
+                int hit = -1;
+                for (int k = 0; k < npaths; k++)
+                    if (ph < kMergeWin && bm_test(paths[k].bm, ph)) { hit = k; break; }
+                if (hit >= 0) {
+                    out = ((paths[hit].count - bm_rank(paths[hit].bm, ph)) << 8) | paths[hit].exit;
+                } else {
+                    Path mine;
+#pragma unroll
+                    for (int i = 0; i < (int)(kMergeWin / 64); i++) mine.bm[i] = 0;
+                    BitReader r;
+                    r.init(p, q0);
+                    uint32_t steps = 0;
+                    bool merged = false, invalid = false;
+                    uint32_t mcount = 0, mexit = 0;
+                    while (r.pos < stop) {
+                        uint32_t rel = (uint32_t)(r.pos - t0);
+                        if (rel < kMergeWin) {
+                            for (int k = 0; k < npaths; k++) {
+                                if (bm_test(paths[k].bm, rel)) {
+                                    merged = true;
+                                    mcount = steps + paths[k].count - bm_rank(paths[k].bm, rel);
+                                    mexit = paths[k].exit;
+                                    break;
+                                }
+                            }
+                            if (merged) break;
+                            mine.bm[rel >> 6] |= 1ull << (rel & 63);
+                        }
+                        uint32_t sym;
+                        uint32_t L = decode_one(p, s_lut, tab, r, sym);
+                        if (L == 0 || r.pos + L > p.bit_len) {
+                            invalid = true;
+                            break;
+                        }
+                        r.consume(p, L);
+                        steps++;
+                    }
+                    if (merged) {
+                        out = (mcount << 8) | mexit;
+                    } else if (invalid) {
+                        out = kExitInvalid;
+                    } else {
+                        uint32_t ex;
+                        if (last) ex = (r.pos == p.bit_len) ? kExitEnd : kExitInvalid;
+                        else ex = (uint32_t)(r.pos - stop);
+                        out = (steps << 8) | ex;
+                        if (npaths < kMaxPaths && ex != kExitInvalid) {
+                            mine.exit = ex;
+                            mine.count = steps;
+                            paths[npaths++] = mine;
+                        }
+                    }
+                }
+            }
+            if ((out & 0xFF) == kExitInvalid) out = kExitInvalid;
+            p.maps[t * p.P + ph] = out;
+        }
+    }
+}
+
+// Level-1/2 composition: thread per (group, phase).  in: n_in maps of P entries
+// (32-bit or 64-bit packed (count << 8) | exit).
+template <typename InT>
+__global__ void k_dec_compose(const InT *in, uint64_t n_in, uint32_t P, uint32_t G, uint64_t *out,
+                              uint64_t nout) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nout * P;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t g = i / P;
+        uint32_t ph = (uint32_t)(i - g * P);
+        uint64_t cnt = 0;
+        uint32_t e = ph;
+        uint64_t a = g * G, b = umin64(a + G, n_in);
+        for (uint64_t k = a; k < b; k++) {
+            uint64_t v = in[k * P + e];
+            uint32_t ex = (uint32_t)(v & 0xFF);
+            cnt += v >> 8;
+            e = ex;
+            if (ex == kExitInvalid || ex == kExitEnd) {
+                // END is only legal as the very last map of the stream
+                if (ex == kExitEnd && k + 1 != n_in) e = kExitInvalid;
+                break;
+            }
+        }
+        out[i] = (cnt << 8) | e;
+    }
+}
+
+// Walk `n` maps of group `g` from entry phase e0 / offset o0, writing each
+// member's entry + offset (used top-down).
+template <typename InT>
+__device__ __forceinline__ void walk_down(const InT *maps, uint32_t P, uint64_t a, uint64_t b,
+                                          uint32_t e, uint64_t o, uint8_t *ent, uint64_t *off) {
+    for (uint64_t k = a; k < b; k++) {
+        ent[k] = (uint8_t)e;
+        off[k] = o;
+        if (e == kExitInvalid || e == kExitEnd) {
+            e = kExitInvalid;
+            continue;
+        }
+        uint64_t v = maps[k * P + e];
+        o += v >> 8;
+        e = (uint32_t)(v & 0xFF);
+    }
+}
+
+__global__ void k_dec_top(DecParams p) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint32_t e = 0;
+    uint64_t o = 0;
+    for (uint64_t h = 0; h < p.ng2; h++) {
+        p.ent2[h] = (uint8_t)e;
+        p.off2[h] = o;
+        if (e == kExitInvalid || e == kExitEnd) {
+            e = kExitInvalid;
+            continue;
+        }
+        uint64_t v = p.g2[h * p.P + e];
+        o += v >> 8;
+        e = (uint32_t)(v & 0xFF);
+    }
+    if (e != kExitEnd || o != p.count) set_status(p.st, LZB_E_CORRUPT);
+    p.st->u[0] = o;
+}
+
+__global__ void k_dec_down2(DecParams p) {
+    for (uint64_t h = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; h < p.ng2;
+         h += (uint64_t)gridDim.x * blockDim.x)
+        walk_down(p.g1, p.P, h * p.G, umin64(h * p.G + p.G, p.ng1), p.ent2[h], p.off2[h], p.ent1,
+                  p.off1);
+}
+
+__global__ void k_dec_down1(DecParams p) {
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < p.ng1;
+         g += (uint64_t)gridDim.x * blockDim.x)
+        walk_down(p.maps, p.P, g * p.G, umin64(g * p.G + p.G, p.T), p.ent1[g], p.off1[g], p.ent0,
+                  p.off0);
+}
+
+// Final decode: lanes decode their subsequence, 32 symbols per round staged in
+// shared memory, and the warp writes each lane's run cooperatively.
+constexpr int kFThreads = 128;
+constexpr int kStage = 32;
+template <typename SymT>
+__global__ void __launch_bounds__(kFThreads) k_dec_final(DecParams p) {
+    __shared__ uint32_t s_lut[kLutSize];
+    __shared__ SymT s_stage[kFThreads / 32][32][kStage + 1];
+    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) s_lut[i] = p.tab->lut[i];
+    __syncthreads();
+    if (p.st->code) return;  // corrupt stream: leave the output untouched
+    const DecTables *tab = p.tab;
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    SymT *out = static_cast<SymT *>(p.out);
+    const uint64_t tstride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t tb = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); tb < p.T;
+         tb += tstride) {
+        const uint64_t t = tb + lane;
+        const bool act = t < p.T;
+        BitReader r;
+        uint64_t stop = 0, o = 0;
+        bool live = false;
+        if (act) {
+            uint32_t e = p.ent0[t];
+            if (e != kExitInvalid && e != kExitEnd) {
+                r.init(p, t * p.S + e);
+                stop = (t == p.T - 1) ? p.bit_len : umin64(t * p.S + p.S, p.bit_len);
+                o = p.off0[t];
+                live = r.pos < stop;
+            }
+        }
+        while (__any_sync(0xffffffffu, live)) {
+            uint32_t k = 0;
+            if (live) {
+                for (; k < (uint32_t)kStage && r.pos < stop; k++) {
+                    uint32_t sym;
+                    uint32_t L = decode_one(p, s_lut, tab, r, sym);
+                    if (L == 0) {
+                        r.pos = stop;
+                        break;
+                    }
+                    s_stage[warp][lane][k] = (SymT)sym;
+                    r.consume(p, L);
+                }
+                live = r.pos < stop;
+            }
+            __syncwarp();
+            // cooperative write-out of every lane's k symbols
+            for (uint32_t j = 0; j < 32; j++) {
+                uint32_t kj = __shfl_sync(0xffffffffu, k, j);
+                uint64_t oj = __shfl_sync(0xffffffffu, o, j);
+                if (lane < kj && oj + lane < p.count) out[oj + lane] = s_stage[warp][j][lane];
+            }
+            o += k;
+            __syncwarp();
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
+struct DecLayout {
+    uint32_t S, P, G;
+    uint64_t T, ng1, ng2;
+};
+
+static DecLayout dec_layout(uint64_t bit_len, uint32_t maxlen) {
+    DecLayout L;
+    L.P = maxlen < 1 ? 1 : maxlen;
+    // enough subsequences to fill the GPU (~2 threads per 148*2048 lanes), S >= 4*P
+    uint64_t S = bit_len / (148ull * 2048ull);
+    if (S < 256) S = 256;
+    if (S > 8192) S = 8192;
+    while (S < 4ull * L.P) S *= 2;
+    S = (S + 31) / 32 * 32;
+    L.S = (uint32_t)S;
+    L.T = bit_len ? (bit_len + S - 1) / S : 1;
+    L.G = 256;
+    L.ng1 = (L.T + L.G - 1) / L.G;
+    L.ng2 = (L.ng1 + L.G - 1) / L.G;
+    return L;
+}
+
+template <typename Sc>
+static void dec_scratch(Sc &s, const DecLayout &L, uint32_t cap) {
+    s.template take<DecTables>(1);
+    s.template take<uint32_t>(cap);
+    s.template take<uint32_t>(L.T * L.P);
+    s.template take<uint64_t>(L.ng1 * L.P);
+    s.template take<uint64_t>(L.ng2 * L.P);
+    s.template take<uint8_t>(L.ng2);
+    s.template take<uint64_t>(L.ng2);
+    s.template take<uint8_t>(L.ng1);
+    s.template take<uint64_t>(L.ng1);
+    s.template take<uint8_t>(L.T);
+    s.template take<uint64_t>(L.T);
+}
+
+static int dev_sms() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 148;
+}
+
+}  // namespace lzb
+
+using namespace lzb;
+
+// ---------------------------------------------------------------------------
+extern "C" size_t lzb_huff_encode_scratch_bytes(uint64_t n) {
+    ScratchSize s;
+    uint64_t nt = (n + kETile - 1) / kETile;
+    s.take<uint64_t>(nt ? nt : 1);
+    s.take<unsigned int>(4);
+    s.take<uint64_t>(4 * (nt ? nt : 1));
+    return s.bytes();
+}
+
+static int huff_encode_impl(const void *sym, int sym_bytes, uint64_t n, const uint8_t *lengths,
+                            const uint64_t *codes, uint32_t cap, uint8_t *out, uint64_t out_bytes,
+                            uint64_t bit_offset, lzb_dstatus *st, void *scratch,
+                            size_t scratch_bytes, void *stream) {
+    if (!lengths || !codes || !st || (sym_bytes != 2 && sym_bytes != 4) || cap == 0)
+        return LZB_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
+    if (n == 0) return LZB_OK;
+    if (!sym || !out) return LZB_E_ARG;
+    uint64_t nt = (n + kETile - 1) / kETile;
+    Scratch sc(scratch, scratch_bytes);
+    EncParams p;
+    p.lb = sc.take<uint64_t>(nt);
+    p.ticket = sc.take<unsigned int>(4);
+    p.frag = sc.take<uint64_t>(4 * nt);
+    if (!p.frag) return LZB_E_ARG;
+    LZB_CUDA_TRY(cudaMemsetAsync(p.lb, 0, nt * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.ticket, 0, 4 * sizeof(unsigned int), s));
+    p.sym = sym;
+    p.n = n;
+    p.lengths = lengths;
+    p.codes = codes;
+    p.cap = cap;
+    p.out = out;
+    p.out_bytes = out_bytes;
+    p.bit_offset = bit_offset;
+    p.st = st;
+    p.ntiles = nt;
+    p.maxlen = 64;
+    p.table_smem = cap <= 4096;
+    size_t table = p.table_smem ? align_up((size_t)cap * 9, 16) : 0;
+    size_t smem = table + ((size_t)kETile * 64 / 32 + 2) * sizeof(uint32_t);
+    auto kern = sym_bytes == 2 ? k_huff_encode<uint16_t> : k_huff_encode<uint32_t>;
+    LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEThreads, smem));
+    uint64_t grid = (uint64_t)dev_sms() * (per_sm > 0 ? per_sm : 1);
+    if (grid > nt) grid = nt;
+    kern<<<(unsigned)grid, kEThreads, smem, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    // bytes actually owned by this stream: through the last bit
+    k_huff_fixup<<<(unsigned)umin64((nt + 255) / 256, 4096), 256, 0, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}
+
+extern "C" int lzb_huff_encode(const void *sym, int sym_bytes, uint64_t n, const uint8_t *lengths,
+                               const uint64_t *codes, uint32_t cap, uint8_t *out, uint64_t out_bytes,
+                               lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream) {
+    return huff_encode_impl(sym, sym_bytes, n, lengths, codes, cap, out, out_bytes, 0, st, scratch,
+                            scratch_bytes, stream);
+}
+
+// Multi-GPU slab variant: the slab's first bit lands at bit `bit_offset` (0..7)
+// of out[0]; out[0]'s leading bits and the last byte's trailing bits are left
+// zero for an OR-merge with the neighbouring slabs.
+extern "C" int lzb_huff_encode_at(const void *sym, int sym_bytes, uint64_t n, const uint8_t *lengths,
+                                  const uint64_t *codes, uint32_t cap, uint64_t bit_offset,
+                                  uint8_t *out, uint64_t out_bytes, lzb_dstatus *st, void *scratch,
+                                  size_t scratch_bytes, void *stream) {
+    if (bit_offset > 7) return LZB_E_ARG;
+    return huff_encode_impl(sym, sym_bytes, n, lengths, codes, cap, out, out_bytes, bit_offset, st,
+                            scratch, scratch_bytes, stream);
+}
+
+extern "C" size_t lzb_huff_decode_scratch_bytes(uint64_t bit_len, uint32_t maxlen, uint32_t cap) {
+    ScratchSize s;
+    dec_scratch(s, dec_layout(bit_len, maxlen), cap);
+    return s.bytes();
+}
+
+extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t count,
+                               const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym,
+                               int sym_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
+                               void *stream) {
+    if (!lengths || !st || (sym_bytes != 2 && sym_bytes != 4) || cap == 0 || maxlen == 0 ||
+        maxlen > 64)
+        return LZB_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
+    DecLayout L = dec_layout(bit_len, maxlen);
+    Scratch sc(scratch, scratch_bytes);
+    DecTables *tab = sc.take<DecTables>(1);
+    uint32_t *syms = sc.take<uint32_t>(cap);
+    if (!syms) return LZB_E_ARG;
+    k_dec_tables<<<1, 1024, 0, s>>>(lengths, cap, maxlen, tab, syms, st);
+    LZB_LAUNCH_CHECK();
+    if (count == 0) {
+        // P/huffman.py:114-117
+        if (bit_len != 0) {
+            lzb_dstatus h{};
+            h.code = LZB_E_CORRUPT;
+            LZB_CUDA_TRY(cudaMemcpyAsync(st, &h, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            LZB_CUDA_TRY(cudaStreamSynchronize(s));
+        }
+        return LZB_OK;
+    }
+    if (!bits || !sym) return LZB_E_ARG;
+    DecParams p;
+    uintptr_t a = reinterpret_cast<uintptr_t>(bits);
+    p.words = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
+    p.head = (uint32_t)(a & 3) * 8;
+    p.nwords = (p.head / 8 + (bit_len + 7) / 8 + 3) / 4;
+    p.bit_len = bit_len;
+    p.count = count;
+    p.tab = tab;
+    p.syms = syms;
+    p.S = L.S;
+    p.T = L.T;
+    p.P = L.P;
+    p.G = L.G;
+    p.ng1 = L.ng1;
+    p.ng2 = L.ng2;
+    p.maps = sc.take<uint32_t>(L.T * L.P);
+    p.g1 = sc.take<uint64_t>(L.ng1 * L.P);
+    p.g2 = sc.take<uint64_t>(L.ng2 * L.P);
+    p.ent2 = sc.take<uint8_t>(L.ng2);
+    p.off2 = sc.take<uint64_t>(L.ng2);
+    p.ent1 = sc.take<uint8_t>(L.ng1);
+    p.off1 = sc.take<uint64_t>(L.ng1);
+    p.ent0 = sc.take<uint8_t>(L.T);
+    p.off0 = sc.take<uint64_t>(L.T);
+    if (!p.off0) return LZB_E_ARG;
+    p.st = st;
+    p.out = sym;
+    const int sms = dev_sms();
+    // phases >= the book's real max length cannot be entries (P = maxlen hint;
+    // k_dec_tables flags a hint that disagrees with the lengths as corrupt).
+    k_dec_maps<<<(unsigned)umin64((L.T + 127) / 128, (uint64_t)sms * 16), 128, 0, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    k_dec_compose<uint32_t><<<(unsigned)umin64((L.ng1 * L.P + 255) / 256, (uint64_t)sms * 32), 256, 0, s>>>(
+        p.maps, L.T, L.P, L.G, p.g1, L.ng1);
+    LZB_LAUNCH_CHECK();
+    k_dec_compose<uint64_t><<<(unsigned)umin64((L.ng2 * L.P + 255) / 256, (uint64_t)sms * 32), 256, 0, s>>>(
+        p.g1, L.ng1, L.P, L.G, p.g2, L.ng2);
+    LZB_LAUNCH_CHECK();
+    k_dec_top<<<1, 32, 0, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    k_dec_down2<<<(unsigned)umin64((L.ng2 + 127) / 128, 1024), 128, 0, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    k_dec_down1<<<(unsigned)umin64((L.ng1 + 127) / 128, (uint64_t)sms * 8), 128, 0, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    if (sym_bytes == 2)
+        k_dec_final<uint16_t><<<(unsigned)umin64((L.T + kFThreads - 1) / kFThreads, (uint64_t)sms * 16), kFThreads, 0, s>>>(p);
+    else
+        k_dec_final<uint32_t><<<(unsigned)umin64((L.T + kFThreads - 1) / kFThreads, (uint64_t)sms * 16), kFThreads, 0, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}

@@ -1,0 +1,814 @@
+// K1: fused prequantization + chunk-local Lorenzo delta + quant code +
+// histogram + outlier gather, writing the chunk-major symbol stream.
+//
+// Reference semantics (P = /root/reference/pkg/src/lzebc):
+//   prequantize            P/quantize.py:90-110
+//   _lorenzo_deltas        P/quantize.py:136-141  (nested first differences,
+//                           zero prepend INSIDE each chunk -- no halo)
+//   construct_chunk        P/quantize.py:144-158
+//   construct_grid         P/quantize.py:161-193  (outliers sorted by global index)
+//   gather_chunk_major     P/pipeline.py:102-105
+//   histogram              P/codebook.py:23-27
+//
+// Design (K1): persistent CTAs claim tiles by ticket.  A tile is up
+// to K whole chunks adjacent along x inside one chunk row, so it is one
+// contiguous box of the input AND one contiguous range of the chunk-major
+// stream.  The box is read once, coalesced, prequantized in f64 into shared
+// memory; deltas are formed from shared memory; codes are staged and written
+// back as one contiguous vectorised range.  The histogram is privatised per
+// CTA in shared memory for the whole persistent loop.  Outliers are compacted
+// in stream order (block scan + decoupled look-back over tiles), i.e. in
+// chunk-major order; a device-side check + stable per-chunk-row reorder turns
+// that into the archive's global row-major order only when needed.
+#include <type_traits>
+
+#include "lzb_common.cuh"
+
+namespace lzb {
+
+constexpr int kQThreads = 256;
+constexpr int kTile = 4096;  // max elements per tile (16 per thread)
+constexpr int kSeg = kTile / kQThreads;
+constexpr uint32_t kSmemHistMaxCap = 4096;
+constexpr double kPrequantLimit = 576460752303423488.0;  // 2^59, P/quantize.py:22
+
+struct QuantParams {
+    const void *x;
+    Geom g;
+    double two_eb;
+    double slack;  // eb_abs * (1 + 1e-12)  (P/quantize.py:108-111)
+    int64_t radius;
+    uint32_t cap;
+    void *codes;
+    unsigned long long *hist;
+    uint64_t *records;  // {u64 index, i64 delta} pairs, chunk-major order
+    uint64_t out_capacity;
+    lzb_dstatus *st;
+    uint64_t *lb;        // look-back status per tile
+    unsigned int *ticket;
+    uint64_t ntiles;
+    // box mode
+    uint32_t K;              // chunks per tile
+    uint64_t tiles_per_row;  // ceil(nbx / K)
+    // maximal-run counting for RLE sizing (P/rle.py:17-35)
+    uint32_t *tfirst, *tlast;
+    unsigned long long *inner_heads;
+};
+
+// f64 prequantization, bit-identical with numpy (P/quantize.py:90-110).
+// Returns false on overflow; sets *bad when the debug-assert invariant fails.
+__device__ __forceinline__ int64_t prequant(double v, double two_eb, double slack, int &flags) {
+    double s = __ddiv_rn(v, two_eb);
+    double r = trunc(__dadd_rn(s, copysign(0.5, s)));
+    if (fabs(r) >= kPrequantLimit) {
+        flags |= 1;
+        return 0;
+    }
+    int64_t c = (int64_t)r;
+    double back = __dmul_rn((double)c, two_eb);
+    if (!(fabs(__dsub_rn(v, back)) <= slack)) flags |= 2;
+    return c;
+}
+
+template <typename InT>
+__device__ __forceinline__ double load_in(const void *x, uint64_t i) {
+    return (double)static_cast<const InT *>(x)[i];
+}
+
+// value at element i as a prequant integer: float inputs are prequantized,
+// int64 inputs (dtype 2, construct_grid on a PrequantGrid) are taken as is.
+template <typename InT>
+__device__ __forceinline__ int64_t load_pre(const QuantParams &p, uint64_t i, int &flags) {
+    if constexpr (std::is_same<InT, int64_t>::value) {
+        return static_cast<const int64_t *>(p.x)[i];
+    } else {
+        return prequant(load_in<InT>(p.x, i), p.two_eb, p.slack, flags);
+    }
+}
+
+// Tile geometry in box mode.
+struct BoxTile {
+    uint64_t X0, Y0, Z0;
+    uint32_t BX, EY, EZ;   // box extents
+    uint32_t kc;           // chunks in this tile
+    uint32_t cx;           // chunk edge x
+    uint32_t last_ex;      // x extent of the last chunk of the tile
+    uint64_t stream_base;  // chunk-major offset of the tile's first element
+    uint32_t n;            // elements
+};
+
+__device__ __forceinline__ BoxTile box_tile(const QuantParams &p, uint64_t t) {
+    const Geom &g = p.g;
+    uint64_t row = t / p.tiles_per_row, j = t - row * p.tiles_per_row;
+    uint64_t bx0 = j * p.K, by = row % g.nby, bz = row / g.nby;
+    BoxTile b;
+    b.kc = (uint32_t)umin64(p.K, g.nbx - bx0);
+    b.X0 = bx0 * g.cx;
+    b.Y0 = by * g.cy;
+    b.Z0 = bz * g.cz;
+    b.BX = (uint32_t)umin64(b.kc * g.cx, g.nx - b.X0);
+    b.EY = (uint32_t)umin64(g.cy, g.ny - b.Y0);
+    b.EZ = (uint32_t)umin64(g.cz, g.nz - b.Z0);
+    b.cx = (uint32_t)g.cx;
+    b.last_ex = b.BX - (b.kc - 1) * b.cx;
+    b.stream_base = chunk_base(g, bx0, by, bz);
+    b.n = b.BX * b.EY * b.EZ;
+    return b;
+}
+
+// stream position inside a box tile -> box coordinates + chunk-local coords
+__device__ __forceinline__ void box_pos(const BoxTile &b, uint32_t p, uint32_t &bxl, uint32_t &ly,
+                                        uint32_t &lz, uint32_t &lx) {
+    uint32_t full = b.cx * b.EY * b.EZ;
+    uint32_t k = p / full;
+    uint32_t r = p - k * full;
+    uint32_t ex = (k == b.kc - 1) ? b.last_ex : b.cx;
+    uint32_t exy = ex * b.EY;
+    lz = r / exy;
+    r -= lz * exy;
+    ly = r / ex;
+    lx = r - ly * ex;
+    bxl = k * b.cx + lx;
+}
+
+// chunk-local Lorenzo delta from the prequant box (zero outside the chunk).
+__device__ __forceinline__ int64_t box_delta(const int64_t *s, const BoxTile &b, uint32_t bxl,
+                                             uint32_t ly, uint32_t lz, uint32_t lx) {
+    const uint32_t sy = b.BX, sz = b.BX * b.EY;
+    const uint32_t i = bxl + sy * ly + sz * lz;
+    int64_t d = s[i];
+    const bool hx = lx > 0, hy = ly > 0, hz = lz > 0;
+    if (hx) d -= s[i - 1];
+    if (hy) d -= s[i - sy];
+    if (hx && hy) d += s[i - 1 - sy];
+    if (hz) {
+        d -= s[i - sz];
+        if (hx) d += s[i - 1 - sz];
+        if (hy) d += s[i - sy - sz];
+        if (hx && hy) d -= s[i - 1 - sy - sz];
+    }
+    return d;
+}
+
+// Generic stream position -> coordinates (any ChunkSpec).
+struct StreamCoord {
+    uint64_t x, y, z;
+    uint64_t lx, ly, lz;
+};
+
+__device__ __forceinline__ StreamCoord stream_coord(const Geom &g, uint64_t pos) {
+    StreamCoord c;
+    uint64_t layer = g.nx * g.ny * g.cz;
+    uint64_t bz = pos / layer;
+    uint64_t r = pos - bz * layer;
+    uint64_t ez = umin64(g.cz, g.nz - bz * g.cz);
+    uint64_t rowsz = g.nx * ez * g.cy;
+    uint64_t by = r / rowsz;
+    r -= by * rowsz;
+    uint64_t ey = umin64(g.cy, g.ny - by * g.cy);
+    uint64_t csz = ez * ey * g.cx;
+    uint64_t bx = r / csz;
+    r -= bx * csz;
+    uint64_t ex = umin64(g.cx, g.nx - bx * g.cx);
+    c.lz = r / (ex * ey);
+    r -= c.lz * ex * ey;
+    c.ly = r / ex;
+    c.lx = r - c.ly * ex;
+    c.x = bx * g.cx + c.lx;
+    c.y = by * g.cy + c.ly;
+    c.z = bz * g.cz + c.lz;
+    return c;
+}
+
+template <typename InT>
+__device__ __forceinline__ int64_t stream_delta(const QuantParams &p, const StreamCoord &c,
+                                                int &flags) {
+    const Geom &g = p.g;
+    const uint64_t i = c.x + g.nx * (c.y + g.ny * c.z);
+    const uint64_t sy = g.nx, sz = g.nx * g.ny;
+    auto pq = [&](uint64_t j) { return load_pre<InT>(p, j, flags); };
+    int64_t d = pq(i);
+    const bool hx = c.lx > 0, hy = c.ly > 0, hz = c.lz > 0;
+    if (hx) d -= pq(i - 1);
+    if (hy) d -= pq(i - sy);
+    if (hx && hy) d += pq(i - 1 - sy);
+    if (hz) {
+        d -= pq(i - sz);
+        if (hx) d += pq(i - 1 - sz);
+        if (hy) d += pq(i - sy - sz);
+        if (hx && hy) d -= pq(i - 1 - sy - sz);
+    }
+    return d;
+}
+
+template <typename InT, typename SymT, bool BOX>
+__global__ void __launch_bounds__(kQThreads) k_quantize(QuantParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // layout: [s_pre int64 kTile (BOX only)] [s_code SymT kTile] [s_bits u32 kTile/32] [s_hist u32 cap]
+    int64_t *s_pre = reinterpret_cast<int64_t *>(smem_raw);
+    SymT *s_code = reinterpret_cast<SymT *>(smem_raw + (BOX ? kTile * sizeof(int64_t) : 0));
+    uint32_t *s_bits = reinterpret_cast<uint32_t *>(reinterpret_cast<unsigned char *>(s_code) +
+                                                    kTile * sizeof(SymT));
+    uint32_t *s_hist = s_bits + kTile / 32;
+    __shared__ uint64_t s_tile, s_excl;
+    __shared__ uint32_t s_scan[33];
+
+    const bool smem_hist = p.cap <= kSmemHistMaxCap;
+    if (smem_hist)
+        for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) s_hist[i] = 0;
+    const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+    const int64_t r = p.radius;
+    int flags = 0;
+    unsigned long long heads = 0;
+
+    while (true) {
+        if (tid == 0) s_tile = atomicAdd(p.ticket, 1u);
+        __syncthreads();
+        const uint64_t t = s_tile;
+        if (t >= p.ntiles) break;
+
+        BoxTile b;
+        uint64_t base;
+        uint32_t n;
+        if (BOX) {
+            b = box_tile(p, t);
+            base = b.stream_base;
+            n = b.n;
+            // ---- load + prequantize the box (coalesced along x) ----
+            const uint32_t bxy = b.BX * b.EY;
+            for (uint32_t i = tid; i < n; i += kQThreads) {
+                uint32_t z = i / bxy, rem = i - z * bxy, y = rem / b.BX, xx = rem - y * b.BX;
+                uint64_t gi = (b.X0 + xx) + p.g.nx * ((b.Y0 + y) + p.g.ny * (b.Z0 + z));
+                s_pre[i] = load_pre<InT>(p, gi, flags);
+            }
+            __syncthreads();
+        } else {
+            base = t * (uint64_t)kTile;
+            uint64_t total = p.g.nx * p.g.ny * p.g.nz;
+            n = (uint32_t)umin64(kTile, total - base);
+        }
+
+        // ---- deltas -> codes (staged), outlier bitmap, histogram ----
+        for (uint32_t j = 0; j < (uint32_t)kTile; j += kQThreads) {
+            const uint32_t pos = j + tid;
+            bool outl = false;
+            if (pos < n) {
+                int64_t d;
+                if (BOX) {
+                    uint32_t bxl, ly, lz, lx;
+                    box_pos(b, pos, bxl, ly, lz, lx);
+                    d = box_delta(s_pre, b, bxl, ly, lz, lx);
+                } else {
+                    d = stream_delta<InT>(p, stream_coord(p.g, base + pos), flags);
+                }
+                int64_t ad = d < 0 ? -d : d;
+                uint32_t code;
+                if (ad < r) {
+                    code = (uint32_t)(d + r);
+                } else {
+                    code = (uint32_t)r;
+                    outl = true;
+                }
+                s_code[pos] = (SymT)code;
+                if (smem_hist)
+                    atomicAdd(&s_hist[code], 1u);
+                else
+                    atomicAdd(&p.hist[code], 1ull);
+            }
+            uint32_t bal = __ballot_sync(0xffffffffu, outl);
+            if (lane == 0) s_bits[(j >> 5) + warp] = bal;
+        }
+        __syncthreads();
+
+        // ---- run heads inside the tile (RLE sizing) ----
+        {
+            const uint32_t a = tid * kSeg;
+#pragma unroll
+            for (int k = 0; k < kSeg; k++) {
+                uint32_t i = a + k;
+                if (i > 0 && i < n) heads += s_code[i] != s_code[i - 1];
+            }
+            if (tid == 0) {
+                p.tfirst[t] = (uint32_t)s_code[0];
+                p.tlast[t] = (uint32_t)s_code[n - 1];
+            }
+        }
+        // ---- write the codes: one contiguous stream range ----
+        SymT *out = static_cast<SymT *>(p.codes) + base;
+        constexpr uint32_t kVec = 16 / sizeof(SymT);
+        if ((reinterpret_cast<uintptr_t>(out) & 15) == 0 && (n % kVec) == 0) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(s_code);
+            uint4 *dst = reinterpret_cast<uint4 *>(out);
+            for (uint32_t i = tid; i < n / kVec; i += kQThreads) dst[i] = src[i];
+        } else {
+            for (uint32_t i = tid; i < n; i += kQThreads) out[i] = s_code[i];
+        }
+
+        // ---- outliers in stream order: thread owns positions [tid*kSeg, +kSeg) ----
+        const uint32_t seg0 = tid * kSeg;
+        uint32_t segbits = (s_bits[seg0 >> 5] >> (seg0 & 31)) & ((1u << kSeg) - 1u);
+        uint32_t cnt = __popc(segbits);
+        uint32_t total;
+        uint32_t off = block_exclusive_scan<uint32_t>(cnt, s_scan, &total);
+        if (warp == 0) {
+            uint64_t ex = lookback_warp(p.lb, t, total);
+            if (lane == 0) s_excl = ex;
+        }
+        __syncthreads();
+        const uint64_t excl = s_excl;
+        uint64_t w = excl + off;
+        while (segbits) {
+            uint32_t bit = __ffs(segbits) - 1;
+            segbits &= segbits - 1;
+            uint32_t pos = seg0 + bit;
+            int64_t d;
+            uint64_t gi;
+            if (BOX) {
+                uint32_t bxl, ly, lz, lx;
+                box_pos(b, pos, bxl, ly, lz, lx);
+                d = box_delta(s_pre, b, bxl, ly, lz, lx);
+                gi = (b.X0 + bxl) + p.g.nx * ((b.Y0 + ly) + p.g.ny * (b.Z0 + lz));
+            } else {
+                StreamCoord c = stream_coord(p.g, base + pos);
+                int dummy = 0;
+                d = stream_delta<InT>(p, c, dummy);
+                gi = c.x + p.g.nx * (c.y + p.g.ny * c.z);
+            }
+            if (w < p.out_capacity) {
+                p.records[2 * w] = gi;
+                p.records[2 * w + 1] = (uint64_t)d;
+            }
+            w++;
+        }
+        if (t == p.ntiles - 1 && tid == 0) {
+            uint64_t nout = excl + total;
+            p.st->u[0] = nout;
+            if (nout > p.out_capacity) set_status(p.st, LZB_E_CAPACITY);
+        }
+        __syncthreads();
+    }
+
+    if (smem_hist) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x)
+            if (s_hist[i]) atomicAdd(&p.hist[i], (unsigned long long)s_hist[i]);
+    }
+    flags = __reduce_or_sync(0xffffffffu, flags);
+    if (lane == 0 && flags) {
+        if (flags & 1) set_status(p.st, LZB_E_OVERFLOW);
+        else set_status(p.st, LZB_E_ASSERT);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) heads += __shfl_xor_sync(0xffffffffu, heads, o);
+    if (lane == 0 && heads) atomicAdd(p.inner_heads, heads);
+}
+
+// maximal runs = 1 + heads inside tiles + heads at tile boundaries
+__global__ void k_count_runs(const uint32_t *tfirst, const uint32_t *tlast, uint64_t ntiles,
+                             const unsigned long long *inner, lzb_dstatus *st) {
+    __shared__ unsigned long long s_b;
+    if (threadIdx.x == 0) s_b = 0;
+    __syncthreads();
+    unsigned long long b = 0;
+    for (uint64_t t = 1 + threadIdx.x; t < ntiles; t += blockDim.x) b += tfirst[t] != tlast[t - 1];
+    atomicAdd(&s_b, b);
+    __syncthreads();
+    if (threadIdx.x == 0) st->u[1] = 1ull + *inner + s_b;
+}
+
+// ----------------------------------------------------------------------------
+// Outlier ordering.  Records come out of K1 in chunk-major order.  The
+// archive wants them sorted by global row-major index (P/quantize.py:184-193).
+// Inside one chunk row (fixed by, bz) the records of one grid row (y, z) are
+// already in x order, so a STABLE counting sort by grid row restricted to each
+// chunk-row segment -- placed at the global row offsets -- yields the global
+// order.  All of this is skipped (device flag) when the records are already
+// strictly increasing, which is the common case (smooth fields put outliers
+// at chunk origins).
+// ----------------------------------------------------------------------------
+struct OrderParams {
+    uint64_t *records;  // in/out
+    uint64_t *tmp;      // copy of records
+    const lzb_dstatus *st;
+    uint64_t capacity;
+    Geom g;
+    uint32_t *unsorted;      // flag
+    uint32_t *row_cnt;       // ny*nz
+    uint64_t *row_start;     // ny*nz
+    uint64_t *seg_start;     // per chunk row
+    uint64_t *seg_end;       // per chunk row (0 = empty)
+    uint64_t *scan_lb;
+    unsigned int *scan_ticket;
+};
+
+__device__ __forceinline__ uint64_t order_count(const OrderParams &p) {
+    uint64_t n = p.st->u[0];
+    return n > p.capacity ? 0 : n;  // capacity errors are reported by K1
+}
+
+__global__ void k_check_sorted(OrderParams p) {
+    const uint64_t n = order_count(p);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i + 1 < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (!(p.records[2 * i] < p.records[2 * (i + 1)])) *p.unsorted = 1u;
+    }
+}
+
+__device__ __forceinline__ uint64_t chunk_row_of(const Geom &g, uint64_t idx) {
+    uint64_t x = idx % g.nx, yz = idx / g.nx;
+    (void)x;
+    uint64_t y = yz % g.ny, z = yz / g.ny;
+    return (y / g.cy) + g.nby * (z / g.cz);
+}
+
+__global__ void k_order_prepare(OrderParams p) {
+    if (!*p.unsorted) return;
+    const uint64_t n = order_count(p);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t idx = p.records[2 * i];
+        p.tmp[2 * i] = idx;
+        p.tmp[2 * i + 1] = p.records[2 * i + 1];
+        atomicAdd(&p.row_cnt[idx / p.g.nx], 1u);
+        uint64_t cr = chunk_row_of(p.g, idx);
+        if (i == 0 || chunk_row_of(p.g, p.records[2 * (i - 1)]) != cr) p.seg_start[cr] = i;
+        if (i + 1 == n || chunk_row_of(p.g, p.records[2 * (i + 1)]) != cr) p.seg_end[cr] = i + 1;
+    }
+}
+
+// exclusive scan u32 -> u64 with decoupled look-back (1 element per thread x 8)
+constexpr int kScanItems = 8;
+__global__ void __launch_bounds__(256) k_scan_u32(const uint32_t *in, uint64_t *out, uint64_t n,
+                                                  uint64_t *lb, unsigned int *ticket,
+                                                  const uint32_t *enable) {
+    if (enable && !*enable) return;
+    __shared__ uint64_t s_t, s_ex;
+    __shared__ uint64_t s_scan[33];
+    if (threadIdx.x == 0) s_t = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint64_t t = s_t;
+    const uint64_t base = t * 256 * kScanItems + (uint64_t)threadIdx.x * kScanItems;
+    uint64_t v[kScanItems];
+    uint64_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        v[k] = base + k < n ? in[base + k] : 0;
+        sum += v[k];
+    }
+    uint64_t total;
+    uint64_t off = block_exclusive_scan<uint64_t>(sum, s_scan, &total);
+    if ((threadIdx.x >> 5) == 0) {
+        uint64_t ex = lookback_warp(lb, t, total);
+        if (lane_id() == 0) s_ex = ex;
+    }
+    __syncthreads();
+    uint64_t run = s_ex + off;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        if (base + k < n) out[base + k] = run;
+        run += v[k];
+    }
+}
+
+// One CTA per chunk row: stable multi-split of its segment by local grid row.
+constexpr uint32_t kOrderMaxRows = 1024;
+__global__ void __launch_bounds__(256) k_order_scatter(OrderParams p) {
+    if (!*p.unsorted) return;
+    __shared__ uint32_t s_run[kOrderMaxRows];
+    __shared__ uint32_t s_w[8][kOrderMaxRows];
+    const Geom &g = p.g;
+    const uint64_t nrows_c = g.nby * g.nbz;
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    for (uint64_t cr = blockIdx.x; cr < nrows_c; cr += gridDim.x) {
+        const uint64_t s0 = p.seg_start[cr], s1 = p.seg_end[cr];
+        if (s1 == 0) continue;
+        const uint64_t by = cr % g.nby, bz = cr / g.nby;
+        const uint64_t Y0 = by * g.cy, Z0 = bz * g.cz;
+        const uint32_t EY = (uint32_t)umin64(g.cy, g.ny - Y0);
+        const uint32_t EZ = (uint32_t)umin64(g.cz, g.nz - Z0);
+        const uint32_t R = EY * EZ;
+        if (R <= kOrderMaxRows) {
+            for (uint32_t i = threadIdx.x; i < R; i += blockDim.x) s_run[i] = 0;
+            for (uint32_t i = threadIdx.x; i < 8 * R; i += blockDim.x) (&s_w[0][0])[i / R * kOrderMaxRows + i % R] = 0;
+            __syncthreads();
+            for (uint64_t b0 = s0; b0 < s1; b0 += blockDim.x) {
+                const uint64_t i = b0 + threadIdx.x;
+                const bool act = i < s1;
+                uint32_t lr = 0xffffffffu;
+                uint64_t idx = 0;
+                if (act) {
+                    idx = p.tmp[2 * i];
+                    uint64_t yz = idx / g.nx;
+                    uint64_t y = yz % g.ny, z = yz / g.ny;
+                    lr = (uint32_t)((y - Y0) + EY * (z - Z0));
+                }
+                uint32_t peers = __match_any_sync(0xffffffffu, lr);
+                uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+                uint32_t leader = __ffs(peers) - 1;
+                if (act && lane == leader) s_w[warp][lr] = __popc(peers);
+                __syncthreads();
+                if (act) {
+                    uint32_t before = s_run[lr];
+                    for (uint32_t w2 = 0; w2 < warp; w2++) before += s_w[w2][lr];
+                    uint64_t dst = p.row_start[idx / g.nx] + before + rank;
+                    // row_start is the global exclusive offset of the grid row;
+                    // `before + rank` counts this row's earlier records.
+                    p.records[2 * dst] = idx;
+                    p.records[2 * dst + 1] = p.tmp[2 * i + 1];
+                }
+                __syncthreads();
+                if (act && lane == leader) {
+                    uint32_t c = s_w[warp][lr];
+                    atomicAdd(&s_run[lr], c);
+                    s_w[warp][lr] = 0;
+                }
+                __syncthreads();
+            }
+        } else {
+            // very tall chunk rows: thread per grid row, ordered walk of the segment
+            for (uint32_t lr = threadIdx.x; lr < R; lr += blockDim.x) {
+                uint64_t y = Y0 + lr % EY, z = Z0 + lr / EY;
+                uint64_t row = y + g.ny * z;
+                uint64_t dst = p.row_start[row];
+                for (uint64_t i = s0; i < s1; i++) {
+                    uint64_t idx = p.tmp[2 * i];
+                    if (idx / g.nx == row) {
+                        p.records[2 * dst] = idx;
+                        p.records[2 * dst + 1] = p.tmp[2 * i + 1];
+                        dst++;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ----------------------------------------------------------------------------
+// host side
+// ----------------------------------------------------------------------------
+static bool box_mode_ok(const Geom &g, uint32_t *K) {
+    uint64_t vol = g.cx * g.cy * g.cz;
+    if (vol == 0 || vol > (uint64_t)kTile) return false;
+    *K = (uint32_t)(kTile / vol);
+    return true;
+}
+
+struct QuantLayout {
+    uint64_t ntiles;
+    bool box;
+    uint32_t K;
+    uint64_t tiles_per_row;
+    uint64_t nrows_grid, nrows_chunk;
+};
+
+static QuantLayout quant_layout(const Geom &g) {
+    QuantLayout L;
+    uint64_t n = g.nx * g.ny * g.nz;
+    L.box = box_mode_ok(g, &L.K);
+    if (L.box) {
+        L.tiles_per_row = (g.nbx + L.K - 1) / L.K;
+        L.ntiles = L.tiles_per_row * g.nby * g.nbz;
+    } else {
+        L.K = 0;
+        L.tiles_per_row = 0;
+        L.ntiles = (n + kTile - 1) / kTile;
+    }
+    L.nrows_grid = g.ny * g.nz;
+    L.nrows_chunk = g.nby * g.nbz;
+    return L;
+}
+
+template <typename S>
+static void quant_scratch(S &s, const QuantLayout &L, uint64_t cap_out) {
+    s.template take<uint64_t>(L.ntiles);                 // look-back
+    s.template take<unsigned int>(4);                    // tickets + flag
+    s.template take<uint64_t>(2 * cap_out);              // reorder copy
+    s.template take<uint32_t>(L.nrows_grid);             // row counts
+    s.template take<uint64_t>(L.nrows_grid);             // row starts
+    s.template take<uint64_t>(L.nrows_chunk);            // seg start
+    s.template take<uint64_t>(L.nrows_chunk);            // seg end
+    s.template take<uint64_t>((L.nrows_grid + 2047) / 2048 + 1);  // scan look-back
+    s.template take<uint32_t>(L.ntiles);                 // tile first code
+    s.template take<uint32_t>(L.ntiles);                 // tile last code
+    s.template take<unsigned long long>(1);              // inner heads
+}
+
+static int device_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = kNumSMs;
+    }
+    return sms;
+}
+
+template <typename InT, typename SymT, bool BOX>
+static int launch_quant(const QuantParams &qp, cudaStream_t s) {
+    size_t smem = (BOX ? kTile * sizeof(int64_t) : 0) + kTile * sizeof(SymT) + kTile / 8 +
+                  (qp.cap <= kSmemHistMaxCap ? qp.cap * sizeof(uint32_t) : 0);
+    auto kern = k_quantize<InT, SymT, BOX>;
+    LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQThreads, smem));
+    if (per_sm < 1) per_sm = 1;
+    uint64_t grid = (uint64_t)device_sms() * per_sm;
+    if (grid > qp.ntiles) grid = qp.ntiles ? qp.ntiles : 1;
+    kern<<<(unsigned)grid, kQThreads, smem, s>>>(qp);
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}
+
+}  // namespace lzb
+
+using namespace lzb;
+
+extern "C" size_t lzb_quantize_scratch_bytes(const lzb_geom *g, uint64_t out_capacity) {
+    if (!g) return 0;
+    ScratchSize s;
+    quant_scratch(s, quant_layout(make_geom(*g)), out_capacity);
+    return s.bytes();
+}
+
+extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double eb_abs,
+                            uint32_t cap, void *codes, int code_bytes, uint64_t *hist,
+                            uint64_t *outliers, uint64_t out_capacity, lzb_dstatus *st,
+                            void *scratch, size_t scratch_bytes, void *stream) {
+    if (!gg || !x || !codes || !hist || !st || dtype < 0 || dtype > 2) return LZB_E_ARG;
+    if (code_bytes != 2 && code_bytes != 4) return LZB_E_ARG;
+    if (cap < 4 || (cap & (cap - 1)) || (code_bytes == 2 && cap > 65536)) return LZB_E_ARG;
+    if (gg->cx < 1 || gg->cy < 1 || gg->cz < 1 || gg->nx < 1 || gg->ny < 1 || gg->nz < 1)
+        return LZB_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    Geom g = make_geom(*gg);
+    QuantLayout L = quant_layout(g);
+    Scratch sc(scratch, scratch_bytes);
+    uint64_t *lb = sc.take<uint64_t>(L.ntiles);
+    unsigned int *tick = sc.take<unsigned int>(4);
+    uint64_t *tmp = sc.take<uint64_t>(2 * out_capacity);
+    uint32_t *row_cnt = sc.take<uint32_t>(L.nrows_grid);
+    uint64_t *row_start = sc.take<uint64_t>(L.nrows_grid);
+    uint64_t *seg_start = sc.take<uint64_t>(L.nrows_chunk);
+    uint64_t *seg_end = sc.take<uint64_t>(L.nrows_chunk);
+    uint64_t *scan_lb = sc.take<uint64_t>((L.nrows_grid + 2047) / 2048 + 1);
+    uint32_t *tfirst = sc.take<uint32_t>(L.ntiles);
+    uint32_t *tlast = sc.take<uint32_t>(L.ntiles);
+    unsigned long long *inner = sc.take<unsigned long long>(1);
+    if (!inner) return LZB_E_ARG;
+    LZB_CUDA_TRY(cudaMemsetAsync(inner, 0, sizeof(unsigned long long), s));
+
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(hist, 0, cap * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(lb, 0, L.ntiles * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(tick, 0, 4 * sizeof(unsigned int), s));
+
+    QuantParams qp;
+    qp.x = x;
+    qp.g = g;
+    qp.two_eb = 2.0 * eb_abs;
+    qp.slack = eb_abs * (1.0 + 1e-12);
+    qp.radius = cap / 2;
+    qp.cap = cap;
+    qp.codes = codes;
+    qp.hist = reinterpret_cast<unsigned long long *>(hist);
+    qp.records = outliers;
+    qp.out_capacity = outliers ? out_capacity : 0;
+    qp.st = st;
+    qp.lb = lb;
+    qp.ticket = &tick[0];
+    qp.ntiles = L.ntiles;
+    qp.K = L.K;
+    qp.tiles_per_row = L.tiles_per_row;
+    qp.tfirst = tfirst;
+    qp.tlast = tlast;
+    qp.inner_heads = inner;
+
+    int rc;
+    if (dtype == 2) {
+        if (L.box)
+            rc = code_bytes == 2 ? launch_quant<int64_t, uint16_t, true>(qp, s)
+                                 : launch_quant<int64_t, uint32_t, true>(qp, s);
+        else
+            rc = code_bytes == 2 ? launch_quant<int64_t, uint16_t, false>(qp, s)
+                                 : launch_quant<int64_t, uint32_t, false>(qp, s);
+    } else if (L.box) {
+        if (dtype == 0)
+            rc = code_bytes == 2 ? launch_quant<float, uint16_t, true>(qp, s)
+                                 : launch_quant<float, uint32_t, true>(qp, s);
+        else
+            rc = code_bytes == 2 ? launch_quant<double, uint16_t, true>(qp, s)
+                                 : launch_quant<double, uint32_t, true>(qp, s);
+    } else {
+        if (dtype == 0)
+            rc = code_bytes == 2 ? launch_quant<float, uint16_t, false>(qp, s)
+                                 : launch_quant<float, uint32_t, false>(qp, s);
+        else
+            rc = code_bytes == 2 ? launch_quant<double, uint16_t, false>(qp, s)
+                                 : launch_quant<double, uint32_t, false>(qp, s);
+    }
+    if (rc) return rc;
+    k_count_runs<<<1, 1024, 0, s>>>(tfirst, tlast, L.ntiles, inner, st);
+    LZB_LAUNCH_CHECK();
+    if (!outliers || out_capacity == 0) return LZB_OK;
+
+    // ---- global row-major ordering of the outlier records ----
+    OrderParams op;
+    op.records = outliers;
+    op.tmp = tmp;
+    op.st = st;
+    op.capacity = out_capacity;
+    op.g = g;
+    op.unsorted = &tick[2];
+    op.row_cnt = row_cnt;
+    op.row_start = row_start;
+    op.seg_start = seg_start;
+    op.seg_end = seg_end;
+    op.scan_lb = scan_lb;
+    op.scan_ticket = &tick[1];
+    const int sms = device_sms();
+    k_check_sorted<<<sms * 4, 256, 0, s>>>(op);
+    LZB_LAUNCH_CHECK();
+    // the remaining launches exit immediately unless *unsorted was set
+    LZB_CUDA_TRY(cudaMemsetAsync(row_cnt, 0, L.nrows_grid * sizeof(uint32_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(seg_end, 0, L.nrows_chunk * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(scan_lb, 0, ((L.nrows_grid + 2047) / 2048 + 1) * sizeof(uint64_t), s));
+    k_order_prepare<<<sms * 4, 256, 0, s>>>(op);
+    LZB_LAUNCH_CHECK();
+    uint64_t scan_tiles = (L.nrows_grid + 2047) / 2048;
+    k_scan_u32<<<(unsigned)scan_tiles, 256, 0, s>>>(row_cnt, row_start, L.nrows_grid, scan_lb,
+                                                   &tick[1], op.unsorted);
+    LZB_LAUNCH_CHECK();
+    uint64_t grid = L.nrows_chunk < (uint64_t)sms * 8 ? L.nrows_chunk : (uint64_t)sms * 8;
+    k_order_scatter<<<(unsigned)(grid ? grid : 1), 256, 0, s>>>(op);
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}
+
+// ----------------------------------------------------------------------------
+// Stand-alone prequantization (stage API, P/quantize.py:95-110)
+// ----------------------------------------------------------------------------
+template <typename InT>
+__global__ void k_prequant(const InT *x, uint64_t n, double two_eb, double slack, int64_t *out,
+                           lzb_dstatus *st) {
+    int flags = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = prequant((double)x[i], two_eb, slack, flags);
+    flags = __reduce_or_sync(0xffffffffu, flags);
+    if (lane_id() == 0 && flags) set_status(st, (flags & 1) ? LZB_E_OVERFLOW : LZB_E_ASSERT);
+}
+
+extern "C" int lzb_prequantize(const void *x, int dtype, uint64_t n, double eb_abs, int64_t *out,
+                               lzb_dstatus *st, void *stream) {
+    if (!x || !out || !st || (dtype != 0 && dtype != 1)) return LZB_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
+    if (n == 0) return LZB_OK;
+    unsigned grid = (unsigned)umin64((n + 255) / 256, (uint64_t)device_sms() * 16);
+    if (dtype == 0)
+        k_prequant<float><<<grid, 256, 0, s>>>((const float *)x, n, 2.0 * eb_abs,
+                                               eb_abs * (1.0 + 1e-12), out, st);
+    else
+        k_prequant<double><<<grid, 256, 0, s>>>((const double *)x, n, 2.0 * eb_abs,
+                                                eb_abs * (1.0 + 1e-12), out, st);
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}
+
+// ----------------------------------------------------------------------------
+// Grid <-> chunk-major reorder (P/pipeline.py:102-117)
+// ----------------------------------------------------------------------------
+template <typename T>
+__global__ void k_chunk_major(const T *src, T *dst, Geom g, int direction) {
+    const uint64_t n = g.nx * g.ny * g.nz;
+    for (uint64_t pos = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; pos < n;
+         pos += (uint64_t)gridDim.x * blockDim.x) {
+        StreamCoord c = stream_coord(g, pos);
+        uint64_t gi = c.x + g.nx * (c.y + g.ny * c.z);
+        if (direction == 0)
+            dst[pos] = src[gi];
+        else
+            dst[gi] = src[pos];
+    }
+}
+
+extern "C" int lzb_chunk_major(const void *src, void *dst, int elem_bytes, const lzb_geom *gg,
+                               int direction, void *stream) {
+    if (!src || !dst || !gg || (direction != 0 && direction != 1)) return LZB_E_ARG;
+    Geom g = make_geom(*gg);
+    uint64_t n = g.nx * g.ny * g.nz;
+    cudaStream_t s = as_stream(stream);
+    unsigned grid = (unsigned)umin64((n + 255) / 256, (uint64_t)device_sms() * 16);
+    if (elem_bytes == 2)
+        k_chunk_major<uint16_t><<<grid, 256, 0, s>>>((const uint16_t *)src, (uint16_t *)dst, g, direction);
+    else if (elem_bytes == 4)
+        k_chunk_major<uint32_t><<<grid, 256, 0, s>>>((const uint32_t *)src, (uint32_t *)dst, g, direction);
+    else if (elem_bytes == 8)
+        k_chunk_major<uint64_t><<<grid, 256, 0, s>>>((const uint64_t *)src, (uint64_t *)dst, g, direction);
+    else
+        return LZB_E_ARG;
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}

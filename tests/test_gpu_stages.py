@@ -1,0 +1,191 @@
+"""GPU stage parity: each C-ABI stage against the oracle / reference KATs."""
+
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_codebook_matches_reference_lengths(golden, cuda):
+    import paper_2105_12912_b200 as lzb
+
+    _, _, k = golden
+    for h, want in zip(k["random_histograms"], k["random_lengths"]):
+        book = lzb.Codebook.from_counts(np.array(h, np.int64))
+        assert book.lengths.tolist() == want
+        assert [int(v) for v in book.codes] == [int(v) for v in O.canonical_codes(
+            np.array(want, np.uint8))]
+
+
+def test_codebook_kats(golden, cuda):
+    import paper_2105_12912_b200 as lzb
+
+    _, _, k = golden
+    for key, val in k.items():
+        if key.startswith("book_"):
+            counts = np.array([int(v) for v in key[5:].split("_")], np.int64)
+            b = lzb.Codebook.from_counts(counts)
+            assert b.lengths.tolist() == val[0]
+            assert [int(v) for v in b.codes] == val[1]
+    with pytest.raises(lzb.CorruptArchiveError):
+        lzb.Codebook.from_lengths(bytes([1, 2, 0, 0, 0, 0, 0, 0]))
+    with pytest.raises(lzb.CorruptArchiveError):
+        lzb.Codebook.from_lengths(bytes([65, 0, 0, 0]))
+    with pytest.raises(lzb.CorruptArchiveError):
+        lzb.Codebook.from_lengths(bytes(16))
+    with pytest.raises(lzb.CorruptArchiveError):
+        lzb.Codebook.from_lengths(bytes([0, 0, 3, 0]))
+
+
+def test_huffman_round_trips_and_bits(golden, cuda):
+    import paper_2105_12912_b200 as lzb
+
+    _, _, k = golden
+    book = lzb.Codebook.from_counts(np.array([2, 1, 1], np.int64))
+    s = lzb.encode(np.array([0, 1, 2], np.uint32), book)
+    assert [s.bit_len, s.count, s.data.tolist()] == k["encode_012"]
+    rng = np.random.default_rng(444)
+    for _ in range(150):
+        nsym = int(rng.integers(1, 64))
+        cap = int(rng.choice([64, 256, 1024]))
+        stream = rng.integers(0, nsym, size=int(rng.integers(1, 20000))).astype(np.uint32)
+        counts = np.bincount(stream, minlength=cap)
+        book = lzb.Codebook.from_counts(counts)
+        bs = lzb.encode(stream, book)
+        ob, oc, od = O.huff_encode(stream, book.lengths, book.codes)
+        assert bs.bit_len == ob and bs.data.tobytes() == od
+        assert np.array_equal(lzb.decode(bs, book), stream)
+    deep = lzb.Codebook.from_counts(np.array([2 ** i for i in range(12, 0, -1)], np.int64))
+    stream = np.full(1000, 11, np.uint32)
+    assert np.array_equal(lzb.decode(lzb.encode(stream, deep), deep), stream)
+    # 40-bit-deep code words (Fibonacci counts)
+    fib = [1, 1]
+    while len(fib) < 42:
+        fib.append(fib[-1] + fib[-2])
+    book = lzb.Codebook.from_counts(np.array(fib, np.int64))
+    assert book.max_len > 32
+    stream = rng.integers(0, 42, size=5000).astype(np.uint32)
+    bs = lzb.encode(stream, book)
+    assert bs.data.tobytes() == O.huff_encode(stream, book.lengths, book.codes)[2]
+    assert np.array_equal(lzb.decode(bs, book), stream)
+
+
+def test_huffman_non_synchronising_books(cuda):
+    """Fixed-length and near-fixed-length codes never self-synchronise: the
+    transfer-map composition must still find every boundary."""
+    import paper_2105_12912_b200 as lzb
+
+    rng = np.random.default_rng(9)
+    for counts in (np.full(1024, 7, np.int64), np.full(16, 3, np.int64),
+                   rng.integers(900, 1100, 1024).astype(np.int64)):
+        book = lzb.Codebook.from_counts(counts)
+        stream = rng.integers(0, len(counts), size=300_000).astype(np.uint32)
+        bs = lzb.encode(stream, book)
+        assert np.array_equal(lzb.decode(bs, book), stream)
+
+
+def test_decode_rejects_bad_streams(cuda):
+    import paper_2105_12912_b200 as lzb
+
+    book = lzb.Codebook.from_counts(np.array([4, 3, 2, 1], np.int64))
+    s = lzb.encode(np.array([0, 1, 2, 3], np.uint32), book)
+    with pytest.raises(lzb.CorruptArchiveError):
+        lzb.decode(lzb.BitStream(s.bit_len - 1, s.count, s.data), book)
+    b2 = lzb.Codebook.from_counts(np.array([4, 3], np.int64))
+    s = lzb.encode(np.array([0, 1, 0], np.uint32), b2)
+    for c in (s.count + 1, s.count - 1):
+        with pytest.raises(lzb.CorruptArchiveError):
+            lzb.decode(lzb.BitStream(s.bit_len, c, s.data), b2)
+    one = lzb.Codebook.from_counts(np.array([1], np.int64))
+    with pytest.raises(lzb.CorruptArchiveError):
+        lzb.decode(lzb.BitStream(3, 0, np.array([0], np.uint8)), one)
+    with pytest.raises(lzb.DataError):
+        lzb.encode(np.array([1], np.uint32), lzb.Codebook.from_counts(np.array([1, 0], np.int64)))
+
+
+def test_rle_stage(golden, cuda):
+    import paper_2105_12912_b200 as lzb
+    from paper_2105_12912_b200 import rle
+
+    _, _, k = golden
+    v, ln = lzb.run_length_encode(np.array([0, 0, 1, 2, 2, 2, 2, 2, 0, 0], np.uint32))
+    assert [v.tolist(), ln.tolist()] == k["rle_textbook"]
+    rng = np.random.default_rng(14)
+    for _ in range(60):
+        s = rng.integers(0, 3, int(rng.integers(1, 50000))).astype(np.uint32)
+        v, ln = lzb.run_length_encode(s)
+        ov, ol = O.rle_encode(s)
+        assert np.array_equal(v, ov) and np.array_equal(ln, ol)
+        assert np.array_equal(lzb.run_length_decode(v, ln), s)
+    old = rle._MAX_RUN
+    try:
+        rle._MAX_RUN = 4
+        s = np.array([5] * 10 + [3] + [5] * 4, np.uint32)
+        v, ln = rle.run_length_encode(s)
+        assert v.tolist() == [5, 5, 5, 3, 5] and ln.tolist() == [4, 4, 2, 1, 4]
+    finally:
+        rle._MAX_RUN = old
+    with pytest.raises(lzb.CorruptArchiveError):
+        lzb.run_length_decode(np.array([1], np.uint32), np.array([0], np.uint32))
+
+
+def test_quantize_stage_kats(golden, cuda):
+    import paper_2105_12912_b200 as lzb
+
+    _, _, k = golden
+    F = lzb.Field.from_array
+    assert lzb.quantize.prequantize(F(np.array([1.0, 0.029, -0.03, 0.0])),
+                                    lzb.QuantConfig(0.01)).codes.tolist() == k["prequant_eb001"]
+    assert lzb.quantize.prequantize(F(np.array([0.5, -0.5, 1.5, -1.5, 2.5])),
+                                    lzb.QuantConfig(0.5)).codes.tolist() == k["prequant_ties"]
+    pq = lzb.PrequantGrid(lzb.Dims.of(4), np.array([0, 5, 5, 6], np.int64))
+    q, o = lzb.quantize.construct_grid(pq, lzb.QuantConfig(0.1, 4), lzb.ChunkSpec(4))
+    assert [q.codes.tolist(), o.indices.tolist(), o.deltas.tolist()] == k["cap4_outlier"]
+    q, o = lzb.quantize.construct_grid(lzb.PrequantGrid(lzb.Dims.of(1), np.array([123])),
+                                       lzb.QuantConfig(0.5, 1024), lzb.ChunkSpec(256))
+    assert q.codes.tolist() == [635] and len(o) == 0
+    got = lzb.dequantize(lzb.PrequantGrid(lzb.Dims.of(3), np.array([-1, 0, 50])),
+                         lzb.QuantConfig(0.01), "f64")
+    assert got.values.tolist() == k["dequant"]
+
+
+def test_partial_sum_equals_sequential_exhaustive_1d(cuda):
+    """Acceptance 2 (P tests/test_acceptance.py:83-118) on the device: every
+    {-1,0,1} delta sequence up to length 8 reconstructs like the oracle."""
+    import paper_2105_12912_b200 as lzb
+
+    cfg = lzb.QuantConfig(0.5, 4)
+    seqs = [np.array(d, np.int64) for L in range(1, 9) for d in itertools.product((-1, 0, 1),
+                                                                                  repeat=L)]
+    # pack every sequence as one chunk of a long 1D grid with chunk edge 8 (pad with zeros)
+    n = 8 * len(seqs)
+    deltas = np.zeros(n, np.int64)
+    for i, d in enumerate(seqs):
+        deltas[8 * i: 8 * i + len(d)] = d
+    quant = lzb.QuantGrid(lzb.Dims.of(n), (deltas + cfg.radius).astype(np.uint32))
+    got = lzb.reconstruct_grid(quant, lzb.OutlierList.empty(), cfg, lzb.ChunkSpec(8)).codes
+    want = np.cumsum(deltas.reshape(-1, 8), axis=1).reshape(-1)
+    assert np.array_equal(got, want)
+
+
+def test_partial_sum_random_2d_3d_with_outliers(cuda):
+    import paper_2105_12912_b200 as lzb
+
+    rng = np.random.default_rng(77)
+    for i in range(40):
+        ndim = 2 if i % 2 else 3
+        shape = tuple(int(n) for n in rng.integers(1, 40, 3))
+        if ndim == 2:
+            shape = (1,) + shape[1:]
+        pre = rng.integers(-10_000, 10_000, size=shape).astype(np.int64)
+        dims = lzb.Dims(shape[2], shape[1], shape[0], ndim=ndim) if ndim == 3 else \
+            lzb.Dims(shape[2], shape[1], ndim=2)
+        spec = lzb.ChunkSpec(*[int(v) for v in rng.integers(1, 9, 3)])
+        cfg = lzb.QuantConfig(0.5, 64)
+        q, o = lzb.quantize.construct_grid(lzb.PrequantGrid(dims, pre.reshape(-1)), cfg, spec)
+        back = lzb.reconstruct_grid(q, o, cfg, spec)
+        assert np.array_equal(back.codes, pre.reshape(-1))
