@@ -1,0 +1,542 @@
+#!/usr/bin/env python
+"""bench.py -- cuSZ+ compress/decompress throughput on B200 (driver contract).
+
+One STEP = one compress + one decompress of the workload field, device
+resident (``compress_device`` -> ``decompress_device``), archives bit-exact
+with the CPU reference.  Default workload (BASELINE.json configs[4], the
+north-star config; it fits one B200): C5 = 2048^3 float32 synthetic smooth
+field (SURVEY 8(d) generator), rel eb 1e-4, auto workflow (-> Huffman).
+Inputs (34 GB) are far larger than L2 (126 MB), so no flush is needed.
+
+  value       uncompressed GB/s of the round trip: N*4 / (t_compress + t_decompress)
+  compress_gbs / decompress_gbs   the two directions separately (paper style)
+  roofline    dominant kernel: algorithmic bytes / CUDA-event time vs the
+              measured HBM copy peak (MEASURED_PEAKS.json)
+  e2e         same metric through the public API with HOST (pinned) buffers:
+              H2D field, compress, D2H archive, H2D archive, decompress, D2H field
+  cpu_baseline  the CPU oracle port (oracle/, 1 thread) on a bounded sub-slab
+
+--impl reference: the reference's CPU algorithm (the oracle port; the Python
+reference cannot travel to the GPU box) on all host threads, per-step sample
+of the same workload; rank 0 only.
+
+Multi-GPU (torchrun, N>1): strong scaling of the same 2048^3 field cut into
+N z-slabs of whole chunk layers (paper_2105_12912_b200.distributed): per rank
+K1 on its slab, NCCL all-reduce of the 8 KB histogram, identical K2 code book,
+all-gather of (bits, outliers) for archive offsets, K3 at the slab's bit
+phase.  Time = max over ranks (CUDA events).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compress/decompress GB/s at 1-8 B200 (% of HBM roofline) + compression ratio"
+
+CONFIGS = {
+    "c5": dict(shape=(2048, 2048, 2048), gen="smooth", eb=1e-4,
+               workload="C5: 3D float32 2048x2048x2048 synthetic smooth field, rel eb 1e-4"),
+    "c1": dict(shape=(100, 500, 500), gen="smooth", eb=1e-4,
+               workload="C1: 3D float32 100x500x500 (Hurricane shape) smooth, rel eb 1e-4"),
+    "c2": dict(shape=(1800, 3600), gen="smooth", eb=1e-4,
+               workload="C2: 2D float32 1800x3600 (CESM shape) smooth, rel eb 1e-4"),
+    "c3": dict(shape=(280953867,), gen="smooth1d", eb=1e-4,
+               workload="C3: 1D float32 280953867 (HACC shape) smooth, rel eb 1e-4"),
+    "c4": dict(shape=(512, 512, 512), gen="sparse", eb=1e-2,
+               workload="C4: 3D float32 512^3 (Nyx shape) sparse, rel eb 1e-2 (RLE+VLE)"),
+}
+
+
+# ---------------------------------------------------------------------------
+# synthetic fields, generated on the device slab by slab
+# ---------------------------------------------------------------------------
+def gen_smooth_device(shape, z0, z1, device, ramp=True):
+    import torch
+
+    nd = len(shape)
+    f64 = torch.float64
+    if nd == 1:
+        (nx,) = shape
+        out = torch.empty(z1 - z0, dtype=torch.float32, device=device)
+        step = 1 << 26
+        for a in range(z0, z1, step):
+            b = min(z1, a + step)
+            x = torch.arange(a, b, dtype=f64, device=device)
+            d = torch.sin(x / 13.0) * 40.0
+            if ramp:
+                d = d + 0.03 * x
+            out[a - z0: b - z0] = d.to(torch.float32)
+        return out
+    if nd == 2:
+        ny, nx = shape
+        y = torch.arange(z0, z1, dtype=f64, device=device)
+        x = torch.arange(nx, dtype=f64, device=device)
+        d = (torch.sin(y / 13.0)[:, None] + torch.sin(x / 20.0)[None, :]) * 40.0
+        if ramp:
+            d = d + 0.03 * x[None, :]
+        return d.to(torch.float32).reshape(-1)
+    nz, ny, nx = shape
+    out = torch.empty((z1 - z0, ny, nx), dtype=torch.float32, device=device)
+    y = torch.arange(ny, dtype=f64, device=device)
+    x = torch.arange(nx, dtype=f64, device=device)
+    sy = torch.sin(y / 20.0)
+    sx = torch.sin(x / 27.0)
+    rx = 0.03 * x
+    for za in range(z0, z1, 16):
+        zb = min(z1, za + 16)
+        z = torch.arange(za, zb, dtype=f64, device=device)
+        sz = torch.sin(z / 13.0)
+        d = ((sz[:, None, None] + sy[None, :, None]) + sx[None, None, :]) * 40.0
+        if ramp:
+            d = d + rx[None, None, :]
+        out[za - z0: zb - z0] = d.to(torch.float32)
+    return out.reshape(-1)
+
+
+def gen_sparse_device(shape, device, seed=0):
+    import numpy as np
+    import torch
+
+    rng = np.random.default_rng(seed)
+    data = torch.full(shape, 1.0, dtype=torch.float64, device=device)
+    nblobs = max(8, int(np.prod(shape) // 2_000_000))
+    for _ in range(nblobs):
+        c = [rng.uniform(0, s) for s in shape]
+        w = rng.uniform(2.0, 6.0)
+        amp = float(np.exp(rng.normal(3.0, 1.0)))
+        lo = [max(0, int(ci - 4 * w)) for ci in c]
+        hi = [min(s, int(ci + 4 * w) + 1) for ci, s in zip(c, shape)]
+        axes = [torch.arange(a, b, dtype=torch.float64, device=device) - ci
+                for a, b, ci in zip(lo, hi, c)]
+        r2 = sum(g.reshape([-1 if k == i else 1 for k in range(len(shape))]) ** 2
+                 for i, g in enumerate(axes))
+        sl = tuple(slice(a, b) for a, b in zip(lo, hi))
+        data[sl] += amp * torch.exp(-r2 / (2 * w * w))
+    return data.to(torch.float32).reshape(-1)
+
+
+def gen_field_device(cfg, device, z0=None, z1=None):
+    shape = cfg["shape"]
+    if cfg["gen"] == "sparse":
+        return gen_sparse_device(shape, device)
+    lead = shape[0]
+    z0 = 0 if z0 is None else z0
+    z1 = lead if z1 is None else z1
+    return gen_smooth_device(shape, z0, z1, device, ramp=cfg["gen"] != "smooth1d")
+
+
+def gen_sample_host(cfg, planes):
+    """Host numpy sub-slab of the workload for the CPU legs (same generator)."""
+    import numpy as np
+
+    shape = list(cfg["shape"])
+    if cfg["gen"] == "sparse":
+        return gen_sparse_device(tuple(shape), "cpu").numpy(), tuple(shape)
+    shape[0] = min(shape[0], planes)
+    axes = [np.arange(n, dtype=np.float64) for n in shape]
+    g = np.meshgrid(*axes, indexing="ij", sparse=True)
+    data = np.zeros(shape, np.float64)
+    for i, a in enumerate(g):
+        data = data + np.sin(a / (13.0 + 7 * i))
+    data = data * 40.0
+    if cfg["gen"] != "smooth1d":
+        data = data + 0.03 * g[-1]
+    return data.astype(np.float32).reshape(-1), tuple(shape)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}.csv")
+
+    def start(self):
+        self.t0 = self.t1 = None
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(1.5)  # nvidia-smi start-up; the first samples precede the timed region
+
+    def mark(self, which):
+        from datetime import datetime
+
+        setattr(self, which, datetime.now())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.3)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        from datetime import datetime
+
+        rows, allrows = [], []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                ts = datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f")
+                row = (float(parts[1]), float(parts[2]), parts[5:9])
+            except ValueError:
+                continue
+            allrows.append(row)
+            if self.t0 and self.t1 and self.t0 <= ts <= self.t1:
+                rows.append(row)
+        if not rows:
+            rows = allrows[-3:]  # timed region shorter than the sampling period
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for _, _, flags in rows for k, f in enumerate(flags)
+                          if f.lower() == "active"})
+        loaded = [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def profiled_traffic(kernel: str):
+    """dram bytes per launch from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+# kernels each C-ABI call launches (ours only; memsets/copies excluded), used
+# for the gpu_launches claim and cross-checked by the committed ncu launch list
+LAUNCHES = {"lzb_quantize": 6, "lzb_codebook": 1, "lzb_huff_encode": 2, "lzb_huff_decode": 8,
+            "lzb_reconstruct_with_outliers": 5, "lzb_reconstruct_no_outliers": 3,
+            "lzb_rle_encode": 6, "lzb_histogram": 1, "lzb_rle_decode": 3}
+
+
+def launches_per_step(header) -> int:
+    from paper_2105_12912_b200 import Workflow
+
+    n = LAUNCHES["lzb_quantize"] + LAUNCHES["lzb_codebook"]
+    if header.workflow is Workflow.HUFFMAN:
+        n += LAUNCHES["lzb_huff_encode"] + LAUNCHES["lzb_huff_decode"]
+    elif header.workflow is Workflow.RLE:
+        n += LAUNCHES["lzb_rle_encode"] + LAUNCHES["lzb_rle_decode"]
+    else:
+        n += (LAUNCHES["lzb_rle_encode"] + LAUNCHES["lzb_histogram"] + LAUNCHES["lzb_codebook"]
+              + LAUNCHES["lzb_huff_encode"] + LAUNCHES["lzb_huff_decode"]
+              + LAUNCHES["lzb_rle_decode"])
+    n += LAUNCHES["lzb_reconstruct_with_outliers" if header.outlier_count
+                  else "lzb_reconstruct_no_outliers"]
+    return n
+
+
+def stage_bytes(name, n, s, arc_bits_bytes, n_out):
+    """Algorithmic bytes per launch of each stage."""
+    return {
+        "K1_quantize": n * s + n * 2 + 16 * n_out,
+        "K3_huff_encode": n * 2 + arc_bits_bytes,
+        "K5_huff_decode": arc_bits_bytes + n * 2,
+        "K6_reconstruct": n * 2 + 16 * n_out + n * s,
+    }.get(name)
+
+
+# ---------------------------------------------------------------------------
+def cpu_oracle_run(values, dims, eb, threads):
+    """One oracle compress + decompress; returns (t_compress, t_decompress, archive bytes)."""
+    from oracle import oracle as O
+
+    vmin, vmax = O.check_finite_minmax(values)
+    t0 = time.perf_counter()
+    arc = O.compress(values, dims, vmin, vmax, eb, threads=threads)
+    t1 = time.perf_counter()
+    O.decompress(arc, threads=threads)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, len(arc)
+
+
+def sample_planes_for(cfg, target_elems):
+    shape = cfg["shape"]
+    per_plane = 1
+    for s in shape[1:]:
+        per_plane *= s
+    return max(1, min(shape[0], target_elems // per_plane))
+
+
+def dims_tuple(shape):
+    ext = list(shape[::-1]) + [1] * (3 - len(shape))
+    return (ext[0], ext[1], ext[2], len(shape))
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle port on all host threads, rank 0 only."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    planes = sample_planes_for(cfg, args.ref_sample_elems)
+    vals, shp = gen_sample_host(cfg, planes)
+    dims = dims_tuple(shp)
+    nbytes = vals.nbytes
+    for _ in range(args.warmup):
+        cpu_oracle_run(vals, dims, cfg["eb"], threads)
+    ts = []
+    arc_len = 0
+    for _ in range(args.steps):
+        tc, td, arc_len = cpu_oracle_run(vals, dims, cfg["eb"], threads)
+        ts.append((tc, td))
+    t = statistics.mean(a + b for a, b in ts)
+    val = nbytes / t / 1e9
+    sample = f"{'x'.join(map(str, shp[::-1]))} sub-slab of {cfg['workload'].split(':')[0]} ({vals.size} elements)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "sample": sample, "threads": threads},
+        "compress_gbs": round(nbytes / statistics.mean(a for a, _ in ts) / 1e9, 6),
+        "decompress_gbs": round(nbytes / statistics.mean(b for _, b in ts) / 1e9, 6),
+        "compression_ratio": round(nbytes / arc_len, 4),
+        "cpu_baseline": {"value": round(val, 6), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(val, 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args, cfg, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_2105_12912_b200 as lzb
+    from paper_2105_12912_b200 import _native
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    _native.lib()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+    shape = cfg["shape"]
+    if world > 1:
+        from paper_2105_12912_b200 import distributed as D
+
+        return D.bench_sharded(args, cfg, rank, world, dev, gen_field_device, METRIC)
+
+    x = gen_field_device(cfg, dev)
+    n = x.numel()
+    s = x.element_size()
+    field = lzb.Field.from_array(x.reshape(shape))
+    eb = cfg["eb"]
+    nbytes = n * s
+
+    def step(prof=None, out=None):
+        arc = lzb.compress_device(field, eb, prof=prof)
+        pre = arc.data[: arc.header.symbols[0] + 32].cpu().numpy().tobytes()
+        y, hdr, _, _ = lzb.decompress_device(arc.data, raw_host=pre, prof=prof, out=out)
+        return arc, y
+
+    ybuf = torch.empty(n, dtype=x.dtype, device=dev)
+    for _ in range(args.warmup):
+        arc, y = step(out=ybuf)
+    torch.cuda.synchronize()
+    hdr = arc.header
+    arc_len = arc.nbytes
+    # correctness spot check of the warm-up output (bound + determinism)
+    err = 0.0
+    step_e = 1 << 28
+    for a in range(0, n, step_e):
+        err = max(err, (y[a:a + step_e].double() - x[a:a + step_e].double()).abs().max().item())
+    slack = float(np.spacing(np.float32(max(abs(field.vmin), abs(field.vmax))))) / 2
+    bound_ok = err <= hdr.eb_abs * (1 + 1e-12) + slack
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    torch.cuda.synchronize()
+    clocks.mark("t0")
+    t_c, t_d, profs = [], [], []
+    for _ in range(args.steps):
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        prof = []
+        e0.record()
+        arc = lzb.compress_device(field, eb, prof=prof)
+        e1.record()
+        pre = arc.data[: arc.header.symbols[0] + 32].cpu().numpy().tobytes()
+        y, _, _, _ = lzb.decompress_device(arc.data, raw_host=pre, prof=prof, out=ybuf)
+        e2.record()
+        torch.cuda.synchronize()
+        t_c.append(e0.elapsed_time(e1) / 1e3)
+        t_d.append(e1.elapsed_time(e2) / 1e3)
+        profs.append(prof)
+    torch.cuda.synchronize()
+    clocks.mark("t1")
+    clk = clocks.stop()
+    tc, td = statistics.mean(t_c), statistics.mean(t_d)
+    t_step = tc + td
+
+    # per-stage device times (CUDA events on the launching stream)
+    stage = {}
+    for prof in profs:
+        for name, a, b in prof:
+            stage.setdefault(name, []).append(a.elapsed_time(b) / 1e3)
+    stage_ms = {k: round(statistics.mean(v) * 1e3, 4) for k, v in stage.items()}
+    bits_bytes = hdr.symbols[1] - 16 if hdr.workflow is lzb.Workflow.HUFFMAN else hdr.symbols[1]
+    dom = max((k for k in stage if stage_bytes(k, n, s, bits_bytes, hdr.outlier_count)),
+              key=lambda k: statistics.mean(stage[k]))
+    peak, peak_kind = measured_peak_hbm()
+    dom_bytes = stage_bytes(dom, n, s, bits_bytes, hdr.outlier_count)
+    achieved = dom_bytes / statistics.mean(stage[dom]) / 1e9
+    per_stage_roofline = {}
+    for k in stage:
+        b = stage_bytes(k, n, s, bits_bytes, hdr.outlier_count)
+        if b:
+            a = b / statistics.mean(stage[k]) / 1e9
+            per_stage_roofline[k] = {"achieved_gbs": round(a, 1), "frac": round(a / peak, 4),
+                                     "bytes": b}
+    pipe_c = (nbytes + arc_len) / tc / 1e9
+    pipe_d = (arc_len + nbytes) / td / 1e9
+
+    # ---- e2e: host (pinned) buffers through the public device API ----
+    e2e = None
+    if args.e2e_steps > 0:
+        xh = torch.empty(n, dtype=x.dtype, pin_memory=True)
+        xh.copy_(x)
+        ah = torch.empty(arc_len + 4096, dtype=torch.uint8, pin_memory=True)
+        yh = torch.empty(n, dtype=x.dtype, pin_memory=True)
+        xd = torch.empty_like(x)
+        ad = torch.empty(arc_len + 4096, dtype=torch.uint8, device=dev)
+        fld = lzb.Field(field.dims, xd, field.vmin, field.vmax)
+        times = []
+        for k in range(args.e2e_steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            xd.copy_(xh, non_blocking=True)
+            a = lzb.compress_device(fld, eb)
+            ah[: a.nbytes].copy_(a.data, non_blocking=True)
+            ad[: a.nbytes].copy_(ah[: a.nbytes], non_blocking=True)
+            pre = ah[: a.header.symbols[0] + 32].numpy().tobytes()
+            yy, _, _, _ = lzb.decompress_device(ad[: a.nbytes], raw_host=pre, out=ybuf)
+            yh.copy_(yy, non_blocking=True)
+            torch.cuda.synchronize()
+            if k:  # first pass warms the pinned paths
+                times.append(time.perf_counter() - t0)
+        te = statistics.mean(times)
+        e2e = {"value": round(nbytes / te / 1e9, 4), "unit": "GB/s",
+               "h2d_bytes_per_step": nbytes + arc_len, "d2h_bytes_per_step": arc_len + nbytes,
+               "ms_per_step": round(te * 1e3, 2), "steps": args.e2e_steps}
+        del xh, ah, yh, xd, ad
+
+    # ---- CPU baseline: oracle port, 1 thread, bounded sub-slab ----
+    cpu = None
+    if not args.no_cpu_baseline:
+        planes = sample_planes_for(cfg, args.cpu_sample_elems)
+        vals, shp = gen_sample_host(cfg, planes)
+        tc0, td0, alen = cpu_oracle_run(vals, dims_tuple(shp), eb, 1)
+        cpu = {"value": round(vals.nbytes / (tc0 + td0) / 1e9, 6), "unit": "GB/s", "cores": 1,
+               "kind": "port",
+               "sample": f"{'x'.join(map(str, shp[::-1]))} sub-slab of the workload "
+                         f"({vals.size} elements), compress {tc0:.2f}s + decompress {td0:.2f}s"}
+
+    line = {
+        "metric": METRIC, "value": round(nbytes / t_step / 1e9, 3), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t_step * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "elements": n, "bytes": nbytes,
+                   "workflow": hdr.workflow.name, "l2": "inputs 34 GB >> 126 MB L2 (no flush)",
+                   "parallelism": f"slab{world}" if world > 1 else "single"},
+        "compress_gbs": round(nbytes / tc / 1e9, 3),
+        "decompress_gbs": round(nbytes / td / 1e9, 3),
+        "compress_ms": round(tc * 1e3, 3), "decompress_ms": round(td * 1e3, 3),
+        "compression_ratio": round(nbytes / arc_len, 4), "archive_bytes": arc_len,
+        "outliers": hdr.outlier_count,
+        "pipeline_roofline": {"compress_frac": round(pipe_c / peak, 4),
+                              "decompress_frac": round(pipe_d / peak, 4),
+                              "compress_gbs_alg": round(pipe_c, 1),
+                              "decompress_gbs_alg": round(pipe_d, 1),
+                              "bytes": "N*4 + |archive| per direction (SURVEY 8(d))"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": profiled_traffic(dom)},
+        "stages_ms": stage_ms, "stage_roofline": per_stage_roofline,
+        "bound_ok": bool(bound_ok), "max_abs_err": err, "eb_abs": hdr.eb_abs,
+        "gpu_launches": launches_per_step(hdr) * args.steps,
+        "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="lzb", choices=["lzb", "reference"])
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-elems", type=int, default=2048 * 2048 * 32)
+    ap.add_argument("--ref-sample-elems", type=int, default=2048 * 2048 * 16)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            torch.cuda.set_device(local_rank)
+        dist.init_process_group(backend)
+    try:
+        if args.impl == "reference":
+            run_reference(args, cfg, rank, world)
+        else:
+            run_gpu(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -157,6 +157,29 @@ def _dev(t):
     return t.data_ptr()
 
 
+class _Stage:
+    """CUDA-event bracket around one stage when profiling (bench.py); no-op otherwise."""
+
+    __slots__ = ("prof", "name", "ev")
+
+    def __init__(self, prof, name):
+        self.prof, self.name, self.ev = prof, name, None
+
+    def __enter__(self):
+        if self.prof is not None:
+            import torch
+
+            self.ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            self.ev[0].record()
+        return self
+
+    def __exit__(self, *exc):
+        if self.prof is not None and exc[0] is None:
+            self.ev[1].record()
+            self.prof.append((self.name, self.ev[0], self.ev[1]))
+        return False
+
+
 @dataclass
 class DeviceArchive:
     """An archive resident in device memory plus its decoded header."""
@@ -183,7 +206,7 @@ def _as_device_values(field: Field):
 
 def compress_device(field: Field, eb: float, eb_mode: str = "rel", cap: int = 1024,
                     workflow=None, chunk: ChunkSpec | None = None, select_mode: str = "exact",
-                    threads: int = 1, values=None) -> DeviceArchive:
+                    threads: int = 1, values=None, prof=None) -> DeviceArchive:
     """Compress to a device-resident archive (the timed region of bench.py).
 
     Same arguments and archive bytes as ``compress``; ``threads`` is accepted
@@ -215,12 +238,14 @@ def compress_device(field: Field, eb: float, eb_mode: str = "rel", cap: int = 10
         outl = _pool.get("outliers", cap_out * 16, dev)
         qs = L.lzb_quantize_scratch_bytes(g, cap_out)
         q_scr = _pool.get("q_scratch", qs, dev)
-        N.check_rc(L.lzb_quantize(_dev(x), _DTYPE_CODES[dt], g, eb_abs, cap, _dev(codes), cb,
-                                  _dev(hist), _dev(outl), cap_out, stp, _dev(q_scr), qs, sp),
-                   "quantize")
-        N.check_rc(L.lzb_codebook(_dev(hist), cap, _dev(lengths), _dev(cwords),
-                                  stp + N.STATUS_BYTES, _dev(cb_scr), cb_scr.numel(), sp),
-                   "codebook")
+        with _Stage(prof, "K1_quantize"):
+            N.check_rc(L.lzb_quantize(_dev(x), _DTYPE_CODES[dt], g, eb_abs, cap, _dev(codes), cb,
+                                      _dev(hist), _dev(outl), cap_out, stp, _dev(q_scr), qs, sp),
+                       "quantize")
+        with _Stage(prof, "K2_codebook"):
+            N.check_rc(L.lzb_codebook(_dev(hist), cap, _dev(lengths), _dev(cwords),
+                                      stp + N.STATUS_BYTES, _dev(cb_scr), cb_scr.numel(), sp),
+                       "codebook")
         sq, sb = N.read_status(st[: 2 * N.STATUS_BYTES])  # sync 1
         if sq.code == N.LZB_E_CAPACITY:
             cap_out = sq.u[0] + 1024
@@ -260,9 +285,11 @@ def compress_device(field: Field, eb: float, eb_mode: str = "rel", cap: int = 10
         _h2d(arc, sym_off, struct.pack("<QQ", bits, n))
         es = L.lzb_huff_encode_scratch_bytes(n)
         e_scr = _pool.get("e_scratch", es, dev)
-        N.check_rc(L.lzb_huff_encode(_dev(codes), cb, n, _dev(lengths), _dev(cwords), cap,
-                                     _dev(arc) + sym_off + 16, nbytes, stp + 2 * N.STATUS_BYTES,
-                                     _dev(e_scr), es, sp), "huff_encode")
+        with _Stage(prof, "K3_huff_encode"):
+            N.check_rc(L.lzb_huff_encode(_dev(codes), cb, n, _dev(lengths), _dev(cwords), cap,
+                                         _dev(arc) + sym_off + 16, nbytes,
+                                         stp + 2 * N.STATUS_BYTES, _dev(e_scr), es, sp),
+                       "huff_encode")
         check_slots = [2]
     else:
         extra = n // _MAX_RUN + 1 if n > _MAX_RUN else 0
@@ -332,8 +359,9 @@ def compress_device(field: Field, eb: float, eb_mode: str = "rel", cap: int = 10
     for a, b in pads:
         if b > a:
             arc[a:b].zero_()
-    if n_out:
-        arc[out_off: out_off + 16 * n_out].copy_(outl[: 16 * n_out])
+    with _Stage(prof, "assemble"):
+        if n_out:
+            arc[out_off: out_off + 16 * n_out].copy_(outl[: 16 * n_out])
     final = N.read_status(st[: 8 * N.STATUS_BYTES])  # sync: encode status
     for k in check_slots:
         N.raise_for(final[k], "encode")
@@ -364,16 +392,16 @@ def compress(field: Field, eb: float, eb_mode: str = "rel", cap: int = 1024, wor
                            threads).to_bytes()
 
 
-def parse_header(raw) -> ArchiveHeader:
+def parse_header(raw, total: int | None = None) -> ArchiveHeader:
     """Validate and decode an archive header + section table (P/pipeline.py:224-272).
 
-    ``raw`` is ``bytes`` or a device uint8 tensor (only 130 bytes are read back).
+    ``raw`` is ``bytes`` or a device uint8 tensor (only 130 bytes are read back);
+    ``total`` overrides the archive length when ``raw`` is only a prefix.
     """
-    total = None
     if not isinstance(raw, (bytes, bytearray, memoryview)):
-        total = raw.numel()
-        raw = raw[: min(total, _HEADER.size)].cpu().numpy().tobytes()
-    else:
+        total = raw.numel() if total is None else total
+        raw = raw[: min(raw.numel(), _HEADER.size)].cpu().numpy().tobytes()
+    elif total is None:
         total = len(raw)
     if len(raw) < _HEADER.size:
         raise CorruptArchiveError("archive shorter than its header")
@@ -428,7 +456,7 @@ def _validate_lengths_host(cb: np.ndarray) -> int:
     return mx
 
 
-def decompress_device(arc, raw_host: bytes | None = None):
+def decompress_device(arc, raw_host: bytes | None = None, prof=None, out=None):
     """Decode a device archive tensor; returns (values CUDA tensor, header, vmin, vmax).
 
     ``raw_host`` (optional) is the same archive on the host, used for the
@@ -437,11 +465,10 @@ def decompress_device(arc, raw_host: bytes | None = None):
     """
     import torch
 
-    hdr = parse_header(raw_host if raw_host is not None else arc)
-    total = arc.numel()
+    hdr = parse_header(raw_host if raw_host is not None else arc, total=arc.numel())
 
     def host_bytes(a: int, b: int) -> bytes:
-        if raw_host is not None:
+        if raw_host is not None and b <= len(raw_host):
             return bytes(raw_host[a:b])
         return arc[a:b].cpu().numpy().tobytes()
 
@@ -470,9 +497,10 @@ def decompress_device(arc, raw_host: bytes | None = None):
             raise CorruptArchiveError("decoded stream length does not match the grid")
         ds = L.lzb_huff_decode_scratch_bytes(bit_len, maxlen, cap)
         d_scr = _pool.get("d_scratch", ds, dev)
-        N.check_rc(L.lzb_huff_decode(base + sym_off + 16, bit_len, count, base + hdr.codebook[0],
-                                     cap, maxlen, _dev(codes), cb, stp, _dev(d_scr), ds, sp),
-                   "huff_decode")
+        with _Stage(prof, "K5_huff_decode"):
+            N.check_rc(L.lzb_huff_decode(base + sym_off + 16, bit_len, count,
+                                         base + hdr.codebook[0], cap, maxlen, _dev(codes), cb,
+                                         stp, _dev(d_scr), ds, sp), "huff_decode")
     else:
         if sym_len < 8:
             raise CorruptArchiveError("run section shorter than its count")
@@ -507,13 +535,15 @@ def decompress_device(arc, raw_host: bytes | None = None):
                                     stp + N.STATUS_BYTES, _dev(r_scr), rs, sp), "rle_decode")
     out_off, out_len = hdr.outliers
     dtn = torch.float32 if hdr.dtype == "f32" else torch.float64
-    y = torch.empty(n, dtype=dtn, device=dev)
+    y = out if out is not None else torch.empty(n, dtype=dtn, device=dev)
     g = N.geom(dims.as_tuple(), chunk.as_tuple())
     rcs = L.lzb_reconstruct_scratch_bytes(g, hdr.outlier_count)
     rc_scr = _pool.get("rc_scratch", rcs, dev)
-    N.check_rc(L.lzb_reconstruct(_dev(codes), cb, base + out_off, hdr.outlier_count, g,
-                                 hdr.eb_abs, cap, y.data_ptr(), _DTYPE_CODES[hdr.dtype], None,
-                                 stp + 2 * N.STATUS_BYTES, _dev(rc_scr), rcs, sp), "reconstruct")
+    with _Stage(prof, "K6_reconstruct"):
+        N.check_rc(L.lzb_reconstruct(_dev(codes), cb, base + out_off, hdr.outlier_count, g,
+                                     hdr.eb_abs, cap, y.data_ptr(), _DTYPE_CODES[hdr.dtype], None,
+                                     stp + 2 * N.STATUS_BYTES, _dev(rc_scr), rcs, sp),
+                   "reconstruct")
     sd, sr, sk = N.read_status(st[: 3 * N.STATUS_BYTES])  # the one sync
     N.raise_for(sd, "decode", "bit stream does not decode to its declared symbols")
     N.raise_for(sr, "rle_decode", "run section does not decode to the grid")
