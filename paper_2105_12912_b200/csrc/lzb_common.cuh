@@ -104,6 +104,42 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t *status, uint64_t til
     return excl;
 }
 
+// Split form for deferred resolution: publish the aggregate as soon as it is
+// known, do other work, then resolve (by then predecessors have usually
+// published, so the look-back rarely spins).
+__device__ __forceinline__ void lb_publish(uint64_t *status, uint64_t tile, uint64_t agg) {
+    if (lane_id() == 0) lb_store(&status[tile], (tile == 0 ? kLbInc : kLbAgg) | agg);
+}
+
+// Called by one full warp after lb_publish(tile, agg); returns the exclusive
+// prefix and publishes the inclusive one.
+__device__ __forceinline__ uint64_t lb_resolve(uint64_t *status, uint64_t tile, uint64_t agg) {
+    const uint32_t lane = lane_id();
+    if (tile == 0) return 0;
+    uint64_t excl = 0;
+    int64_t base = (int64_t)tile - 1;
+    while (true) {
+        int64_t idx = base - (int64_t)lane;
+        uint64_t v = (idx >= 0) ? lb_load(&status[idx]) : (kLbInc | 0ull);
+        while (__any_sync(0xffffffffu, (v >> 62) == 0)) {
+            if ((v >> 62) == 0) v = lb_load(&status[idx]);
+        }
+        uint32_t inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        uint64_t val = v & kLbMask;
+        if (inc) {
+            uint32_t first = __ffs(inc) - 1;
+            if (lane > first) val = 0;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        excl += val;
+        if (inc) break;
+        base -= 32;
+    }
+    if (lane == 0) lb_store(&status[tile], kLbInc | (excl + agg));
+    return excl;
+}
+
 // Block-wide exclusive scan of one u32 per thread (blockDim multiple of 32,
 // <= 1024).  `warp_sums` needs 33 entries of shared memory.  Returns the
 // exclusive prefix; *total receives the block total.

@@ -23,6 +23,7 @@
 #include <type_traits>
 
 #include "lzb_common.cuh"
+#include "lzb_quant3d.cuh"
 
 namespace lzb {
 
@@ -556,6 +557,7 @@ static bool box_mode_ok(const Geom &g, uint32_t *K) {
 
 struct QuantLayout {
     uint64_t ntiles;
+    bool fast3d;
     bool box;
     uint32_t K;
     uint64_t tiles_per_row;
@@ -576,6 +578,12 @@ static QuantLayout quant_layout(const Geom &g) {
     }
     L.nrows_grid = g.ny * g.nz;
     L.nrows_chunk = g.nby * g.nbz;
+    L.fast3d = g.cx == 8 && g.cy == 8 && g.cz == 8;
+    if (L.fast3d) {
+        uint64_t nch = g.nbx * g.nby * g.nbz;
+        uint64_t nt = (nch + kQ3TileChunks - 1) / kQ3TileChunks;
+        if (nt > L.ntiles) L.ntiles = nt;
+    }
     return L;
 }
 
@@ -592,6 +600,13 @@ static void quant_scratch(S &s, const QuantLayout &L, uint64_t cap_out) {
     s.template take<uint32_t>(L.ntiles);                 // tile first code
     s.template take<uint32_t>(L.ntiles);                 // tile last code
     s.template take<unsigned long long>(1);              // inner heads
+    if (L.fast3d) {
+        s.template take<uint64_t>(L.ntiles * 2 * kQ3Slot);  // record slots
+        s.template take<uint32_t>(L.ntiles);                // tile counts
+        s.template take<uint32_t>(L.ntiles);                // overflow list
+        s.template take<uint64_t>(L.ntiles);                // tile offsets
+        s.template take<uint64_t>((L.ntiles + 2047) / 2048 + 1);  // scan look-back
+    }
 }
 
 static int device_sms() {
@@ -657,6 +672,17 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
     uint32_t *tlast = sc.take<uint32_t>(L.ntiles);
     unsigned long long *inner = sc.take<unsigned long long>(1);
     if (!inner) return LZB_E_ARG;
+    uint64_t *slots = nullptr, *tile_off = nullptr, *slb = nullptr;
+    uint32_t *tile_cnt = nullptr, *over_list = nullptr;
+    if (L.fast3d) {
+        slots = sc.take<uint64_t>(L.ntiles * 2 * kQ3Slot);
+        tile_cnt = sc.take<uint32_t>(L.ntiles);
+        over_list = sc.take<uint32_t>(L.ntiles);
+        tile_off = sc.take<uint64_t>(L.ntiles);
+        slb = sc.take<uint64_t>((L.ntiles + 2047) / 2048 + 1);
+        if (!slb) return LZB_E_ARG;
+        LZB_CUDA_TRY(cudaMemsetAsync(slb, 0, ((L.ntiles + 2047) / 2048 + 1) * sizeof(uint64_t), s));
+    }
     LZB_CUDA_TRY(cudaMemsetAsync(inner, 0, sizeof(unsigned long long), s));
 
     LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
@@ -686,6 +712,76 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
     qp.inner_heads = inner;
 
     int rc;
+    if (L.fast3d && dtype != 2) {
+        Q3Params q3;
+        q3.x = x;
+        q3.g = g;
+        q3.two_eb = 2.0 * eb_abs;
+        q3.inv = 1.0 / (2.0 * eb_abs);
+        q3.inv_hi = (float)q3.inv;
+        q3.inv_lo = (float)(q3.inv - (double)q3.inv_hi);
+        q3.slack = eb_abs * (1.0 + 1e-12);
+        q3.r = (int32_t)(cap / 2);
+        q3.cap = cap;
+        q3.codes = codes;
+        q3.hist = reinterpret_cast<unsigned long long *>(hist);
+        q3.records = outliers;
+        q3.out_capacity = outliers ? out_capacity : 0;
+        q3.st = st;
+        q3.lb = lb;
+        q3.ticket = &tick[0];
+        q3.nchunks = g.nbx * g.nby * g.nbz;
+        q3.ntiles = (q3.nchunks + kQ3TileChunks - 1) / kQ3TileChunks;
+        q3.tfirst = tfirst;
+        q3.tlast = tlast;
+        q3.inner_heads = inner;
+        q3.slots = slots;
+        q3.tile_cnt = tile_cnt;
+        q3.over_list = over_list;
+        q3.n_over = &tick[3];
+        q3.tile_off = tile_off;
+        const size_t esz = dtype == 0 ? 4 : 8;
+        q3.vec_ok = (g.nx % (16 / esz) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+        size_t smem = (size_t)kQ3Warps * 512 * code_bytes + (size_t)cap * 4;
+        auto launch = [&](auto kern) -> int {
+            LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int per_sm = 0;
+            LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQ3Threads, smem));
+            if (per_sm < 1) per_sm = 1;
+            uint64_t grid = umin64((uint64_t)device_sms() * per_sm, (q3.ntiles + kQ3Warps - 1) / kQ3Warps);
+            kern<<<(unsigned)(grid ? grid : 1), kQ3Threads, smem, s>>>(q3);
+            LZB_LAUNCH_CHECK();
+            return LZB_OK;
+        };
+        if (dtype == 0)
+            rc = code_bytes == 2 ? launch(k_quantize3d8<float, uint16_t>) : launch(k_quantize3d8<float, uint32_t>);
+        else
+            rc = code_bytes == 2 ? launch(k_quantize3d8<double, uint16_t>) : launch(k_quantize3d8<double, uint32_t>);
+        if (rc) return rc;
+        k_count_runs<<<1, 1024, 0, s>>>(tfirst, tlast, q3.ntiles, inner, st);
+        LZB_LAUNCH_CHECK();
+        // phase 2: tile offsets, slot compaction, overflow re-emission
+        const int sms = device_sms();
+        k_q3_scan<<<(unsigned)umin64((q3.ntiles + 2047) / 2048, (uint64_t)sms * 4), 256, 0, s>>>(
+            q3, tile_off, slb, &tick[2]);
+        LZB_LAUNCH_CHECK();
+        if (outliers && out_capacity) {
+            k_q3_compact<<<(unsigned)umin64((q3.ntiles * 32 + 255) / 256, (uint64_t)sms * 16), 256, 0, s>>>(q3);
+            LZB_LAUNCH_CHECK();
+            size_t esm = (size_t)kQ3Warps * 512 * code_bytes;
+            if (dtype == 0) {
+                if (code_bytes == 2) k_q3_emit<float, uint16_t><<<sms, kQ3Threads, esm, s>>>(q3);
+                else k_q3_emit<float, uint32_t><<<sms, kQ3Threads, esm, s>>>(q3);
+            } else {
+                if (code_bytes == 2) k_q3_emit<double, uint16_t><<<sms, kQ3Threads, esm, s>>>(q3);
+                else k_q3_emit<double, uint32_t><<<sms, kQ3Threads, esm, s>>>(q3);
+            }
+            LZB_LAUNCH_CHECK();
+        }
+        LZB_CUDA_TRY(cudaMemsetAsync(&tick[2], 0, sizeof(unsigned int), s));  // reused below
+        rc = LZB_OK;
+        goto order;
+    }
     if (dtype == 2) {
         if (L.box)
             rc = code_bytes == 2 ? launch_quant<int64_t, uint16_t, true>(qp, s)
@@ -711,6 +807,7 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
     if (rc) return rc;
     k_count_runs<<<1, 1024, 0, s>>>(tfirst, tlast, L.ntiles, inner, st);
     LZB_LAUNCH_CHECK();
+order:
     if (!outliers || out_capacity == 0) return LZB_OK;
 
     // ---- global row-major ordering of the outlier records ----
