@@ -22,6 +22,7 @@
 // reduction.  Prefix sums along different axes commute, so the order of the
 // three passes does not matter for the (exact integer) result.
 #include "lzb_common.cuh"
+#include "lzb_recon3d.cuh"
 
 namespace lzb {
 
@@ -299,6 +300,7 @@ __global__ void __launch_bounds__(kRcThreads) k_reconstruct(RcParams p) {
 struct OutParams {
     const uint8_t *rec;  // 16-byte LE records, any alignment
     uint64_t n_out;
+    int fast3d;          // tiles = 8 consecutive chunk ordinals (K6 fast path)
     Geom g;
     uint32_t K;
     uint64_t tiles_per_row;
@@ -323,6 +325,11 @@ __device__ __forceinline__ uint64_t tile_of(const OutParams &p, uint64_t idx, ui
     uint64_t x = idx % g.nx, yz = idx / g.nx;
     uint64_t y = yz % g.ny, z = yz / g.ny;
     uint64_t bx = x / g.cx, by = y / g.cy, bz = z / g.cz;
+    if (p.fast3d) {
+        uint64_t ord = bx + g.nbx * (by + g.nby * bz);
+        *boxpos = (uint32_t)(((ord & 7) << 9) | ((z & 7) << 6) | ((y & 7) << 3) | (x & 7));
+        return ord >> 3;
+    }
     uint64_t j = bx / p.K;
     uint64_t t = (bz * g.nby + by) * p.tiles_per_row + j;
     uint64_t X0 = j * p.K * g.cx;
@@ -589,6 +596,7 @@ static int nsms() {
 }
 
 struct RcLayout {
+    bool fast3d;
     bool box;
     uint32_t K;
     uint64_t tiles_per_row, ntiles;
@@ -597,6 +605,14 @@ struct RcLayout {
 static RcLayout rc_layout(const Geom &g) {
     RcLayout L;
     uint64_t vol = g.cx * g.cy * g.cz;
+    L.fast3d = g.cx == 8 && g.cy == 8 && g.cz == 8;
+    if (L.fast3d) {
+        L.box = true;
+        L.K = 0;
+        L.tiles_per_row = 0;
+        L.ntiles = (g.nbx * g.nby * g.nbz + kR3TileChunks - 1) / kR3TileChunks;
+        return L;
+    }
     L.box = vol >= 1 && vol <= (uint64_t)kRcTile;
     if (L.box) {
         L.K = (uint32_t)(kRcTile / vol);
@@ -671,6 +687,7 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
         OutParams op;
         op.rec = outliers;
         op.n_out = n_out;
+        op.fast3d = L.fast3d;
         op.g = g;
         op.K = L.K;
         op.tiles_per_row = L.tiles_per_row;
@@ -691,6 +708,46 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
         if (n_out) {
             k_out_scatter<<<go, 256, 0, s>>>(op);
             LZB_LAUNCH_CHECK();
+        }
+        if (L.fast3d) {
+            R3Params r3;
+            r3.codes = codes;
+            r3.g = g;
+            r3.two_eb = 2.0 * eb_abs;
+            r3.r = (int32_t)(cap / 2);
+            r3.y = y;
+            r3.pre = prequant_out;
+            r3.st = st;
+            r3.mm = mm;
+            r3.nchunks = g.nbx * g.nby * g.nbz;
+            r3.ntiles = L.ntiles;
+            r3.tile_start = tile_start;
+            r3.brec = brec;
+            r3.ticket = &tick[1];
+            const size_t osz = dtype == 0 ? 4 : 8;
+            r3.vec_ok = (g.nx % (16 / osz) == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
+            auto launch = [&](auto kern) -> int {
+                int per_sm = 0;
+                LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kR3Threads, 0));
+                if (per_sm < 1) per_sm = 1;
+                uint64_t grid = umin64((uint64_t)sm * per_sm, (L.ntiles + kR3Warps - 1) / kR3Warps);
+                kern<<<(unsigned)(grid ? grid : 1), kR3Threads, 0, s>>>(r3);
+                LZB_LAUNCH_CHECK();
+                return LZB_OK;
+            };
+            int rc;
+            if (code_bytes == 2)
+                rc = dtype == 0 ? launch(k_reconstruct3d8<uint16_t, float>) : launch(k_reconstruct3d8<uint16_t, double>);
+            else
+                rc = dtype == 0 ? launch(k_reconstruct3d8<uint32_t, float>) : launch(k_reconstruct3d8<uint32_t, double>);
+            if (rc) return rc;
+            unsigned gf = (unsigned)umin64((n + 255) / 256, (uint64_t)sm * 8);
+            if (dtype == 0) k_first_nonfinite<float><<<gf, 256, 0, s>>>((const float *)y, n, mm);
+            else k_first_nonfinite<double><<<gf, 256, 0, s>>>((const double *)y, n, mm);
+            LZB_LAUNCH_CHECK();
+            k_rc_finish<<<1, 1, 0, s>>>(st, mm);
+            LZB_LAUNCH_CHECK();
+            return LZB_OK;
         }
         RcParams rp;
         rp.codes = codes;

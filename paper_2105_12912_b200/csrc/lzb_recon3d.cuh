@@ -1,0 +1,230 @@
+// K6 fast path for ChunkSpec(8,8,8): one warp per chunk, eight consecutive
+// chunk ordinals per warp task.  Included by lzb_recon.cu.  Semantics as the
+// generic K6 (P/reconstruct.py:22-88, P/pipeline.py:108-117); register layout
+// in lzb_fast3d.cuh.
+//
+// Per chunk: the lane's two 8-symbol rows are one 16-byte load each (the
+// chunk is 1 KB contiguous in the chunk-major stream), q' = code - r, the
+// chunk's outliers (bucketed per warp tile by a counting sort) are added, then
+// inclusive scans along x (in registers), y (3 shuffle steps inside 8-lane
+// groups) and z (in-lane pair + 2 shuffle steps), and the f64 dequantisation
+// feeds two 32-byte row stores in grid order plus a running min/max.
+// Values that might leave int32 (an outlier |delta| >= 2^20) send the chunk
+// to the exact int64 variant with the reference's f64 prefix-sum guard.
+#pragma once
+
+#include "lzb_fast3d.cuh"
+
+namespace lzb {
+
+constexpr int kR3Warps = 8;
+constexpr int kR3Threads = kR3Warps * 32;
+constexpr int kR3TileChunks = 8;
+
+struct R3Params {
+    const void *codes;
+    Geom g;
+    double two_eb;
+    int32_t r;
+    void *y;
+    int64_t *pre;             // optional int64 prequant output
+    lzb_dstatus *st;
+    unsigned long long *mm;   // [min key, max key, first bad offset]
+    uint64_t nchunks, ntiles;
+    const uint64_t *tile_start;  // ntiles + 1
+    const uint64_t *brec;        // per record: [k << 9 | lz << 6 | ly << 3 | lx, delta]
+    unsigned int *ticket;
+    int vec_ok;
+};
+
+__device__ __forceinline__ unsigned long long r3_dkey(double v) {
+    unsigned long long b = __double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+template <typename I>
+__device__ __forceinline__ void r3_add_outliers(const R3Params &p, uint64_t r0, uint64_t r1,
+                                                uint32_t k, uint32_t lane, I (&v0)[8], I (&v1)[8]) {
+    const uint32_t ly = lane & 7, lz0 = (lane >> 3) * 2;
+    for (uint64_t i = r0; i < r1; i++) {
+        const uint64_t key = p.brec[2 * i];
+        if ((uint32_t)(key >> 9) != k) continue;
+        const int64_t d = (int64_t)p.brec[2 * i + 1];
+        const uint32_t lx = key & 7, oy = (key >> 3) & 7, oz = (key >> 6) & 7;
+        if (oy != ly) continue;
+        if (oz == lz0) {
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if ((uint32_t)j == lx) v0[j] += (I)d;
+        } else if (oz == lz0 + 1) {
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if ((uint32_t)j == lx) v1[j] += (I)d;
+        }
+    }
+}
+
+// does any record of chunk k carry a delta too large for the int32 path?
+__device__ __forceinline__ bool r3_needs_wide(const R3Params &p, uint64_t r0, uint64_t r1, uint32_t k) {
+    bool wide = false;
+    for (uint64_t i = r0 + lane_id(); i < r1; i += 32) {
+        const uint64_t key = p.brec[2 * i];
+        const int64_t d = (int64_t)p.brec[2 * i + 1];
+        if ((uint32_t)(key >> 9) == k && (d >= (1ll << 20) || d <= -(1ll << 20))) wide = true;
+    }
+    return __any_sync(f3::kFull, wide);
+}
+
+template <typename SymT, typename OutT, typename I>
+__device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch, uint32_t k,
+                                         uint64_t r0, uint64_t r1, uint32_t lane, OutT &vmin,
+                                         OutT &vmax, bool &overflow) {
+    const uint32_t ly = lane & 7, lz0 = (lane >> 3) * 2;
+    const SymT *cs = static_cast<const SymT *>(p.codes) + ch.base;
+    I v0[8], v1[8];
+    const uint32_t xmask = (1u << ch.ex) - 1u;
+    const uint32_t m0 = (ly < ch.ey && lz0 < ch.ez) ? xmask : 0u;
+    const uint32_t m1 = (ly < ch.ey && lz0 + 1 < ch.ez) ? xmask : 0u;
+    const bool fast = ch.full && ((ch.base & 7) == 0);
+    if (fast) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            I(&v)[8] = h ? v1 : v0;
+            const SymT *src = cs + 8 * (ly + 8 * (lz0 + h));
+            if constexpr (sizeof(SymT) == 2) {
+                uint4 a = __ldg(reinterpret_cast<const uint4 *>(src));
+                uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    v[2 * j] = (I)(int32_t)(w[j] & 0xFFFFu) - p.r;
+                    v[2 * j + 1] = (I)(int32_t)(w[j] >> 16) - p.r;
+                }
+            } else {
+                uint4 a = __ldg(reinterpret_cast<const uint4 *>(src));
+                uint4 b = __ldg(reinterpret_cast<const uint4 *>(src) + 1);
+                uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+                for (int j = 0; j < 8; j++) v[j] = (I)(int64_t)w[j] - p.r;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            v0[j] = ((m0 >> j) & 1u) ? (I)(int64_t)cs[f3::lpos(ch, j, ly, lz0)] - p.r : (I)0;
+            v1[j] = ((m1 >> j) & 1u) ? (I)(int64_t)cs[f3::lpos(ch, j, ly, lz0 + 1)] - p.r : (I)0;
+        }
+    }
+    if (r1 > r0) r3_add_outliers<I>(p, r0, r1, k, lane, v0, v1);
+    if constexpr (sizeof(I) == 8) {
+        // prefix-sum magnitude guard (P/reconstruct.py:48-53), f64 sum per chunk
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) s += fabs((double)v0[j]) + fabs((double)v1[j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(f3::kFull, s, o);
+        if (s >= 4611686018427387904.0) overflow = true;
+    }
+    f3::psums<I>(v0, v1, lane);
+    OutT *yo = static_cast<OutT *>(p.y);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const I(&v)[8] = h ? v1 : v0;
+        const uint32_t mm = h ? m1 : m0;
+        const uint64_t gi = ch.x0 + p.g.nx * ((ch.y0 + ly) + p.g.ny * (ch.z0 + lz0 + h));
+        OutT o[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            o[j] = (OutT)__dmul_rn((double)v[j], p.two_eb);
+            if ((mm >> j) & 1u) {
+                vmin = o[j] < vmin ? o[j] : vmin;
+                vmax = o[j] > vmax ? o[j] : vmax;
+            }
+        }
+        if (fast && p.vec_ok) {
+            if constexpr (sizeof(OutT) == 4) {
+                float4 *dst = reinterpret_cast<float4 *>(yo + gi);
+                dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+                dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+            } else {
+                double2 *dst = reinterpret_cast<double2 *>(yo + gi);
+#pragma unroll
+                for (int j = 0; j < 4; j++) dst[j] = make_double2(o[2 * j], o[2 * j + 1]);
+            }
+            if (p.pre)
+#pragma unroll
+                for (int j = 0; j < 8; j++) p.pre[gi + j] = (int64_t)v[j];
+        } else if (mm) {
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if ((mm >> j) & 1u) {
+                    yo[gi + j] = o[j];
+                    if (p.pre) p.pre[gi + j] = (int64_t)v[j];
+                }
+        }
+    }
+}
+
+template <typename SymT, typename OutT>
+__device__ __noinline__ void r3_chunk_wide(const R3Params *pp, uint64_t c, uint32_t k, uint64_t r0,
+                                           uint64_t r1, uint32_t lane, OutT *mm, bool *ovf) {
+    const f3::Chunk ch = f3::chunk_of(pp->g, c);
+    OutT vmin = mm[0], vmax = mm[1];
+    bool o = *ovf;
+    r3_chunk<SymT, OutT, int64_t>(*pp, ch, k, r0, r1, lane, vmin, vmax, o);
+    mm[0] = vmin;
+    mm[1] = vmax;
+    *ovf = o;
+}
+
+template <typename SymT, typename OutT>
+__global__ void __launch_bounds__(kR3Threads, 2) k_reconstruct3d8(const __grid_constant__ R3Params p) {
+    const uint32_t lane = lane_id();
+    OutT vmin = (OutT)INFINITY, vmax = (OutT)-INFINITY;
+    bool overflow = false;
+    while (true) {
+        uint64_t t = 0;
+        if (lane == 0) t = atomicAdd(p.ticket, 1u);
+        t = __shfl_sync(f3::kFull, t, 0);
+        if (t >= p.ntiles) break;
+        const uint64_t c0 = t * kR3TileChunks;
+        const uint64_t c1 = umin64(c0 + kR3TileChunks, p.nchunks);
+        const uint64_t r0 = p.tile_start[t], r1 = p.tile_start[t + 1];
+        for (uint64_t c = c0; c < c1; c++) {
+            const uint32_t k = (uint32_t)(c - c0);
+            if (r1 > r0 && r3_needs_wide(p, r0, r1, k)) {
+                OutT mmv[2] = {vmin, vmax};
+                r3_chunk_wide<SymT, OutT>(&p, c, k, r0, r1, lane, mmv, &overflow);
+                vmin = mmv[0];
+                vmax = mmv[1];
+            } else {
+                const f3::Chunk ch = f3::chunk_of(p.g, c);
+                r3_chunk<SymT, OutT, int32_t>(p, ch, k, r0, r1, lane, vmin, vmax, overflow);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        OutT a = __shfl_xor_sync(f3::kFull, vmin, o), b = __shfl_xor_sync(f3::kFull, vmax, o);
+        vmin = a < vmin ? a : vmin;
+        vmax = b > vmax ? b : vmax;
+    }
+    if (lane == 0 && vmin <= vmax) {
+        atomicMin(&p.mm[0], r3_dkey((double)vmin));
+        atomicMax(&p.mm[1], r3_dkey((double)vmax));
+    }
+    if (__any_sync(f3::kFull, overflow) && lane == 0) set_status(p.st, LZB_E_OVERFLOW);
+}
+
+// Non-finite outputs are rare (an overflowing dequantisation).  The running
+// min/max already see any +-inf; only then does this pass look for the first
+// offending offset (the reference reports it, P/grid.py:176-180).
+template <typename OutT>
+__global__ void k_first_nonfinite(const OutT *y, uint64_t n, unsigned long long *mm) {
+    const unsigned long long kinf_lo = r3_dkey(-INFINITY), kinf_hi = r3_dkey(INFINITY);
+    if (mm[0] != kinf_lo && mm[1] != kinf_hi) return;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        if (!isfinite((double)y[i])) atomicMin(&mm[2], (unsigned long long)i);
+}
+
+}  // namespace lzb
