@@ -137,21 +137,23 @@ int lzb_codebook_from_lengths(const uint8_t *lengths, uint32_t cap, uint64_t *co
  * K3: Huffman bit packing (P/huffman.py:46-61).  Writes exactly
  * ceil(bit_len/8) bytes at `out` (MSB first, last byte zero padded); out
  * need not be aligned.  out_bytes must be >= ceil(bit_len/8) where bit_len =
- * sum(len(sym)) (known beforehand from lzb_codebook's u[0]).
+ * sum(len(sym)) (known beforehand from lzb_codebook's u[0]).  maxlen = the
+ * book's longest code word (lzb_codebook's u[2]; 0 = unknown, generic path).
  * st->u[0] = bit_len.  code = LZB_E_DATA if a symbol has no code word.
  * ------------------------------------------------------------------- */
 size_t lzb_huff_encode_scratch_bytes(uint64_t n);
 int lzb_huff_encode(const void *sym, int sym_bytes, uint64_t n, const uint8_t *lengths,
-                    const uint64_t *codes, uint32_t cap, uint8_t *out, uint64_t out_bytes,
-                    lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream);
+                    const uint64_t *codes, uint32_t cap, uint32_t maxlen, uint8_t *out,
+                    uint64_t out_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
+                    void *stream);
 
 /* Multi-GPU slab variant of lzb_huff_encode: the first bit lands at bit
  * `bit_offset` (0..7, MSB first) of out[0]; bits outside the slab are zero so
  * neighbouring slabs OR-merge their shared boundary byte. */
 int lzb_huff_encode_at(const void *sym, int sym_bytes, uint64_t n, const uint8_t *lengths,
-                       const uint64_t *codes, uint32_t cap, uint64_t bit_offset, uint8_t *out,
-                       uint64_t out_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
-                       void *stream);
+                       const uint64_t *codes, uint32_t cap, uint32_t maxlen, uint64_t bit_offset,
+                       uint8_t *out, uint64_t out_bytes, lzb_dstatus *st, void *scratch,
+                       size_t scratch_bytes, void *stream);
 
 /* ---------------------------------------------------------------------
  * K5: self-synchronising parallel Huffman decode of a dense MSB-first bit

@@ -61,123 +61,160 @@ __device__ __forceinline__ void store_word_bytes(uint8_t *out, uint64_t byte0, u
         if (byte0 + k < limit) out[byte0 + k] = (uint8_t)(be_word >> (24 - 8 * k));
 }
 
-template <typename SymT>
+// K3 kernel.  SHORT = every code word has <= 32 bits (the host passes the
+// book's max length; practically always true): the table is one u64 per
+// symbol (code | len << 32) and each code word is placed branch-free with one
+// or two shared-memory ORs.  !SHORT handles 33..64-bit code words generically.
+template <typename SymT, bool SHORT>
 __global__ void __launch_bounds__(kEThreads) k_huff_encode(EncParams p) {
     extern __shared__ __align__(16) unsigned char e_smem[];
-    uint64_t *s_codes = reinterpret_cast<uint64_t *>(e_smem);
-    uint8_t *s_lens = reinterpret_cast<uint8_t *>(s_codes + (p.table_smem ? p.cap : 0));
-    uint32_t *s_words = reinterpret_cast<uint32_t *>(
-        e_smem + (((p.table_smem ? p.cap * 9u : 0u) + 15u) & ~15u));
+    // [table: cap x u64 (code | len << 32) or cap x (u64 code + u8 len)][words]
+    uint64_t *s_tab = reinterpret_cast<uint64_t *>(e_smem);
+    uint8_t *s_lens = reinterpret_cast<uint8_t *>(s_tab + p.cap);
+    const size_t tbytes = p.table_smem ? (size_t)p.cap * 9 : 0;
+    uint32_t *s_words = reinterpret_cast<uint32_t *>(e_smem + ((tbytes + 15) & ~(size_t)15));
     __shared__ uint32_t s_scan[33];
     __shared__ uint64_t s_tile, s_excl;
-    const uint64_t *g_codes = p.table_smem ? s_codes : p.codes;
-    const uint8_t *g_lens = p.table_smem ? s_lens : p.lengths;
+    const uint64_t *tab = p.codes;
+    const uint8_t *lens = p.lengths;
     if (p.table_smem) {
         for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) {
-            s_codes[i] = p.codes[i];
-            s_lens[i] = p.lengths[i];
+            if (SHORT) s_tab[i] = (p.codes[i] & 0xFFFFFFFFull) | ((uint64_t)p.lengths[i] << 32);
+            else {
+                s_tab[i] = p.codes[i];
+                s_lens[i] = p.lengths[i];
+            }
         }
+        tab = s_tab;
+        lens = s_lens;
     }
     const uint32_t tid = threadIdx.x;
-    bool bad = false;
+    const uint32_t capm1 = p.cap - 1;
+    uint32_t bad = 0;
     while (true) {
         if (tid == 0) s_tile = atomicAdd(p.ticket, 1u);
         __syncthreads();
         const uint64_t t = s_tile;
         if (t >= p.ntiles) break;
         const uint64_t base = t * kETile + (uint64_t)tid * kESyms;
-        uint32_t s[kESyms];
+        uint32_t sy[kESyms];
         const SymT *sp = static_cast<const SymT *>(p.sym) + base;
-        if (base + kESyms <= p.n && sizeof(SymT) == 2 &&
-            (reinterpret_cast<uintptr_t>(sp) & 15) == 0) {
+        const bool fullv = base + kESyms <= p.n && sizeof(SymT) == 2 &&
+                           (reinterpret_cast<uintptr_t>(sp) & 15) == 0;
+        uint32_t nvalid = kESyms;
+        if (fullv) {
             uint4 a = reinterpret_cast<const uint4 *>(sp)[0];
             uint4 b = reinterpret_cast<const uint4 *>(sp)[1];
             uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
             for (int k = 0; k < 8; k++) {
-                s[2 * k] = w[k] & 0xFFFFu;
-                s[2 * k + 1] = w[k] >> 16;
+                sy[2 * k] = w[k] & 0xFFFFu;
+                sy[2 * k + 1] = w[k] >> 16;
             }
         } else {
+            nvalid = base >= p.n ? 0u : (uint32_t)umin64(kESyms, p.n - base);
 #pragma unroll
-            for (int k = 0; k < kESyms; k++) s[k] = base + k < p.n ? (uint32_t)sp[k] : 0xFFFFFFFFu;
+            for (int k = 0; k < kESyms; k++) sy[k] = (uint32_t)k < nvalid ? (uint32_t)sp[k] : 0u;
         }
+        uint32_t Ls[kESyms];
+        uint64_t Cs[kESyms];
         uint32_t nb = 0;
 #pragma unroll
         for (int k = 0; k < kESyms; k++) {
-            if (s[k] != 0xFFFFFFFFu) {
-                uint32_t L = s[k] < p.cap ? g_lens[s[k]] : 0u;
-                if (L == 0) bad = true;
-                nb += L;
+            const uint32_t sv = sy[k];
+            const uint32_t idx = sv < capm1 ? sv : capm1;
+            uint32_t L;
+            uint64_t c;
+            if (SHORT) {
+                const uint64_t e = tab[idx];
+                L = (uint32_t)(e >> 32);
+                c = (uint32_t)e;
+            } else {
+                L = lens[idx];
+                c = tab[idx];
             }
+            const bool v = (uint32_t)k < nvalid;
+            bad |= (uint32_t)(v && (sv > capm1 || L == 0));
+            L = v ? L : 0u;
+            Ls[k] = L;
+            Cs[k] = c;
+            nb += L;
         }
         uint32_t tile_bits;
-        uint32_t off = block_exclusive_scan<uint32_t>(nb, s_scan, &tile_bits);
+        const uint32_t off = block_exclusive_scan<uint32_t>(nb, s_scan, &tile_bits);
+        // publish the aggregate now; resolve after the packing work
+        if (tid == 0) lb_store(&p.lb[t], (t == 0 ? kLbInc : kLbAgg) | tile_bits);
+        const uint32_t nwords = (tile_bits + 31) >> 5;
+        for (uint32_t i = tid; i <= nwords + 1; i += kEThreads) s_words[i] = 0;
+        __syncthreads();
+        // pack at tile-relative bit offsets (phase 0)
+        uint32_t pos = off;
+#pragma unroll
+        for (int k = 0; k < kESyms; k++) {
+            const uint32_t L = Ls[k];
+            if (SHORT) {
+                const uint32_t w = pos >> 5, sh = pos & 31;
+                const uint32_t amt = 64u - sh - (L ? L : 1u);
+                const uint64_t v = L ? (Cs[k] << amt) : 0ull;
+                atomicOr(&s_words[w], (uint32_t)(v >> 32));
+                if (sh + L > 32) atomicOr(&s_words[w + 1], (uint32_t)v);
+            } else {
+                uint32_t rem = L, q = pos;
+                const uint64_t c = Cs[k];
+                while (rem) {
+                    const uint32_t sh = q & 31, take = (32 - sh) < rem ? (32 - sh) : rem;
+                    const uint32_t piece = (uint32_t)((c >> (rem - take)) & ((1ull << take) - 1ull));
+                    atomicOr(&s_words[q >> 5], piece << (32 - sh - take));
+                    rem -= take;
+                    q += take;
+                }
+            }
+            pos += L;
+        }
         if ((tid >> 5) == 0) {
-            uint64_t ex = lookback_warp(p.lb, t, tile_bits);
+            uint64_t ex = lb_resolve(p.lb, t, tile_bits);
             if (lane_id() == 0) s_excl = ex;
         }
         __syncthreads();
-        const uint64_t G = s_excl + p.bit_offset;  // absolute bit position of the tile
-        const uint32_t lead = (uint32_t)(G & 31);
+        // write out with the tile's bit phase: out word j = (w[j-1] << (32-s)) | (w[j] >> s)
+        const uint64_t G = s_excl + p.bit_offset;
+        const uint32_t sft = (uint32_t)(G & 31);
         const uint64_t wbase = G >> 5;
-        const uint32_t nwords = (lead + tile_bits + 31) >> 5;
-        for (uint32_t i = tid; i < nwords; i += kEThreads) s_words[i] = 0;
-        __syncthreads();
-        uint32_t pos = lead + off;
-#pragma unroll
-        for (int k = 0; k < kESyms; k++) {
-            if (s[k] == 0xFFFFFFFFu || s[k] >= p.cap) continue;
-            uint32_t L = g_lens[s[k]];
-            uint64_t c = g_codes[s[k]];
-            while (L > 0) {
-                uint32_t w = pos >> 5, b = pos & 31;
-                uint32_t room = 32 - b;
-                uint32_t take = L < room ? L : room;
-                uint32_t piece = (uint32_t)((c >> (L - take)) & ((1ull << take) - 1ull));
-                atomicOr(&s_words[w], piece << (room - take));
-                L -= take;
-                pos += take;
-            }
-        }
-        __syncthreads();
-        // words fully inside [G, G + tile_bits) are stored directly
         const uint64_t endbit = G + tile_bits;
+        const uint32_t nout = (uint32_t)(((endbit + 31) >> 5) - wbase);
         const bool aligned = (reinterpret_cast<uintptr_t>(p.out) & 3) == 0;
-        for (uint32_t i = tid; i < nwords; i += kEThreads) {
-            uint64_t gw = wbase + i;
-            bool full = (gw * 32 >= G) && (gw * 32 + 32 <= endbit);
-            if (!full) continue;
-            uint32_t v = s_words[i];
-            if (aligned)
-                reinterpret_cast<uint32_t *>(p.out)[gw] = bswap32(v);
-            else
-                store_word_bytes(p.out, gw * 4, v, ~0ull);
+        for (uint32_t j = tid; j < nout; j += kEThreads) {
+            const uint32_t cur = j < nwords ? s_words[j] : 0u;
+            const uint32_t prv = j > 0 ? s_words[j - 1] : 0u;
+            const uint32_t v = sft ? ((prv << (32 - sft)) | (cur >> sft)) : cur;
+            const uint64_t gw = wbase + j;
+            const bool full = (gw * 32 >= G) && (gw * 32 + 32 <= endbit);
+            if (full) {
+                if (aligned) reinterpret_cast<uint32_t *>(p.out)[gw] = bswap32(v);
+                else store_word_bytes(p.out, gw * 4, v, ~0ull);
+            } else if (j == 0 || j == nout - 1) {
+                // partial boundary words go to the fix-up pass
+                const bool head = (j == 0) && (sft != 0);
+                if (head) {
+                    p.frag[4 * t + 0] = gw;
+                    p.frag[4 * t + 1] = v;
+                }
+                if (j == nout - 1 && !(head && nout == 1)) {
+                    p.frag[4 * t + 2] = gw;
+                    p.frag[4 * t + 3] = v;
+                }
+            }
         }
         if (tid == 0) {
-            uint64_t hw = ~0ull, hb = 0, tw = ~0ull, tb = 0;
-            if (tile_bits > 0) {
-                if (lead != 0) {
-                    hw = wbase;
-                    hb = s_words[0];
-                }
-                if ((endbit & 31) != 0) {
-                    uint64_t last = (endbit - 1) >> 5;
-                    if (last != hw) {
-                        tw = last;
-                        tb = s_words[nwords - 1];
-                    }
-                }
-            }
-            p.frag[4 * t + 0] = hw;
-            p.frag[4 * t + 1] = hb;
-            p.frag[4 * t + 2] = tw;
-            p.frag[4 * t + 3] = tb;
+            const bool has_head = tile_bits > 0 && sft != 0;
+            const bool has_tail = tile_bits > 0 && (endbit & 31) != 0 && !(has_head && nout == 1);
+            if (!has_head) p.frag[4 * t + 0] = ~0ull;
+            if (!has_tail) p.frag[4 * t + 2] = ~0ull;
             if (t == p.ntiles - 1) p.st->u[0] = s_excl + tile_bits;
         }
         __syncthreads();
     }
-    if (__any_sync(0xffffffffu, bad) && lane_id() == 0) set_status(p.st, LZB_E_DATA);
+    if (__any_sync(0xffffffffu, bad != 0) && lane_id() == 0) set_status(p.st, LZB_E_DATA);
 }
 
 // Boundary words: each partial word is shared by at most the tail of tile t
@@ -214,13 +251,35 @@ constexpr int kMaxPaths = 4;
 constexpr uint32_t kMergeWin = 128;  // bits in which phases look for a merge
 
 struct DecTables {
-    uint32_t lut[kLutSize];  // (len << 20) | sym ; 0 = long code or invalid prefix
+    // Multi-symbol LUT on the next 12 bits: up to three complete code words
+    // greedily decoded from the window.  bits 0-1 count (0 = first code word
+    // longer than 12 bits or invalid prefix), 2-5/6-9/10-13 their lengths,
+    // 16-31/32-47/48-63 their symbols (books with cap > 65536 use count 0).
+    uint64_t lutm[kLutSize];
     uint64_t first[65];
     uint64_t cnt[65];
     uint32_t off[65];
     uint32_t maxlen;
     uint32_t nsym;
 };
+
+// The canonical tables for code words longer than the LUT, copied to shared
+// memory by each decode CTA.
+struct DecCanon {
+    uint64_t first[65];
+    uint64_t cnt[65];
+    uint32_t off[65];
+    uint32_t maxlen;
+};
+
+__device__ __forceinline__ void load_canon(DecCanon &c, const DecTables *t) {
+    for (uint32_t i = threadIdx.x; i < 65; i += blockDim.x) {
+        c.first[i] = t->first[i];
+        c.cnt[i] = t->cnt[i];
+        c.off[i] = t->off[i];
+    }
+    if (threadIdx.x == 0) c.maxlen = t->maxlen;
+}
 
 struct DecParams {
     const uint32_t *words;  // 4-byte aligned base covering the stream
@@ -290,15 +349,19 @@ struct BitReader {
     }
 };
 
+__device__ __forceinline__ uint32_t lm_count(uint64_t e) { return (uint32_t)(e & 3u); }
+__device__ __forceinline__ uint32_t lm_len(uint64_t e, int i) { return (uint32_t)(e >> (2 + 4 * i)) & 15u; }
+__device__ __forceinline__ uint32_t lm_sym(uint64_t e, int i) { return (uint32_t)(e >> (16 + 16 * i)) & 0xFFFFu; }
+
 // Decode one code word at the reader.  Returns len (0 = invalid), *sym.
-__device__ __forceinline__ uint32_t decode_one(const DecParams &p, const uint32_t *lut,
-                                               const DecTables *tab, BitReader &r, uint32_t &sym) {
-    uint32_t e = lut[r.buf >> (64 - kLutBits)];
-    if (e) {
-        sym = e & 0xFFFFFu;
-        return e >> 20;
+__device__ __forceinline__ uint32_t decode_one(const DecParams &p, const uint64_t *lutm,
+                                               const DecCanon *tab, BitReader &r, uint32_t &sym) {
+    const uint64_t e = lutm[r.buf >> (64 - kLutBits)];
+    if (lm_count(e)) {
+        sym = lm_sym(e, 0);
+        return lm_len(e, 0);
     }
-    // long code (or invalid prefix): canonical tables, reading 64 bits directly
+    // long code (> 12 bits) or invalid prefix: canonical tables on 64 peeked bits
     uint64_t v = (r.nb >= 64) ? r.buf : peek64(p, r.pos);
     for (uint32_t L = kLutBits + 1; L <= tab->maxlen; L++) {
         uint64_t c = v >> (64 - L);
@@ -321,7 +384,6 @@ __global__ void k_dec_tables(const uint8_t *lengths, uint32_t cap, uint32_t maxl
         s_bad = 0;
         s_max = 0;
     }
-    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) tab->lut[i] = 0;
     __syncthreads();
     for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
         uint32_t L = lengths[s];
@@ -382,20 +444,37 @@ __global__ void k_dec_tables(const uint8_t *lengths, uint32_t cap, uint32_t maxl
             uint32_t peers = __match_any_sync(0xffffffffu, L);
             uint32_t rank = __popc(peers & ((1u << lane) - 1u));
             uint32_t o = s_off[L];
-            if (s < cap && L) {
-                uint32_t idx = o + rank;
-                syms[idx] = s;
-                if (L <= (uint32_t)kLutBits) {
-                    uint64_t code = tab->first[L] + (idx - tab->off[L]);
-                    uint32_t lo = (uint32_t)(code << (kLutBits - L));
-                    uint32_t hi = lo + (1u << (kLutBits - L));
-                    for (uint32_t v = lo; v < hi; v++) tab->lut[v] = (L << 20) | s;
-                }
-            }
+            if (s < cap && L) syms[o + rank] = s;
             __syncwarp();
             if (L && lane == (uint32_t)(__ffs(peers) - 1)) s_off[L] = o + __popc(peers);
             __syncwarp();
         }
+    }
+    __syncthreads();
+    // multi-symbol LUT: greedy decode of up to three code words in 12 bits
+    for (uint32_t v = threadIdx.x; v < kLutSize; v += blockDim.x) {
+        uint64_t e = 0;
+        uint32_t used = 0, n = 0;
+        if (cap <= 65536) {
+            for (int i = 0; i < 3; i++) {
+                bool found = false;
+                for (uint32_t L = 1; L + used <= (uint32_t)kLutBits && L <= s_max; L++) {
+                    const uint32_t code = (v >> (kLutBits - used - L)) & ((1u << L) - 1u);
+                    const uint64_t f = tab->first[L], k = tab->cnt[L];
+                    if (k && code >= f && code - f < k) {
+                        const uint32_t sym = syms[tab->off[L] + (uint32_t)(code - f)];
+                        e |= (uint64_t)L << (2 + 4 * i);
+                        e |= (uint64_t)sym << (16 + 16 * i);
+                        used += L;
+                        n++;
+                        found = true;
+                        break;
+                    }
+                }
+                if (!found) break;
+            }
+        }
+        tab->lutm[v] = e | n;
     }
 }
 
@@ -420,10 +499,12 @@ __device__ __forceinline__ uint32_t bm_rank(const uint64_t *bm, uint32_t q) {  /
 
 // Phase maps: thread per subsequence.
 __global__ void __launch_bounds__(128) k_dec_maps(DecParams p) {
-    __shared__ uint32_t s_lut[kLutSize];
-    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) s_lut[i] = p.tab->lut[i];
+    __shared__ uint64_t s_lut[kLutSize];
+    __shared__ DecCanon s_can;
+    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) s_lut[i] = p.tab->lutm[i];
+    load_canon(s_can, p.tab);
     __syncthreads();
-    const DecTables *tab = p.tab;
+    const DecCanon *tab = &s_can;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < p.T;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t t0 = t * p.S;
@@ -454,6 +535,17 @@ __global__ void __launch_bounds__(128) k_dec_maps(DecParams p) {
                     uint32_t mcount = 0, mexit = 0;
                     while (r.pos < stop) {
                         uint32_t rel = (uint32_t)(r.pos - t0);
+                        if (rel >= kMergeWin && r.pos + kLutBits <= stop) {
+                            // past the merge window: up to three code words per lookup
+                            const uint64_t e = s_lut[r.buf >> (64 - kLutBits)];
+                            const uint32_t n = lm_count(e);
+                            if (n) {
+                                const uint32_t used = lm_len(e, 0) + lm_len(e, 1) + lm_len(e, 2);
+                                r.consume(p, used);
+                                steps += n;
+                                continue;
+                            }
+                        }
                         if (rel < kMergeWin) {
                             for (int k = 0; k < npaths; k++) {
                                 if (bm_test(paths[k].bm, rel)) {
@@ -582,12 +674,16 @@ constexpr int kFThreads = 128;
 constexpr int kStage = 32;
 template <typename SymT>
 __global__ void __launch_bounds__(kFThreads) k_dec_final(DecParams p) {
-    __shared__ uint32_t s_lut[kLutSize];
-    __shared__ SymT s_stage[kFThreads / 32][32][kStage + 1];
-    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) s_lut[i] = p.tab->lut[i];
+    extern __shared__ __align__(16) unsigned char f_smem[];
+    uint64_t *s_lut = reinterpret_cast<uint64_t *>(f_smem);
+    typedef SymT StageRow[kStage + 1];
+    StageRow(*s_stage)[32] = reinterpret_cast<StageRow(*)[32]>(f_smem + kLutSize * sizeof(uint64_t));
+    __shared__ DecCanon s_can;
+    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) s_lut[i] = p.tab->lutm[i];
+    load_canon(s_can, p.tab);
     __syncthreads();
     if (p.st->code) return;  // corrupt stream: leave the output untouched
-    const DecTables *tab = p.tab;
+    const DecCanon *tab = &s_can;
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     SymT *out = static_cast<SymT *>(p.out);
     const uint64_t tstride = (uint64_t)gridDim.x * blockDim.x;
@@ -610,7 +706,19 @@ __global__ void __launch_bounds__(kFThreads) k_dec_final(DecParams p) {
         while (__any_sync(0xffffffffu, live)) {
             uint32_t k = 0;
             if (live) {
-                for (; k < (uint32_t)kStage && r.pos < stop; k++) {
+                while (k < (uint32_t)kStage && r.pos < stop) {
+                    if (k + 3 <= (uint32_t)kStage && r.pos + kLutBits <= stop) {
+                        const uint64_t e = s_lut[r.buf >> (64 - kLutBits)];
+                        const uint32_t n = lm_count(e);
+                        if (n) {  // up to three symbols per lookup
+                            s_stage[warp][lane][k] = (SymT)lm_sym(e, 0);
+                            s_stage[warp][lane][k + 1] = (SymT)lm_sym(e, 1);
+                            s_stage[warp][lane][k + 2] = (SymT)lm_sym(e, 2);
+                            r.consume(p, lm_len(e, 0) + lm_len(e, 1) + lm_len(e, 2));
+                            k += n;
+                            continue;
+                        }
+                    }
                     uint32_t sym;
                     uint32_t L = decode_one(p, s_lut, tab, r, sym);
                     if (L == 0) {
@@ -619,6 +727,7 @@ __global__ void __launch_bounds__(kFThreads) k_dec_final(DecParams p) {
                     }
                     s_stage[warp][lane][k] = (SymT)sym;
                     r.consume(p, L);
+                    k++;
                 }
                 live = r.pos < stop;
             }
@@ -695,8 +804,8 @@ extern "C" size_t lzb_huff_encode_scratch_bytes(uint64_t n) {
 }
 
 static int huff_encode_impl(const void *sym, int sym_bytes, uint64_t n, const uint8_t *lengths,
-                            const uint64_t *codes, uint32_t cap, uint8_t *out, uint64_t out_bytes,
-                            uint64_t bit_offset, lzb_dstatus *st, void *scratch,
+                            const uint64_t *codes, uint32_t cap, uint32_t maxlen, uint8_t *out,
+                            uint64_t out_bytes, uint64_t bit_offset, lzb_dstatus *st, void *scratch,
                             size_t scratch_bytes, void *stream) {
     if (!lengths || !codes || !st || (sym_bytes != 2 && sym_bytes != 4) || cap == 0)
         return LZB_E_ARG;
@@ -723,11 +832,13 @@ static int huff_encode_impl(const void *sym, int sym_bytes, uint64_t n, const ui
     p.bit_offset = bit_offset;
     p.st = st;
     p.ntiles = nt;
-    p.maxlen = 64;
+    p.maxlen = (maxlen >= 1 && maxlen <= 64) ? maxlen : 64;
     p.table_smem = cap <= 4096;
+    const bool shortc = p.maxlen <= 32;
     size_t table = p.table_smem ? align_up((size_t)cap * 9, 16) : 0;
-    size_t smem = table + ((size_t)kETile * 64 / 32 + 2) * sizeof(uint32_t);
-    auto kern = sym_bytes == 2 ? k_huff_encode<uint16_t> : k_huff_encode<uint32_t>;
+    size_t smem = table + ((size_t)kETile * p.maxlen / 32 + 4) * sizeof(uint32_t);
+    auto kern = sym_bytes == 2 ? (shortc ? k_huff_encode<uint16_t, true> : k_huff_encode<uint16_t, false>)
+                               : (shortc ? k_huff_encode<uint32_t, true> : k_huff_encode<uint32_t, false>);
     LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEThreads, smem));
@@ -742,22 +853,23 @@ static int huff_encode_impl(const void *sym, int sym_bytes, uint64_t n, const ui
 }
 
 extern "C" int lzb_huff_encode(const void *sym, int sym_bytes, uint64_t n, const uint8_t *lengths,
-                               const uint64_t *codes, uint32_t cap, uint8_t *out, uint64_t out_bytes,
-                               lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream) {
-    return huff_encode_impl(sym, sym_bytes, n, lengths, codes, cap, out, out_bytes, 0, st, scratch,
-                            scratch_bytes, stream);
+                               const uint64_t *codes, uint32_t cap, uint32_t maxlen, uint8_t *out,
+                               uint64_t out_bytes, lzb_dstatus *st, void *scratch,
+                               size_t scratch_bytes, void *stream) {
+    return huff_encode_impl(sym, sym_bytes, n, lengths, codes, cap, maxlen, out, out_bytes, 0, st,
+                            scratch, scratch_bytes, stream);
 }
 
 // Multi-GPU slab variant: the slab's first bit lands at bit `bit_offset` (0..7)
 // of out[0]; out[0]'s leading bits and the last byte's trailing bits are left
 // zero for an OR-merge with the neighbouring slabs.
 extern "C" int lzb_huff_encode_at(const void *sym, int sym_bytes, uint64_t n, const uint8_t *lengths,
-                                  const uint64_t *codes, uint32_t cap, uint64_t bit_offset,
-                                  uint8_t *out, uint64_t out_bytes, lzb_dstatus *st, void *scratch,
-                                  size_t scratch_bytes, void *stream) {
+                                  const uint64_t *codes, uint32_t cap, uint32_t maxlen,
+                                  uint64_t bit_offset, uint8_t *out, uint64_t out_bytes,
+                                  lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream) {
     if (bit_offset > 7) return LZB_E_ARG;
-    return huff_encode_impl(sym, sym_bytes, n, lengths, codes, cap, out, out_bytes, bit_offset, st,
-                            scratch, scratch_bytes, stream);
+    return huff_encode_impl(sym, sym_bytes, n, lengths, codes, cap, maxlen, out, out_bytes,
+                            bit_offset, st, scratch, scratch_bytes, stream);
 }
 
 extern "C" size_t lzb_huff_decode_scratch_bytes(uint64_t bit_len, uint32_t maxlen, uint32_t cap) {
@@ -837,10 +949,13 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
     LZB_LAUNCH_CHECK();
     k_dec_down1<<<(unsigned)umin64((L.ng1 + 127) / 128, (uint64_t)sms * 8), 128, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
-    if (sym_bytes == 2)
-        k_dec_final<uint16_t><<<(unsigned)umin64((L.T + kFThreads - 1) / kFThreads, (uint64_t)sms * 16), kFThreads, 0, s>>>(p);
-    else
-        k_dec_final<uint32_t><<<(unsigned)umin64((L.T + kFThreads - 1) / kFThreads, (uint64_t)sms * 16), kFThreads, 0, s>>>(p);
+    {
+        const unsigned fg = (unsigned)umin64((L.T + kFThreads - 1) / kFThreads, (uint64_t)sms * 16);
+        const size_t fsm = kLutSize * sizeof(uint64_t) + (size_t)(kFThreads / 32) * 32 * (kStage + 1) * sym_bytes;
+        auto kern = sym_bytes == 2 ? k_dec_final<uint16_t> : k_dec_final<uint32_t>;
+        LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+        kern<<<fg, kFThreads, fsm, s>>>(p);
+    }
     LZB_LAUNCH_CHECK();
     return LZB_OK;
 }

@@ -72,7 +72,8 @@ def encode(codes, book: Codebook) -> BitStream:
     es = L.lzb_huff_encode_scratch_bytes(n)
     scr = N.empty_bytes(es)
     N.check_rc(L.lzb_huff_encode(c.data_ptr(), c.element_size(), n, lens.data_ptr(),
-                                 words.data_ptr(), cap, out.data_ptr(), nbytes, st.data_ptr(),
+                                 words.data_ptr(), cap, book.max_len, out.data_ptr(), nbytes,
+                                 st.data_ptr(),
                                  scr.data_ptr(), es, N.stream_ptr()), "huff_encode")
     (s,) = N.read_status(st)
     if s.code:

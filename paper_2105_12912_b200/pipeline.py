@@ -287,7 +287,7 @@ def compress_device(field: Field, eb: float, eb_mode: str = "rel", cap: int = 10
         e_scr = _pool.get("e_scratch", es, dev)
         with _Stage(prof, "K3_huff_encode"):
             N.check_rc(L.lzb_huff_encode(_dev(codes), cb, n, _dev(lengths), _dev(cwords), cap,
-                                         _dev(arc) + sym_off + 16, nbytes,
+                                         sb.u[2], _dev(arc) + sym_off + 16, nbytes,
                                          stp + 2 * N.STATUS_BYTES, _dev(e_scr), es, sp),
                        "huff_encode")
         check_slots = [2]
@@ -344,7 +344,7 @@ def compress_device(field: Field, eb: float, eb_mode: str = "rel", cap: int = 10
             es = L.lzb_huff_encode_scratch_bytes(R)
             e_scr = _pool.get("e_scratch", es, dev)
             N.check_rc(L.lzb_huff_encode(_dev(vals), 4, R, _dev(lengths), _dev(cwords), cap,
-                                         _dev(arc) + sym_off + 24, nbytes,
+                                         sv.u[2], _dev(arc) + sym_off + 24, nbytes,
                                          stp + 2 * N.STATUS_BYTES, _dev(e_scr), es, sp),
                        "huff_encode")
             lo = sym_off + 8 + sub
