@@ -65,29 +65,31 @@ __device__ __forceinline__ void store_word_bytes(uint8_t *out, uint64_t byte0, u
 // book's max length; practically always true): the table is one u64 per
 // symbol (code | len << 32) and each code word is placed branch-free with one
 // or two shared-memory ORs.  !SHORT handles 33..64-bit code words generically.
-template <typename SymT, bool SHORT>
+template <typename SymT, bool SHORT, bool TSMEM>
 __global__ void __launch_bounds__(kEThreads) k_huff_encode(EncParams p) {
     extern __shared__ __align__(16) unsigned char e_smem[];
     // [table: cap x u64 (code | len << 32) or cap x (u64 code + u8 len)][words]
     uint64_t *s_tab = reinterpret_cast<uint64_t *>(e_smem);
     uint8_t *s_lens = reinterpret_cast<uint8_t *>(s_tab + p.cap);
-    const size_t tbytes = p.table_smem ? (size_t)p.cap * 9 : 0;
+    const size_t tbytes = TSMEM ? (size_t)p.cap * 9 : 0;
     uint32_t *s_words = reinterpret_cast<uint32_t *>(e_smem + ((tbytes + 15) & ~(size_t)15));
     __shared__ uint32_t s_scan[33];
     __shared__ uint64_t s_tile, s_excl;
-    const uint64_t *tab = p.codes;
-    const uint8_t *lens = p.lengths;
-    if (p.table_smem) {
+    if (TSMEM) {
         for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) {
-            if (SHORT) s_tab[i] = (p.codes[i] & 0xFFFFFFFFull) | ((uint64_t)p.lengths[i] << 32);
+            if (SHORT) {  // left-aligned 32-bit code word | length << 32
+                const uint32_t L = p.lengths[i];
+                const uint32_t cal = L ? (uint32_t)(p.codes[i] << (32 - L)) : 0u;
+                s_tab[i] = (uint64_t)cal | ((uint64_t)L << 32);
+            }
             else {
                 s_tab[i] = p.codes[i];
                 s_lens[i] = p.lengths[i];
             }
         }
-        tab = s_tab;
-        lens = s_lens;
     }
+    const uint64_t *tab = TSMEM ? s_tab : p.codes;
+    const uint8_t *lens = TSMEM ? s_lens : p.lengths;
     const uint32_t tid = threadIdx.x;
     const uint32_t capm1 = p.cap - 1;
     uint32_t bad = 0;
@@ -119,6 +121,7 @@ __global__ void __launch_bounds__(kEThreads) k_huff_encode(EncParams p) {
         uint32_t Ls[kESyms];
         uint64_t Cs[kESyms];
         uint32_t nb = 0;
+        if (fullv) nvalid = kESyms;
 #pragma unroll
         for (int k = 0; k < kESyms; k++) {
             const uint32_t sv = sy[k];
@@ -126,9 +129,14 @@ __global__ void __launch_bounds__(kEThreads) k_huff_encode(EncParams p) {
             uint32_t L;
             uint64_t c;
             if (SHORT) {
-                const uint64_t e = tab[idx];
-                L = (uint32_t)(e >> 32);
-                c = (uint32_t)e;
+                if (TSMEM) {
+                    const uint64_t e = tab[idx];
+                    L = (uint32_t)(e >> 32);
+                    c = (uint32_t)e;
+                } else {  // big books: raw tables in global memory
+                    L = lens[idx];
+                    c = L ? (uint32_t)(tab[idx] << (32 - L)) : 0u;
+                }
             } else {
                 L = lens[idx];
                 c = tab[idx];
@@ -137,7 +145,7 @@ __global__ void __launch_bounds__(kEThreads) k_huff_encode(EncParams p) {
             bad |= (uint32_t)(v && (sv > capm1 || L == 0));
             L = v ? L : 0u;
             Ls[k] = L;
-            Cs[k] = c;
+            Cs[k] = L ? c : 0ull;  // zero-length entries contribute nothing
             nb += L;
         }
         uint32_t tile_bits;
@@ -149,15 +157,19 @@ __global__ void __launch_bounds__(kEThreads) k_huff_encode(EncParams p) {
         __syncthreads();
         // pack at tile-relative bit offsets (phase 0)
         uint32_t pos = off;
+        const uint32_t wbase_s = (uint32_t)__cvta_generic_to_shared(s_words);
 #pragma unroll
         for (int k = 0; k < kESyms; k++) {
             const uint32_t L = Ls[k];
             if (SHORT) {
-                const uint32_t w = pos >> 5, sh = pos & 31;
-                const uint32_t amt = 64u - sh - (L ? L : 1u);
-                const uint64_t v = L ? (Cs[k] << amt) : 0ull;
-                atomicOr(&s_words[w], (uint32_t)(v >> 32));
-                if (sh + L > 32) atomicOr(&s_words[w + 1], (uint32_t)v);
+                // code word -> bits [sh, sh + L) of a 64-bit window at word w:
+                // two unconditional shared-memory ORs (the second ORs zero
+                // unless the code word crosses a word boundary), no branches
+                const uint32_t sh = pos & 31;
+                const uint32_t addr = wbase_s + ((pos >> 5) << 2);
+                const uint64_t v = (Cs[k] << 32) >> sh;  // Cs = left-aligned code word
+                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"((uint32_t)(v >> 32)) : "memory");
+                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr + 4), "r"((uint32_t)v) : "memory");
             } else {
                 uint32_t rem = L, q = pos;
                 const uint64_t c = Cs[k];
@@ -256,6 +268,10 @@ struct DecTables {
     // longer than 12 bits or invalid prefix), 2-5/6-9/10-13 their lengths,
     // 16-31/32-47/48-63 their symbols (books with cap > 65536 use count 0).
     uint64_t lutm[kLutSize];
+    // Count-only LUT for the phase-map pass: all complete code words greedily
+    // decoded from the 12-bit window (up to 7): count | bits consumed << 3.
+    uint16_t lutc[kLutSize];
+    uint8_t lut1[kLutSize];  // length of the first code word (0: > 12 bits or invalid)
     uint64_t first[65];
     uint64_t cnt[65];
     uint32_t off[65];
@@ -352,6 +368,54 @@ struct BitReader {
 __device__ __forceinline__ uint32_t lm_count(uint64_t e) { return (uint32_t)(e & 3u); }
 __device__ __forceinline__ uint32_t lm_len(uint64_t e, int i) { return (uint32_t)(e >> (2 + 4 * i)) & 15u; }
 __device__ __forceinline__ uint32_t lm_sym(uint64_t e, int i) { return (uint32_t)(e >> (16 + 16 * i)) & 0xFFFFu; }
+
+// Branch-free bit window for the decode loops: two consecutive stream words
+// (w0:w1) and the bit offset sh < 32 of the current position inside w0.
+// peek12() = next 12 bits; consume(L <= 32) advances, pulling the next word
+// (predicated load, L1-resident stream) when the position leaves w0.
+struct Win {
+    uint64_t wi;  // word index of w0
+    uint32_t w0, w1, w2, w3, sh;  // w2/w3 are prefetched: a load is needed ~3 words later
+    __device__ __forceinline__ void init(const DecParams &p, uint64_t q) {
+        const uint64_t a = q + p.head;
+        wi = a >> 5;
+        sh = (uint32_t)(a & 31);
+        w0 = bswap_load(p, wi);
+        w1 = bswap_load(p, wi + 1);
+        w2 = bswap_load(p, wi + 2);
+        w3 = bswap_load(p, wi + 3);
+    }
+    __device__ __forceinline__ uint32_t peek32() const { return __funnelshift_l(w1, w0, sh); }
+    __device__ __forceinline__ uint32_t peek12() const { return peek32() >> (32 - kLutBits); }
+    __device__ __forceinline__ void consume(const DecParams &p, uint32_t L) {
+        sh += L;
+        if (sh >= 32) {
+            sh -= 32;
+            wi++;
+            w0 = w1;
+            w1 = w2;
+            w2 = w3;
+            w3 = bswap_load(p, wi + 3);
+        }
+    }
+    __device__ __forceinline__ uint64_t abs_pos(const DecParams &p) const { return wi * 32 + sh - p.head; }
+};
+
+// Long code word (> 12 bits) or invalid prefix at absolute bit q: canonical
+// tables on 64 peeked bits.  Returns len (0 = invalid), *sym.
+__device__ __forceinline__ uint32_t decode_long(const DecParams &p, const DecCanon *tab, uint64_t q,
+                                                uint32_t &sym) {
+    const uint64_t v = peek64(p, q);
+    for (uint32_t L = kLutBits + 1; L <= tab->maxlen; L++) {
+        const uint64_t c = v >> (64 - L);
+        const uint64_t f = tab->first[L], k = tab->cnt[L];
+        if (k && c >= f && c - f < k) {
+            sym = p.syms[tab->off[L] + (uint32_t)(c - f)];
+            return L;
+        }
+    }
+    return 0;
+}
 
 // Decode one code word at the reader.  Returns len (0 = invalid), *sym.
 __device__ __forceinline__ uint32_t decode_one(const DecParams &p, const uint64_t *lutm,
@@ -475,6 +539,24 @@ __global__ void k_dec_tables(const uint8_t *lengths, uint32_t cap, uint32_t maxl
             }
         }
         tab->lutm[v] = e | n;
+        // count-only entry
+        uint32_t cu = 0, cn = 0;
+        while (cn < 7) {
+            bool found = false;
+            for (uint32_t L = 1; L + cu <= (uint32_t)kLutBits && L <= s_max; L++) {
+                const uint32_t code = (v >> (kLutBits - cu - L)) & ((1u << L) - 1u);
+                const uint64_t f = tab->first[L], k = tab->cnt[L];
+                if (k && code >= f && code - f < k) {
+                    cu += L;
+                    cn++;
+                    found = true;
+                    break;
+                }
+            }
+            if (!found) break;
+        }
+        tab->lutc[v] = (uint16_t)(cn | (cu << 3));
+        tab->lut1[v] = (uint8_t)(n ? ((e >> 2) & 15u) : 0u);
     }
 }
 
@@ -497,95 +579,137 @@ __device__ __forceinline__ uint32_t bm_rank(const uint64_t *bm, uint32_t q) {  /
     return r;
 }
 
-// Phase maps: thread per subsequence.
-__global__ void __launch_bounds__(128) k_dec_maps(DecParams p) {
-    __shared__ uint64_t s_lut[kLutSize];
+// Phase maps: thread per subsequence, positions relative to the subsequence
+// start (32-bit).  Written as a warp-uniform state machine: every lane runs
+// the same phase and the step loop re-converges the warp at each step
+// (__any_sync), so lanes decode in lock-step instead of drifting apart after a
+// rare long code word.  Modes per lane and phase:
+//   1 merge window: one code word per step, record starts, look for merges
+//   2 bulk:         count-only LUT, up to seven code words per 12-bit lookup
+//   3 tail:         one code word per step up to the subsequence boundary
+constexpr int kMThreads = 512;
+__global__ void __launch_bounds__(kMThreads) k_dec_maps(DecParams p) {
+    __shared__ uint8_t s_len1[kLutSize];
+    __shared__ uint16_t s_cnt[kLutSize];
     __shared__ DecCanon s_can;
-    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) s_lut[i] = p.tab->lutm[i];
+    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) {
+        s_len1[i] = p.tab->lut1[i];
+        s_cnt[i] = p.tab->lutc[i];
+    }
     load_canon(s_can, p.tab);
     __syncthreads();
     const DecCanon *tab = &s_can;
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < p.T;
-         t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t tb = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); tb < p.T;
+         tb += stride) {
+        const uint64_t t = tb + lane_id();
+        const bool act = t < p.T;
         const uint64_t t0 = t * p.S;
         const bool last = (t == p.T - 1);
-        const uint64_t stop = last ? p.bit_len : t0 + p.S;  // decode while pos < stop
+        const uint32_t stop = act ? (uint32_t)((last ? p.bit_len : t0 + p.S) - t0) : 0;
+        const uint32_t endrel = act ? (uint32_t)umin64(p.bit_len - t0, 0xFFFFFFF0u) : 0;
+        const uint32_t lim = stop >= (uint32_t)kLutBits ? stop - kLutBits : 0;
         Path paths[kMaxPaths];
         int npaths = 0;
         for (uint32_t ph = 0; ph < p.P; ph++) {
-            uint32_t out;
-            const uint64_t q0 = t0 + ph;
-            if (ph >= p.S || q0 > p.bit_len) {
-                out = kExitInvalid;
-            } else {
-                // immediate merge?
+            // ---- per-lane phase setup ----
+            uint32_t out = kExitInvalid;
+            int mode = 0;
+            Path mine;
+#pragma unroll
+            for (int i = 0; i < (int)(kMergeWin / 64); i++) mine.bm[i] = 0;
+            Win r;
+            uint32_t rel = ph, steps = 0;
+            if (act && ph < p.S && t0 + ph <= p.bit_len) {
                 int hit = -1;
                 for (int k = 0; k < npaths; k++)
                     if (ph < kMergeWin && bm_test(paths[k].bm, ph)) { hit = k; break; }
                 if (hit >= 0) {
                     out = ((paths[hit].count - bm_rank(paths[hit].bm, ph)) << 8) | paths[hit].exit;
                 } else {
-                    Path mine;
-#pragma unroll
-                    for (int i = 0; i < (int)(kMergeWin / 64); i++) mine.bm[i] = 0;
-                    BitReader r;
-                    r.init(p, q0);
-                    uint32_t steps = 0;
-                    bool merged = false, invalid = false;
-                    uint32_t mcount = 0, mexit = 0;
-                    while (r.pos < stop) {
-                        uint32_t rel = (uint32_t)(r.pos - t0);
-                        if (rel >= kMergeWin && r.pos + kLutBits <= stop) {
-                            // past the merge window: up to three code words per lookup
-                            const uint64_t e = s_lut[r.buf >> (64 - kLutBits)];
-                            const uint32_t n = lm_count(e);
-                            if (n) {
-                                const uint32_t used = lm_len(e, 0) + lm_len(e, 1) + lm_len(e, 2);
-                                r.consume(p, used);
-                                steps += n;
-                                continue;
-                            }
-                        }
-                        if (rel < kMergeWin) {
-                            for (int k = 0; k < npaths; k++) {
-                                if (bm_test(paths[k].bm, rel)) {
-                                    merged = true;
-                                    mcount = steps + paths[k].count - bm_rank(paths[k].bm, rel);
-                                    mexit = paths[k].exit;
-                                    break;
-                                }
-                            }
-                            if (merged) break;
-                            mine.bm[rel >> 6] |= 1ull << (rel & 63);
-                        }
-                        uint32_t sym;
-                        uint32_t L = decode_one(p, s_lut, tab, r, sym);
-                        if (L == 0 || r.pos + L > p.bit_len) {
-                            invalid = true;
-                            break;
-                        }
-                        r.consume(p, L);
-                        steps++;
-                    }
-                    if (merged) {
-                        out = (mcount << 8) | mexit;
-                    } else if (invalid) {
-                        out = kExitInvalid;
+                    r.init(p, t0 + ph);
+                    mode = 1;
+                }
+            }
+            // ---- lock-step decode ----
+            while (__any_sync(0xffffffffu, mode != 0)) {
+                if (mode == 2) {
+                    if (rel > lim) {
+                        mode = 3;
                     } else {
+                        const uint32_t c = s_cnt[r.peek12()];
+                        if (c & 7u) {
+                            const uint32_t used = c >> 3;
+                            r.consume(p, used);
+                            rel += used;
+                            steps += c & 7u;
+                        } else {
+                            uint32_t sym;
+                            const uint32_t L = decode_long(p, tab, t0 + rel, sym);
+                            if (L == 0 || rel + L > endrel) {
+                                out = kExitInvalid;
+                                mode = 0;
+                            } else {
+                                if (L <= 32) r.consume(p, L);
+                                else r.init(p, t0 + rel + L);
+                                rel += L;
+                                steps++;
+                            }
+                        }
+                    }
+                } else if (mode == 1 || mode == 3) {
+                    if (rel >= stop) {
+                        // reached the boundary: exit phase (or END for the last subsequence)
                         uint32_t ex;
-                        if (last) ex = (r.pos == p.bit_len) ? kExitEnd : kExitInvalid;
-                        else ex = (uint32_t)(r.pos - stop);
-                        out = (steps << 8) | ex;
+                        if (last) ex = (rel == stop) ? kExitEnd : kExitInvalid;
+                        else ex = rel - stop;
+                        out = ex == kExitInvalid ? kExitInvalid : ((steps << 8) | ex);
                         if (npaths < kMaxPaths && ex != kExitInvalid) {
                             mine.exit = ex;
                             mine.count = steps;
                             paths[npaths++] = mine;
                         }
+                        mode = 0;
+                    } else if (mode == 1 && rel >= kMergeWin) {
+                        mode = 2;
+                    } else {
+                        bool merged = false;
+                        if (mode == 1) {
+                            for (int k = 0; k < npaths; k++) {
+                                if (bm_test(paths[k].bm, rel)) {
+                                    out = ((steps + paths[k].count - bm_rank(paths[k].bm, rel)) << 8) |
+                                          paths[k].exit;
+                                    merged = true;
+                                    break;
+                                }
+                            }
+                            if (!merged) mine.bm[rel >> 6] |= 1ull << (rel & 63);
+                        }
+                        if (merged) {
+                            mode = 0;
+                        } else {
+                            uint32_t L = s_len1[r.peek12()];
+                            if (!L) {
+                                uint32_t sym;
+                                L = decode_long(p, tab, t0 + rel, sym);
+                            }
+                            if (L == 0 || rel + L > endrel) {
+                                out = kExitInvalid;
+                                mode = 0;
+                            } else {
+                                if (L <= 32) r.consume(p, L);
+                                else r.init(p, t0 + rel + L);
+                                rel += L;
+                                steps++;
+                            }
+                        }
                     }
                 }
             }
-            if ((out & 0xFF) == kExitInvalid) out = kExitInvalid;
-            p.maps[t * p.P + ph] = out;
+            if (act) {
+                if ((out & 0xFF) == kExitInvalid) out = kExitInvalid;
+                p.maps[t * p.P + ph] = out;
+            }
         }
     }
 }
@@ -668,9 +792,10 @@ __global__ void k_dec_down1(DecParams p) {
                   p.off0);
 }
 
-// Final decode: lanes decode their subsequence, 32 symbols per round staged in
-// shared memory, and the warp writes each lane's run cooperatively.
-constexpr int kFThreads = 128;
+// Final decode: lanes decode their subsequence from the resolved entry,
+// up to three symbols per LUT lookup, staged 32 per round in shared memory;
+// the warp then writes each lane's run cooperatively (coalesced).
+constexpr int kFThreads = 512;
 constexpr int kStage = 32;
 template <typename SymT>
 __global__ void __launch_bounds__(kFThreads) k_dec_final(DecParams p) {
@@ -686,56 +811,71 @@ __global__ void __launch_bounds__(kFThreads) k_dec_final(DecParams p) {
     const DecCanon *tab = &s_can;
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     SymT *out = static_cast<SymT *>(p.out);
+    SymT *stg = &s_stage[warp][lane][0];
     const uint64_t tstride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t tb = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); tb < p.T;
          tb += tstride) {
         const uint64_t t = tb + lane;
         const bool act = t < p.T;
-        BitReader r;
-        uint64_t stop = 0, o = 0;
+        Win r;
+        uint64_t o = 0, t0 = 0;
+        uint32_t rel = 0, stop = 0;
         bool live = false;
         if (act) {
-            uint32_t e = p.ent0[t];
+            const uint32_t e = p.ent0[t];
             if (e != kExitInvalid && e != kExitEnd) {
-                r.init(p, t * p.S + e);
-                stop = (t == p.T - 1) ? p.bit_len : umin64(t * p.S + p.S, p.bit_len);
+                t0 = t * p.S;
+                stop = (uint32_t)(((t == p.T - 1) ? p.bit_len : umin64(t0 + p.S, p.bit_len)) - t0);
+                rel = e;
+                r.init(p, t0 + rel);
                 o = p.off0[t];
-                live = r.pos < stop;
+                live = rel < stop;
             }
         }
+        const uint32_t lim = stop >= (uint32_t)kLutBits ? stop - kLutBits : 0;
         while (__any_sync(0xffffffffu, live)) {
             uint32_t k = 0;
-            if (live) {
-                while (k < (uint32_t)kStage && r.pos < stop) {
-                    if (k + 3 <= (uint32_t)kStage && r.pos + kLutBits <= stop) {
-                        const uint64_t e = s_lut[r.buf >> (64 - kLutBits)];
-                        const uint32_t n = lm_count(e);
-                        if (n) {  // up to three symbols per lookup
-                            s_stage[warp][lane][k] = (SymT)lm_sym(e, 0);
-                            s_stage[warp][lane][k + 1] = (SymT)lm_sym(e, 1);
-                            s_stage[warp][lane][k + 2] = (SymT)lm_sym(e, 2);
-                            r.consume(p, lm_len(e, 0) + lm_len(e, 1) + lm_len(e, 2));
-                            k += n;
-                            continue;
+            // lock-step round: every lane takes one step per iteration (the
+            // vote re-converges the warp), at most kStage symbols per lane
+            bool go = live;
+            while (__any_sync(0xffffffffu, go)) {
+                if (go) {
+                    const uint64_t e = s_lut[r.peek12()];
+                    const uint32_t n = lm_count(e);
+                    if (n && k <= (uint32_t)kStage - 3 && rel <= lim) {
+                        stg[k] = (SymT)lm_sym(e, 0);
+                        stg[k + 1] = (SymT)lm_sym(e, 1);
+                        stg[k + 2] = (SymT)lm_sym(e, 2);
+                        const uint32_t used = lm_len(e, 0) + lm_len(e, 1) + lm_len(e, 2);
+                        r.consume(p, used);
+                        rel += used;
+                        k += n;
+                    } else {
+                        uint32_t L, sym;
+                        if (n) {
+                            L = lm_len(e, 0);
+                            sym = lm_sym(e, 0);
+                        } else {
+                            L = decode_long(p, tab, t0 + rel, sym);
+                        }
+                        if (L == 0) {
+                            rel = stop;
+                        } else {
+                            stg[k++] = (SymT)sym;
+                            if (L <= 32) r.consume(p, L);
+                            else r.init(p, t0 + rel + L);
+                            rel += L;
                         }
                     }
-                    uint32_t sym;
-                    uint32_t L = decode_one(p, s_lut, tab, r, sym);
-                    if (L == 0) {
-                        r.pos = stop;
-                        break;
-                    }
-                    s_stage[warp][lane][k] = (SymT)sym;
-                    r.consume(p, L);
-                    k++;
+                    go = rel < stop && k < (uint32_t)kStage;
                 }
-                live = r.pos < stop;
             }
+            live = rel < stop;
             __syncwarp();
             // cooperative write-out of every lane's k symbols
             for (uint32_t j = 0; j < 32; j++) {
-                uint32_t kj = __shfl_sync(0xffffffffu, k, j);
-                uint64_t oj = __shfl_sync(0xffffffffu, o, j);
+                const uint32_t kj = __shfl_sync(0xffffffffu, k, j);
+                const uint64_t oj = __shfl_sync(0xffffffffu, o, j);
                 if (lane < kj && oj + lane < p.count) out[oj + lane] = s_stage[warp][j][lane];
             }
             o += k;
@@ -837,8 +977,14 @@ static int huff_encode_impl(const void *sym, int sym_bytes, uint64_t n, const ui
     const bool shortc = p.maxlen <= 32;
     size_t table = p.table_smem ? align_up((size_t)cap * 9, 16) : 0;
     size_t smem = table + ((size_t)kETile * p.maxlen / 32 + 4) * sizeof(uint32_t);
-    auto kern = sym_bytes == 2 ? (shortc ? k_huff_encode<uint16_t, true> : k_huff_encode<uint16_t, false>)
-                               : (shortc ? k_huff_encode<uint32_t, true> : k_huff_encode<uint32_t, false>);
+    void (*kern)(EncParams);
+    if (sym_bytes == 2) {
+        if (shortc) kern = p.table_smem ? k_huff_encode<uint16_t, true, true> : k_huff_encode<uint16_t, true, false>;
+        else kern = p.table_smem ? k_huff_encode<uint16_t, false, true> : k_huff_encode<uint16_t, false, false>;
+    } else {
+        if (shortc) kern = p.table_smem ? k_huff_encode<uint32_t, true, true> : k_huff_encode<uint32_t, true, false>;
+        else kern = p.table_smem ? k_huff_encode<uint32_t, false, true> : k_huff_encode<uint32_t, false, false>;
+    }
     LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEThreads, smem));
@@ -935,7 +1081,7 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
     const int sms = dev_sms();
     // phases >= the book's real max length cannot be entries (P = maxlen hint;
     // k_dec_tables flags a hint that disagrees with the lengths as corrupt).
-    k_dec_maps<<<(unsigned)umin64((L.T + 127) / 128, (uint64_t)sms * 16), 128, 0, s>>>(p);
+    k_dec_maps<<<(unsigned)umin64((L.T + kMThreads - 1) / kMThreads, (uint64_t)sms * 4), kMThreads, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
     k_dec_compose<uint32_t><<<(unsigned)umin64((L.ng1 * L.P + 255) / 256, (uint64_t)sms * 32), 256, 0, s>>>(
         p.maps, L.T, L.P, L.G, p.g1, L.ng1);
@@ -950,7 +1096,7 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
     k_dec_down1<<<(unsigned)umin64((L.ng1 + 127) / 128, (uint64_t)sms * 8), 128, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
     {
-        const unsigned fg = (unsigned)umin64((L.T + kFThreads - 1) / kFThreads, (uint64_t)sms * 16);
+        const unsigned fg = (unsigned)umin64((L.T + kFThreads - 1) / kFThreads, (uint64_t)sms * 4);
         const size_t fsm = kLutSize * sizeof(uint64_t) + (size_t)(kFThreads / 32) * 32 * (kStage + 1) * sym_bytes;
         auto kern = sym_bytes == 2 ? k_dec_final<uint16_t> : k_dec_final<uint32_t>;
         LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
