@@ -95,7 +95,6 @@ int lzb_prequantize(const void *x, int dtype, uint64_t n, double eb_abs, int64_t
  * PrequantGrid, P/quantize.py:161): prequantization is then skipped.
  * st->u[0] = outlier count.  If it exceeds out_capacity the records are not
  * complete and code = LZB_E_CAPACITY (retry with a larger buffer).
- * st->u[1] = number of maximal runs of the stream (sizes RLE, P/rle.py:17-35).
  * ------------------------------------------------------------------- */
 size_t lzb_quantize_scratch_bytes(const lzb_geom *g, uint64_t out_capacity);
 int lzb_quantize(const void *x, int dtype, const lzb_geom *g, double eb_abs, uint32_t cap,
@@ -169,6 +168,12 @@ int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t count,
                     const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym,
                     int sym_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
                     void *stream);
+
+/* ---------------------------------------------------------------------
+ * Number of maximal runs of a symbol stream (sizes K4's outputs before the
+ * RLE / RLE_VLE workflows, P/rle.py:17-35).  st->u[0] = run count.
+ * ------------------------------------------------------------------- */
+int lzb_count_runs(const void *sym, int sym_bytes, uint64_t n, lzb_dstatus *st, void *stream);
 
 /* ---------------------------------------------------------------------
  * K4: run-length encode (P/rle.py:17-35): maximal runs, runs longer than

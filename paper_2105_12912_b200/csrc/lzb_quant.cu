@@ -51,9 +51,6 @@ struct QuantParams {
     // box mode
     uint32_t K;              // chunks per tile
     uint64_t tiles_per_row;  // ceil(nbx / K)
-    // maximal-run counting for RLE sizing (P/rle.py:17-35)
-    uint32_t *tfirst, *tlast;
-    unsigned long long *inner_heads;
 };
 
 // f64 prequantization, bit-identical with numpy (P/quantize.py:90-110).
@@ -220,7 +217,6 @@ __global__ void __launch_bounds__(kQThreads) k_quantize(QuantParams p) {
     const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const int64_t r = p.radius;
     int flags = 0;
-    unsigned long long heads = 0;
 
     while (true) {
         if (tid == 0) s_tile = atomicAdd(p.ticket, 1u);
@@ -281,19 +277,6 @@ __global__ void __launch_bounds__(kQThreads) k_quantize(QuantParams p) {
         }
         __syncthreads();
 
-        // ---- run heads inside the tile (RLE sizing) ----
-        {
-            const uint32_t a = tid * kSeg;
-#pragma unroll
-            for (int k = 0; k < kSeg; k++) {
-                uint32_t i = a + k;
-                if (i > 0 && i < n) heads += s_code[i] != s_code[i - 1];
-            }
-            if (tid == 0) {
-                p.tfirst[t] = (uint32_t)s_code[0];
-                p.tlast[t] = (uint32_t)s_code[n - 1];
-            }
-        }
         // ---- write the codes: one contiguous stream range ----
         SymT *out = static_cast<SymT *>(p.codes) + base;
         constexpr uint32_t kVec = 16 / sizeof(SymT);
@@ -359,22 +342,6 @@ __global__ void __launch_bounds__(kQThreads) k_quantize(QuantParams p) {
         if (flags & 1) set_status(p.st, LZB_E_OVERFLOW);
         else set_status(p.st, LZB_E_ASSERT);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) heads += __shfl_xor_sync(0xffffffffu, heads, o);
-    if (lane == 0 && heads) atomicAdd(p.inner_heads, heads);
-}
-
-// maximal runs = 1 + heads inside tiles + heads at tile boundaries
-__global__ void k_count_runs(const uint32_t *tfirst, const uint32_t *tlast, uint64_t ntiles,
-                             const unsigned long long *inner, lzb_dstatus *st) {
-    __shared__ unsigned long long s_b;
-    if (threadIdx.x == 0) s_b = 0;
-    __syncthreads();
-    unsigned long long b = 0;
-    for (uint64_t t = 1 + threadIdx.x; t < ntiles; t += blockDim.x) b += tfirst[t] != tlast[t - 1];
-    atomicAdd(&s_b, b);
-    __syncthreads();
-    if (threadIdx.x == 0) st->u[1] = 1ull + *inner + s_b;
 }
 
 // ----------------------------------------------------------------------------
@@ -597,9 +564,6 @@ static void quant_scratch(S &s, const QuantLayout &L, uint64_t cap_out) {
     s.template take<uint64_t>(L.nrows_chunk);            // seg start
     s.template take<uint64_t>(L.nrows_chunk);            // seg end
     s.template take<uint64_t>((L.nrows_grid + 2047) / 2048 + 1);  // scan look-back
-    s.template take<uint32_t>(L.ntiles);                 // tile first code
-    s.template take<uint32_t>(L.ntiles);                 // tile last code
-    s.template take<unsigned long long>(1);              // inner heads
     if (L.fast3d) {
         s.template take<uint64_t>(L.ntiles * 2 * kQ3Slot);  // record slots
         s.template take<uint32_t>(L.ntiles);                // tile counts
@@ -668,10 +632,7 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
     uint64_t *seg_start = sc.take<uint64_t>(L.nrows_chunk);
     uint64_t *seg_end = sc.take<uint64_t>(L.nrows_chunk);
     uint64_t *scan_lb = sc.take<uint64_t>((L.nrows_grid + 2047) / 2048 + 1);
-    uint32_t *tfirst = sc.take<uint32_t>(L.ntiles);
-    uint32_t *tlast = sc.take<uint32_t>(L.ntiles);
-    unsigned long long *inner = sc.take<unsigned long long>(1);
-    if (!inner) return LZB_E_ARG;
+    if (!scan_lb) return LZB_E_ARG;
     uint64_t *slots = nullptr, *tile_off = nullptr, *slb = nullptr;
     uint32_t *tile_cnt = nullptr, *over_list = nullptr;
     if (L.fast3d) {
@@ -683,7 +644,6 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
         if (!slb) return LZB_E_ARG;
         LZB_CUDA_TRY(cudaMemsetAsync(slb, 0, ((L.ntiles + 2047) / 2048 + 1) * sizeof(uint64_t), s));
     }
-    LZB_CUDA_TRY(cudaMemsetAsync(inner, 0, sizeof(unsigned long long), s));
 
     LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     LZB_CUDA_TRY(cudaMemsetAsync(hist, 0, cap * sizeof(uint64_t), s));
@@ -707,9 +667,6 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
     qp.ntiles = L.ntiles;
     qp.K = L.K;
     qp.tiles_per_row = L.tiles_per_row;
-    qp.tfirst = tfirst;
-    qp.tlast = tlast;
-    qp.inner_heads = inner;
 
     int rc;
     if (L.fast3d && dtype != 2) {
@@ -732,9 +689,6 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
         q3.ticket = &tick[0];
         q3.nchunks = g.nbx * g.nby * g.nbz;
         q3.ntiles = (q3.nchunks + kQ3TileChunks - 1) / kQ3TileChunks;
-        q3.tfirst = tfirst;
-        q3.tlast = tlast;
-        q3.inner_heads = inner;
         q3.slots = slots;
         q3.tile_cnt = tile_cnt;
         q3.over_list = over_list;
@@ -742,7 +696,9 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
         q3.tile_off = tile_off;
         const size_t esz = dtype == 0 ? 4 : 8;
         q3.vec_ok = (g.nx % (16 / esz) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-        size_t smem = (size_t)kQ3Warps * 512 * code_bytes + (size_t)cap * 4;
+        size_t smem = (size_t)kQ3Warps * 2 * 32 * 16 * (dtype == 0 ? 4 : 8) +
+                      (size_t)kQ3Warps * 512 * code_bytes + (size_t)kQ3Warps * 16 * 32 * 4 +
+                      (size_t)cap * 4;
         auto launch = [&](auto kern) -> int {
             LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int per_sm = 0;
@@ -758,8 +714,6 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
         else
             rc = code_bytes == 2 ? launch(k_quantize3d8<double, uint16_t>) : launch(k_quantize3d8<double, uint32_t>);
         if (rc) return rc;
-        k_count_runs<<<1, 1024, 0, s>>>(tfirst, tlast, q3.ntiles, inner, st);
-        LZB_LAUNCH_CHECK();
         // phase 2: tile offsets, slot compaction, overflow re-emission
         const int sms = device_sms();
         k_q3_scan<<<(unsigned)umin64((q3.ntiles + 2047) / 2048, (uint64_t)sms * 4), 256, 0, s>>>(
@@ -805,8 +759,6 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
                                  : launch_quant<double, uint32_t, false>(qp, s);
     }
     if (rc) return rc;
-    k_count_runs<<<1, 1024, 0, s>>>(tfirst, tlast, L.ntiles, inner, st);
-    LZB_LAUNCH_CHECK();
 order:
     if (!outliers || out_capacity == 0) return LZB_OK;
 

@@ -40,8 +40,6 @@ struct Q3Params {
     uint64_t *lb;
     unsigned int *ticket;
     uint64_t nchunks, ntiles;
-    uint32_t *tfirst, *tlast;
-    unsigned long long *inner_heads;
     int vec_ok;  // rows of full chunks are 16-byte aligned for vector loads
     // two-phase outlier ordering: per-tile record slots + counts
     uint64_t *slots;        // ntiles * kQ3Slot records
@@ -55,8 +53,6 @@ template <typename InT>
 struct Q3Warp {
     // per-lane state across the warp's chunks
     uint64_t hw0, hw1;  // packed 8-bit counters for codes r-8 .. r+7
-    uint32_t hw_n;      // chunks accumulated in hw0/hw1
-    unsigned long long heads;
     int flags;
 };
 
@@ -233,30 +229,19 @@ __device__ __forceinline__ uint32_t q3_chunk_body(const Q3Params &p, uint64_t c,
     }
     if (emit) return total;
 
-    // codes were staged in stream order: one contiguous write + run heads
+    // codes were staged in stream order: one contiguous write
     __syncwarp();
     const uint32_t cnt = k.ex * k.ey * k.ez;
     SymT *out = static_cast<SymT *>(p.codes) + k.base;
-    unsigned long long hd = 0;
     if (cnt == 512 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
         constexpr int V = 16 / sizeof(SymT);  // symbols per uint4
         const uint4 *src = reinterpret_cast<const uint4 *>(s_codes);
         uint4 *dst = reinterpret_cast<uint4 *>(out);
 #pragma unroll
         for (int i = lane; i < 512 / V; i += 32) dst[i] = src[i];
-        // run heads: lane covers positions [16 lane, 16 lane + 16)
-#pragma unroll
-        for (int j = 0; j < 16; j++) {
-            uint32_t i = 16 * lane + j;
-            if (i > 0) hd += s_codes[i] != s_codes[i - 1];
-        }
     } else {
-        for (uint32_t i = lane; i < cnt; i += 32) {
-            out[i] = s_codes[i];
-            if (i > 0) hd += s_codes[i] != s_codes[i - 1];
-        }
+        for (uint32_t i = lane; i < cnt; i += 32) out[i] = s_codes[i];
     }
-    w.heads += hd;
     first_code = (uint32_t)s_codes[0];
     last_code = (uint32_t)s_codes[cnt - 1];
     __syncwarp();
@@ -266,7 +251,6 @@ __device__ __forceinline__ uint32_t q3_chunk_body(const Q3Params &p, uint64_t c,
 struct Q3Res {
     uint32_t n, first, last;
     int flags;
-    unsigned long long heads;
 };
 
 // The exact int64 path lives out of line so the hot path never saves
@@ -278,15 +262,12 @@ __device__ __noinline__ Q3Res q3_chunk_wide(const Q3Params *pp, uint64_t c, uint
     const Q3Params &p = *pp;
     Q3Warp<InT> t;
     t.hw0 = t.hw1 = 0;
-    t.hw_n = 0;
-    t.heads = 0;
     t.flags = 0;
     Q3Res res;
     res.n = q3_chunk_body<InT, SymT, true>(p, c, lane, s_codes, stash, wcount, t, s_hist, emit,
                                            emit_pos, res.first, res.last);
     if (p.cap >= 16) q3_hist_flush<SymT>(t.hw0, t.hw1, p.r, s_hist, lane);
     res.flags = t.flags;
-    res.heads = t.heads;
     return res;
 }
 
@@ -305,29 +286,29 @@ __device__ __forceinline__ uint32_t q3_chunk(const Q3Params &p, uint64_t c, uint
         first_code = r.first;
         last_code = r.last;
         w.flags |= r.flags;
-        w.heads += r.heads;
     }
     return n;
 }
 
-// Lean path for a FULL 8x8x8 chunk: no masks, no staging, no divisions.
-// gi0 = global index of this lane's row0 start, sbase = stream offset of the
-// chunk.  Returns kQ3Redo (nothing written) when a value needs the exact path.
+// Lean path for a FULL 8x8x8 chunk: no masks, no divisions.  The lane's two
+// input rows were prefetched into shared memory (`stg`, cp.async) one chunk
+// ahead.  gi0 = global index of this lane's row0 start, sbase = stream offset
+// of the chunk.  Returns kQ3Redo (nothing written) when a value needs the
+// exact path.  Histogram: the 16 codes around the radius go to this lane's
+// private column of a per-warp shared table (conflict-free red.shared), the
+// rest to the CTA table.
 template <typename InT, typename SymT>
-__device__ __forceinline__ uint32_t q3_full(const Q3Params &p, uint64_t gi0, uint64_t sbase,
-                                            uint32_t lane, uint64_t *stash, uint32_t wcount,
-                                            Q3Warp<InT> &w, uint32_t *s_hist, bool emit,
-                                            uint64_t emit_pos, uint32_t &first_code,
-                                            uint32_t &last_code) {
+__device__ __forceinline__ uint32_t q3_full(const Q3Params &p, const InT *stg, uint64_t gi0,
+                                            uint64_t sbase, uint32_t lane, uint64_t *stash,
+                                            uint32_t wcount, uint32_t colbase, uint32_t hbase,
+                                            bool emit, uint64_t emit_pos) {
     const uint32_t ly = lane & 7, lz0 = (lane >> 3) * 2;
     const uint64_t plane = p.g.nx * p.g.ny;
-    const InT *in = static_cast<const InT *>(p.x);
     int32_t d0[8], d1[8];
     bool ok = true;
     if constexpr (sizeof(InT) == 4) {
-        const float4 *q0 = reinterpret_cast<const float4 *>(in + gi0);
-        const float4 *q1 = reinterpret_cast<const float4 *>(in + gi0 + plane);
-        float4 a = __ldg(q0), b = __ldg(q0 + 1), c = __ldg(q1), d = __ldg(q1 + 1);
+        const float4 *q = reinterpret_cast<const float4 *>(stg);
+        float4 a = q[0], b = q[1], c = q[2], d = q[3];
         float x0[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
         float x1[8] = {c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w};
 #pragma unroll
@@ -336,11 +317,10 @@ __device__ __forceinline__ uint32_t q3_full(const Q3Params &p, uint64_t gi0, uin
             d1[j] = f3::pq_fast_f32(x1[j], p.inv_hi, p.inv_lo, ok);
         }
     } else {
-        const double2 *q0 = reinterpret_cast<const double2 *>(in + gi0);
-        const double2 *q1 = reinterpret_cast<const double2 *>(in + gi0 + plane);
+        const double2 *q = reinterpret_cast<const double2 *>(stg);
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            double2 a = __ldg(q0 + j), b = __ldg(q1 + j);
+            double2 a = q[j], b = q[4 + j];
             d0[2 * j] = f3::pq_fast(a.x, p.inv, ok);
             d0[2 * j + 1] = f3::pq_fast(a.y, p.inv, ok);
             d1[2 * j] = f3::pq_fast(b.x, p.inv, ok);
@@ -351,6 +331,8 @@ __device__ __forceinline__ uint32_t q3_full(const Q3Params &p, uint64_t gi0, uin
     f3::deltas<int32_t>(d0, d1, lane);
 
     const int32_t r = p.r;
+    // window of private columns: codes r-8 .. r+7 (none when cap < 16)
+    const uint32_t klo = p.cap >= 16 ? (uint32_t)(r - 8) : (uint32_t)(r + 16);
     uint32_t o0 = 0, o1 = 0;
     uint32_t c0[8], c1[8];
 #pragma unroll
@@ -403,28 +385,15 @@ __device__ __forceinline__ uint32_t q3_full(const Q3Params &p, uint64_t gi0, uin
     }
     if (emit) return total;
 
-    // histogram: packed 8-bit counters for r-8 .. r+7, the rest in shared memory
-    if (p.cap >= 16) {
+    // histogram (fire-and-forget shared-memory reductions)
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-#pragma unroll
-            for (int j = 0; j < 8; j++) {
-                const uint32_t code = h ? c1[j] : c0[j];
-                const uint32_t bin = code - (uint32_t)(r - 8);
-                if (bin < 16u) {
-                    const uint64_t inc = 1ull << ((bin & 7u) * 8u);
-                    if (bin < 8u) w.hw0 += inc;
-                    else w.hw1 += inc;
-                } else {
-                    atomicAdd(&s_hist[code], 1u);
-                }
-            }
-        }
-    } else {
+    for (int h = 0; h < 2; h++) {
 #pragma unroll
         for (int j = 0; j < 8; j++) {
-            atomicAdd(&s_hist[c0[j]], 1u);
-            atomicAdd(&s_hist[c1[j]], 1u);
+            const uint32_t code = h ? c1[j] : c0[j];
+            const uint32_t key = code - klo;
+            const uint32_t addr = key < 16u ? colbase + (key << 7) : hbase + (code << 2);
+            asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
         }
     }
 
@@ -446,48 +415,70 @@ __device__ __forceinline__ uint32_t q3_full(const Q3Params &p, uint64_t gi0, uin
             reinterpret_cast<uint4 *>(dst)[1] = make_uint4(cr[4], cr[5], cr[6], cr[7]);
         }
     }
-    // run heads in stream order (rows r = ly + 8 lz): in-row from registers,
-    // row starts against the previous row's last symbol (shuffles)
-    {
-        const uint32_t a = __shfl_up_sync(f3::kFull, c0[7], 1);
-        const uint32_t b = __shfl_up_sync(f3::kFull, c1[7], 1);
-        const uint32_t cc = __shfl_down_sync(f3::kFull, c0[7], 7);
-        unsigned long long hd = 0;
-        if (ly) {
-            hd += c0[0] != a;
-            hd += c1[0] != b;
-        } else {
-            if (lane >= 8) hd += c0[0] != b;
-            hd += c1[0] != cc;
-        }
-#pragma unroll
-        for (int j = 1; j < 8; j++) {
-            hd += c0[j] != c0[j - 1];
-            hd += c1[j] != c1[j - 1];
-        }
-        w.heads += hd;
-    }
-    first_code = __shfl_sync(f3::kFull, c0[0], 0);
-    last_code = __shfl_sync(f3::kFull, c1[7], 31);
     return total;
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// chunk c of the fast grid: full? + lane row0 global index + stream offset
+struct Q3Loc {
+    bool full;
+    uint64_t gi0, sbase;
+};
+
+__device__ __forceinline__ Q3Loc q3_loc(const Q3Params &p, uint64_t bx, uint64_t by, uint64_t bz,
+                                        uint32_t lane) {
+    Q3Loc l;
+    l.full = p.vec_ok && (bx * 8 + 8 <= p.g.nx) && (by * 8 + 8 <= p.g.ny) && (bz * 8 + 8 <= p.g.nz);
+    l.sbase = p.g.nx * p.g.ny * 8 * bz + p.g.nx * 64 * by + 512 * bx;
+    l.full = l.full && ((l.sbase & 7) == 0);
+    l.gi0 = bx * 8 + p.g.nx * ((by * 8 + (lane & 7)) + p.g.ny * (bz * 8 + (lane >> 3) * 2));
+    return l;
+}
+
+// the lane copies its two rows (2 x 8 values) into its stage slot
+template <typename InT>
+__device__ __forceinline__ void q3_prefetch(const Q3Params &p, const Q3Loc &l, uint32_t saddr) {
+    const InT *in = static_cast<const InT *>(p.x);
+    const InT *r0 = in + l.gi0;
+    const InT *r1 = r0 + p.g.nx * p.g.ny;
+    constexpr int V = 16 / sizeof(InT);  // values per 16-byte copy
+#pragma unroll
+    for (int k = 0; k < 8 / V; k++) {
+        cp_async16(saddr + 16 * k, r0 + V * k);
+        cp_async16(saddr + 16 * (8 / V + k), r1 + V * k);
+    }
 }
 
 template <typename InT, typename SymT>
 __global__ void __launch_bounds__(kQ3Threads, 2) k_quantize3d8(const __grid_constant__ Q3Params p) {
     extern __shared__ __align__(16) unsigned char q3_smem[];
-    // [s_codes: warps x 512 SymT (partial-chunk staging)][s_hist: cap u32]
+    // [stage: warps x 2 x 32 lanes x 16 values][s_codes: warps x 512 SymT]
+    // [s_col: warps x 16 bins x 32 lanes u32][s_hist: cap u32]
+    constexpr uint32_t kLaneStage = 16 * sizeof(InT);
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    SymT *s_codes = reinterpret_cast<SymT *>(q3_smem) + warp * 512;
-    uint32_t *s_hist = reinterpret_cast<uint32_t *>(q3_smem + kQ3Warps * 512 * sizeof(SymT));
+    unsigned char *stage = q3_smem + warp * 2 * 32 * kLaneStage;
+    unsigned char *after_stage = q3_smem + kQ3Warps * 2 * 32 * kLaneStage;
+    SymT *s_codes = reinterpret_cast<SymT *>(after_stage) + warp * 512;
+    uint32_t *s_col = reinterpret_cast<uint32_t *>(after_stage + kQ3Warps * 512 * sizeof(SymT));
+    uint32_t *s_hist = s_col + kQ3Warps * 16 * 32;
+    for (uint32_t i = threadIdx.x; i < kQ3Warps * 16 * 32; i += blockDim.x) s_col[i] = 0;
     for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
+    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage) + lane * kLaneStage;
+    const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(s_hist);
+    // codes outside the 16-bin window (or books with cap < 16) go straight to s_hist
+    const uint32_t colbase = p.cap >= 16
+        ? (uint32_t)__cvta_generic_to_shared(s_col + warp * 16 * 32) + lane * 4
+        : 0xFFFFFFFFu;
 
     Q3Warp<InT> w;
     w.hw0 = w.hw1 = 0;
-    w.hw_n = 0;
-    w.heads = 0;
     w.flags = 0;
-    const bool win = p.cap >= 16;
     while (true) {
         uint64_t t = 0;
         if (lane == 0) t = atomicAdd(p.ticket, 1u);
@@ -496,26 +487,15 @@ __global__ void __launch_bounds__(kQ3Threads, 2) k_quantize3d8(const __grid_cons
         const uint64_t c0 = t * kQ3TileChunks;
         const uint64_t c1 = umin64(c0 + kQ3TileChunks, p.nchunks);
         uint64_t *slot = p.slots + t * 2 * kQ3Slot;
-        uint32_t wcount = 0, fc = 0, prev_last = 0;
+        uint32_t wcount = 0;
         uint64_t bx = c0 % p.g.nbx, rowc = c0 / p.g.nbx;
         uint64_t by = rowc % p.g.nby, bz = rowc / p.g.nby;
+        Q3Loc cur = q3_loc(p, bx, by, bz, lane);
+        if (cur.full) q3_prefetch<InT>(p, cur, stage_s);
+        cp_async_commit();
+        uint32_t sb = 0;
         for (uint64_t c = c0; c < c1; c++) {
-            uint32_t f, l;
-            uint32_t n = kQ3Redo;
-            const bool full = p.vec_ok && (bx * 8 + 8 <= p.g.nx) && (by * 8 + 8 <= p.g.ny) &&
-                              (bz * 8 + 8 <= p.g.nz);
-            if (full) {
-                const uint64_t sbase = p.g.nx * p.g.ny * 8 * bz + p.g.nx * 64 * by + 512 * bx;
-                if ((sbase & 7) == 0) {
-                    const uint64_t gi0 = bx * 8 + p.g.nx * ((by * 8 + (lane & 7)) +
-                                                            p.g.ny * (bz * 8 + (lane >> 3) * 2));
-                    n = q3_full<InT, SymT>(p, gi0, sbase, lane, slot, wcount, w, s_hist, false, 0,
-                                           f, l);
-                }
-            }
-            if (n == kQ3Redo)
-                n = q3_chunk<InT, SymT>(p, c, lane, s_codes, slot, wcount, w, s_hist, false, 0, f,
-                                        l);
+            // prefetch the next chunk of the tile into the other stage buffer
             if (++bx == p.g.nbx) {
                 bx = 0;
                 if (++by == p.g.nby) {
@@ -523,32 +503,48 @@ __global__ void __launch_bounds__(kQ3Threads, 2) k_quantize3d8(const __grid_cons
                     ++bz;
                 }
             }
-            if (c == c0) fc = f;
-            else if (lane == 0) w.heads += (f != prev_last);  // head at the chunk boundary
-            prev_last = l;
-            wcount += n;
-            if (win && ++w.hw_n == 15) {
-                q3_hist_flush<SymT>(w.hw0, w.hw1, p.r, s_hist, lane);
-                w.hw_n = 0;
+            Q3Loc nxt;
+            nxt.full = false;
+            if (c + 1 < c1) {
+                nxt = q3_loc(p, bx, by, bz, lane);
+                if (nxt.full) q3_prefetch<InT>(p, nxt, stage_s + (sb ^ 1) * 32 * kLaneStage);
             }
+            cp_async_commit();
+            cp_async_wait1();  // this chunk's rows have landed
+            uint32_t n = kQ3Redo;
+            if (cur.full)
+                n = q3_full<InT, SymT>(p, reinterpret_cast<const InT *>(stage + sb * 32 * kLaneStage + lane * kLaneStage),
+                                       cur.gi0, cur.sbase, lane, slot, wcount, colbase, hbase, false, 0);
+            if (n == kQ3Redo) {
+                uint32_t f, l;
+                n = q3_chunk<InT, SymT>(p, c, lane, s_codes, slot, wcount, w, s_hist, false, 0, f, l);
+                // partial chunks: fold the 8-bit window counters right away
+                if (p.cap >= 16) q3_hist_flush<SymT>(w.hw0, w.hw1, p.r, s_hist, lane);
+            }
+            wcount += n;
+            cur = nxt;
+            sb ^= 1;
         }
         if (lane == 0) {
-            p.tfirst[t] = fc;
-            p.tlast[t] = prev_last;
             p.tile_cnt[t] = wcount;
             if (wcount > (uint32_t)kQ3Slot) p.over_list[atomicAdd(p.n_over, 1u)] = (uint32_t)t;
         }
     }
-    if (win && w.hw_n) q3_hist_flush<SymT>(w.hw0, w.hw1, p.r, s_hist, lane);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    // fold this warp's private columns into the CTA histogram
+    if (p.cap >= 16) {
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            const uint32_t v = __reduce_add_sync(f3::kFull, s_col[(warp * 16 + k) * 32 + lane]);
+            if (lane == 0 && v) atomicAdd(&s_hist[p.r - 8 + k], v);
+        }
+    }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x)
         if (s_hist[i]) atomicAdd(&p.hist[i], (unsigned long long)s_hist[i]);
     int flags = __reduce_or_sync(f3::kFull, w.flags);
     if (lane == 0 && flags) set_status(p.st, (flags & 1) ? LZB_E_OVERFLOW : LZB_E_ASSERT);
-    unsigned long long hsum = w.heads;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(f3::kFull, hsum, o);
-    if (lane == 0 && hsum) atomicAdd(p.inner_heads, hsum);
 }
 
 // Phase 2a: copy each tile's slot records to its final (chunk-major) place.
@@ -579,8 +575,6 @@ __global__ void __launch_bounds__(kQ3Threads) k_q3_emit(const __grid_constant__ 
     const uint32_t nover = *p.n_over;
     Q3Warp<InT> w;
     w.hw0 = w.hw1 = 0;
-    w.hw_n = 0;
-    w.heads = 0;
     w.flags = 0;
     const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;

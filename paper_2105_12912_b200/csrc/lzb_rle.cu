@@ -260,9 +260,56 @@ static int sms() {
     return s > 0 ? s : 148;
 }
 
+// Maximal-run count of a symbol stream (sizes K4's outputs).  Each thread
+// compares 8 consecutive symbols (one 16-byte load for u16) with their
+// predecessors; the block total goes to st->u[0] with one atomic.
+template <typename SymT>
+__global__ void __launch_bounds__(256) k_count_runs(const SymT *sym, uint64_t n, lzb_dstatus *st) {
+    unsigned long long heads = 0;
+    const uint64_t ngroups = (n + 7) / 8;
+    for (uint64_t gidx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; gidx < ngroups;
+         gidx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = gidx * 8;
+        uint32_t prev = b > 0 ? (uint32_t)__ldg(sym + b - 1) : ~(uint32_t)sym[0];
+        if (b + 8 <= n && sizeof(SymT) == 2 && (reinterpret_cast<uintptr_t>(sym + b) & 15) == 0) {
+            uint4 v = __ldg(reinterpret_cast<const uint4 *>(sym + b));
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const uint32_t lo = w[k] & 0xFFFFu, hi = w[k] >> 16;
+                heads += (lo != prev) + (hi != lo);
+                prev = hi;
+            }
+        } else {
+            const uint64_t e = b + 8 < n ? b + 8 : n;
+            for (uint64_t i = b; i < e; i++) {
+                const uint32_t c = (uint32_t)__ldg(sym + i);
+                heads += c != prev;
+                prev = c;
+            }
+        }
+    }
+    heads = __reduce_add_sync(0xffffffffu, (unsigned)heads);
+    if (lane_id() == 0 && heads) atomicAdd(reinterpret_cast<unsigned long long *>(&st->u[0]), heads);
+}
+
 }  // namespace lzb
 
 using namespace lzb;
+
+extern "C" int lzb_count_runs(const void *sym, int sym_bytes, uint64_t n, lzb_dstatus *st,
+                              void *stream) {
+    if (!st || (n && !sym) || (sym_bytes != 2 && sym_bytes != 4)) return LZB_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
+    if (n == 0) return LZB_OK;
+    const uint64_t ng = (n + 7) / 8;
+    const unsigned grid = (unsigned)umin64((ng + 255) / 256, (uint64_t)sms() * 8);
+    if (sym_bytes == 2) k_count_runs<uint16_t><<<grid, 256, 0, s>>>(static_cast<const uint16_t *>(sym), n, st);
+    else k_count_runs<uint32_t><<<grid, 256, 0, s>>>(static_cast<const uint32_t *>(sym), n, st);
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}
 
 extern "C" size_t lzb_rle_encode_scratch_bytes(uint64_t n) {
     // cap_runs is bounded by n

@@ -253,7 +253,7 @@ def compress_device(field: Field, eb: float, eb_mode: str = "rel", cap: int = 10
             continue
         N.raise_for(sq, "quantize")
         break
-    n_out, runs = sq.u[0], sq.u[1]
+    n_out = sq.u[0]
 
     chosen = resolve_workflow(workflow)
     if chosen is None:
@@ -292,6 +292,10 @@ def compress_device(field: Field, eb: float, eb_mode: str = "rel", cap: int = 10
                        "huff_encode")
         check_slots = [2]
     else:
+        N.check_rc(L.lzb_count_runs(_dev(codes), cb, n, stp + 3 * N.STATUS_BYTES, sp), "count_runs")
+        (sc,) = N.read_status(st[3 * N.STATUS_BYTES: 4 * N.STATUS_BYTES])
+        N.raise_for(sc, "count_runs")
+        runs = sc.u[0]
         extra = n // _MAX_RUN + 1 if n > _MAX_RUN else 0
         cap_runs = runs + extra
         vals = _pool.get("rle_vals", cap_runs * 4, dev)

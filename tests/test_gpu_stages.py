@@ -133,6 +133,23 @@ def test_rle_stage(golden, cuda):
         lzb.run_length_decode(np.array([1], np.uint32), np.array([0], np.uint32))
 
 
+def test_count_runs(cuda):
+    import torch
+    from paper_2105_12912_b200 import _native as N
+
+    L = N.lib()
+    rng = np.random.default_rng(15)
+    st = torch.zeros(N.STATUS_BYTES, dtype=torch.uint8, device="cuda")
+    for n in [1, 7, 8, 9, 4095, 4096, 100003]:
+        for dt, cb in [(np.uint16, 2), (np.uint32, 4)]:
+            s = rng.integers(0, 3, n).astype(dt)
+            s[: n // 3] = 1  # a long run at the start
+            d = torch.from_numpy(s.view(np.uint8).copy()).cuda()
+            N.check_rc(L.lzb_count_runs(d.data_ptr(), cb, n, st.data_ptr(), N.stream_ptr()), "count_runs")
+            (sr,) = N.read_status(st)
+            assert sr.code == 0 and sr.u[0] == len(O.rle_encode(s.astype(np.uint32))[0]), (n, cb)
+
+
 def test_quantize_stage_kats(golden, cuda):
     import paper_2105_12912_b200 as lzb
 
