@@ -290,6 +290,61 @@ __device__ __forceinline__ uint32_t q3_chunk(const Q3Params &p, uint64_t c, uint
     return n;
 }
 
+// Partial / unaligned chunks, out of line so the hot loop stays small in the
+// instruction cache; the 8-bit window counters are folded before returning.
+template <typename InT, typename SymT>
+__device__ __noinline__ Q3Res q3_chunk_slow(const Q3Params *pp, uint64_t c, uint32_t lane,
+                                            SymT *s_codes, uint64_t *stash, uint32_t wcount,
+                                            uint32_t *s_hist) {
+    Q3Warp<InT> t;
+    t.hw0 = t.hw1 = 0;
+    t.flags = 0;
+    Q3Res res;
+    res.n = q3_chunk<InT, SymT>(*pp, c, lane, s_codes, stash, wcount, t, s_hist, false, 0, res.first,
+                                res.last);
+    if (pp->cap >= 16) q3_hist_flush<SymT>(t.hw0, t.hw1, pp->r, s_hist, lane);
+    res.flags = t.flags;
+    return res;
+}
+
+__device__ __forceinline__ void q3_put_record(const Q3Params &p, uint64_t *stash, uint32_t wcount,
+                                              bool emit, uint64_t emit_pos, uint32_t rk, uint64_t gi,
+                                              int64_t dd) {
+    if (emit) {
+        const uint64_t wpos = emit_pos + rk;
+        if (wpos < p.out_capacity) {
+            p.records[2 * wpos] = gi;
+            p.records[2 * wpos + 1] = (uint64_t)dd;
+        }
+    } else if (wcount + rk < (uint32_t)kQ3Stash) {
+        stash[2 * (wcount + rk)] = gi;
+        stash[2 * (wcount + rk) + 1] = (uint64_t)dd;
+    }
+}
+
+// Any outlier pattern: ranks by a warp scan over rows, then each lane walks
+// its outlier bits (row0 then row1, x ascending = stream order).
+__device__ __forceinline__ uint32_t q3_outliers_general(const Q3Params &p, uint64_t *stash,
+                                                        uint32_t wcount, bool emit, uint64_t emit_pos,
+                                                        uint32_t lane, uint64_t gi0, uint64_t plane,
+                                                        uint32_t o0, uint32_t o1, const int32_t (&d0)[8],
+                                                        const int32_t (&d1)[8]) {
+    uint32_t r0, r1, total;
+    f3::row_ranks(__popc(o0), __popc(o1), lane, r0, r1, total);
+    for (int h = 0; h < 2; h++) {
+        uint32_t m = h ? o1 : o0, rk = h ? r1 : r0;
+        while (m) {
+            const uint32_t j = __ffs(m) - 1;
+            m &= m - 1;
+            int32_t dd = h ? d1[0] : d0[0];  // select without dynamic indexing
+#pragma unroll
+            for (int k = 1; k < 8; k++) dd = (j == (uint32_t)k) ? (h ? d1[k] : d0[k]) : dd;
+            q3_put_record(p, stash, wcount, emit, emit_pos, rk++, gi0 + (h ? plane : 0) + j, dd);
+        }
+    }
+    return total;
+}
+
 // Lean path for a FULL 8x8x8 chunk: no masks, no divisions.  The lane's two
 // input rows were prefetched into shared memory (`stg`, cp.async) one chunk
 // ahead.  gi0 = global index of this lane's row0 start, sbase = stream offset
@@ -308,7 +363,7 @@ __device__ __forceinline__ uint32_t q3_full(const Q3Params &p, const InT *stg, u
     bool ok = true;
     if constexpr (sizeof(InT) == 4) {
         const float4 *q = reinterpret_cast<const float4 *>(stg);
-        float4 a = q[0], b = q[1], c = q[2], d = q[3];
+        float4 a = q[0], b = q[32], c = q[64], d = q[96];
         float x0[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
         float x1[8] = {c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w};
 #pragma unroll
@@ -320,7 +375,7 @@ __device__ __forceinline__ uint32_t q3_full(const Q3Params &p, const InT *stg, u
         const double2 *q = reinterpret_cast<const double2 *>(stg);
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            double2 a = q[j], b = q[4 + j];
+            double2 a = q[32 * j], b = q[32 * (4 + j)];
             d0[2 * j] = f3::pq_fast(a.x, p.inv, ok);
             d0[2 * j + 1] = f3::pq_fast(a.y, p.inv, ok);
             d1[2 * j] = f3::pq_fast(b.x, p.inv, ok);
@@ -344,43 +399,19 @@ __device__ __forceinline__ uint32_t q3_full(const Q3Params &p, const InT *stg, u
         o0 |= (uint32_t)!i0 << j;
         o1 |= (uint32_t)!i1 << j;
     }
-    // outliers: ranks in stream order (usually only the chunk origin)
+    // outliers: ranks in stream order.  Common case: only the chunk origin
+    // (lane 0, row 0, x 0) -- one record written by lane 0.
     const uint32_t any = __ballot_sync(f3::kFull, (o0 | o1) != 0);
     uint32_t total = 0;
     if (any) {
-        uint32_t r0, r1;
         const bool origin_only =
             any == 1u && __shfl_sync(f3::kFull, (o0 == 1u && o1 == 0u) ? 1 : 0, 0);
         if (origin_only) {
-            r0 = 0;
-            r1 = 1;
             total = 1;
+            if (lane == 0) q3_put_record(p, stash, wcount, emit, emit_pos, 0, gi0, d0[0]);
         } else {
-            f3::row_ranks(__popc(o0), __popc(o1), lane, r0, r1, total);
-        }
-        if (o0 | o1) {
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const uint32_t om = h ? o1 : o0;
-                uint32_t rk = h ? r1 : r0;
-#pragma unroll
-                for (int j = 0; j < 8; j++) {
-                    if (!((om >> j) & 1u)) continue;
-                    const uint64_t gi = gi0 + (h ? plane : 0) + j;
-                    const int64_t dd = h ? d1[j] : d0[j];
-                    if (emit) {
-                        const uint64_t wpos = emit_pos + rk;
-                        if (wpos < p.out_capacity) {
-                            p.records[2 * wpos] = gi;
-                            p.records[2 * wpos + 1] = (uint64_t)dd;
-                        }
-                    } else if (wcount + rk < (uint32_t)kQ3Stash) {
-                        stash[2 * (wcount + rk)] = gi;
-                        stash[2 * (wcount + rk) + 1] = (uint64_t)dd;
-                    }
-                    rk++;
-                }
-            }
+            total = q3_outliers_general(p, stash, wcount, emit, emit_pos, lane, gi0, plane, o0, o1,
+                                        d0, d1);
         }
     }
     if (emit) return total;
@@ -425,18 +456,22 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // chunk c of the fast grid: full? + lane row0 global index + stream offset
+// Location of chunk (bx, by, bz) of the fast grid: full?, the lane's row0
+// global index and the chunk's stream offset (meaningful for full chunks,
+// where the stream offset is nx*ny*8*bz + nx*64*by + 512*bx).  Along a chunk
+// row the next location is an increment (q3_next).
 struct Q3Loc {
-    bool full;
+    bool full, row_full;
     uint64_t gi0, sbase;
 };
 
 __device__ __forceinline__ Q3Loc q3_loc(const Q3Params &p, uint64_t bx, uint64_t by, uint64_t bz,
-                                        uint32_t lane) {
+                                        uint64_t lane_off) {
     Q3Loc l;
-    l.full = p.vec_ok && (bx * 8 + 8 <= p.g.nx) && (by * 8 + 8 <= p.g.ny) && (bz * 8 + 8 <= p.g.nz);
+    l.row_full = p.vec_ok && (by * 8 + 8 <= p.g.ny) && (bz * 8 + 8 <= p.g.nz);
+    l.full = l.row_full && (bx * 8 + 8 <= p.g.nx);
     l.sbase = p.g.nx * p.g.ny * 8 * bz + p.g.nx * 64 * by + 512 * bx;
-    l.full = l.full && ((l.sbase & 7) == 0);
-    l.gi0 = bx * 8 + p.g.nx * ((by * 8 + (lane & 7)) + p.g.ny * (bz * 8 + (lane >> 3) * 2));
+    l.gi0 = bx * 8 + p.g.nx * (by * 8 + p.g.ny * (bz * 8)) + lane_off;
     return l;
 }
 
@@ -448,9 +483,9 @@ __device__ __forceinline__ void q3_prefetch(const Q3Params &p, const Q3Loc &l, u
     const InT *r1 = r0 + p.g.nx * p.g.ny;
     constexpr int V = 16 / sizeof(InT);  // values per 16-byte copy
 #pragma unroll
-    for (int k = 0; k < 8 / V; k++) {
-        cp_async16(saddr + 16 * k, r0 + V * k);
-        cp_async16(saddr + 16 * (8 / V + k), r1 + V * k);
+    for (int k = 0; k < 8 / V; k++) {  // piece-major: conflict-free 16-byte reads
+        cp_async16(saddr + 512 * k, r0 + V * k);
+        cp_async16(saddr + 512 * (8 / V + k), r1 + V * k);
     }
 }
 
@@ -469,7 +504,8 @@ __global__ void __launch_bounds__(kQ3Threads, 2) k_quantize3d8(const __grid_cons
     for (uint32_t i = threadIdx.x; i < kQ3Warps * 16 * 32; i += blockDim.x) s_col[i] = 0;
     for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
-    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage) + lane * kLaneStage;
+    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage) + lane * 16;
+    const uint64_t lane_off = p.g.nx * ((lane & 7) + p.g.ny * ((lane >> 3) * 2));
     const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(s_hist);
     // codes outside the 16-bin window (or books with cap < 16) go straight to s_hist
     const uint32_t colbase = p.cap >= 16
@@ -488,38 +524,40 @@ __global__ void __launch_bounds__(kQ3Threads, 2) k_quantize3d8(const __grid_cons
         const uint64_t c1 = umin64(c0 + kQ3TileChunks, p.nchunks);
         uint64_t *slot = p.slots + t * 2 * kQ3Slot;
         uint32_t wcount = 0;
-        uint64_t bx = c0 % p.g.nbx, rowc = c0 / p.g.nbx;
-        uint64_t by = rowc % p.g.nby, bz = rowc / p.g.nby;
-        Q3Loc cur = q3_loc(p, bx, by, bz, lane);
+        const uint64_t rowc = c0 / p.g.nbx;
+        uint32_t bx = (uint32_t)(c0 - rowc * p.g.nbx);
+        uint32_t by = (uint32_t)(rowc % p.g.nby), bz = (uint32_t)(rowc / p.g.nby);
+        const uint32_t nk = (uint32_t)(c1 - c0);
+        Q3Loc cur = q3_loc(p, bx, by, bz, lane_off);
         if (cur.full) q3_prefetch<InT>(p, cur, stage_s);
         cp_async_commit();
         uint32_t sb = 0;
-        for (uint64_t c = c0; c < c1; c++) {
+        for (uint32_t k = 0; k < nk; k++) {
             // prefetch the next chunk of the tile into the other stage buffer
-            if (++bx == p.g.nbx) {
+            Q3Loc nxt = cur;
+            if (++bx < (uint32_t)p.g.nbx) {  // same chunk row: increment
+                nxt.gi0 += 8;
+                nxt.sbase += 512;
+                nxt.full = nxt.row_full && (bx * 8 + 8 <= p.g.nx);
+            } else {
                 bx = 0;
-                if (++by == p.g.nby) {
+                if (++by == (uint32_t)p.g.nby) {
                     by = 0;
                     ++bz;
                 }
+                nxt = q3_loc(p, bx, by, bz, lane_off);
             }
-            Q3Loc nxt;
-            nxt.full = false;
-            if (c + 1 < c1) {
-                nxt = q3_loc(p, bx, by, bz, lane);
-                if (nxt.full) q3_prefetch<InT>(p, nxt, stage_s + (sb ^ 1) * 32 * kLaneStage);
-            }
+            if (k + 1 < nk && nxt.full) q3_prefetch<InT>(p, nxt, stage_s + (sb ^ 1) * 32 * kLaneStage);
             cp_async_commit();
             cp_async_wait1();  // this chunk's rows have landed
             uint32_t n = kQ3Redo;
             if (cur.full)
-                n = q3_full<InT, SymT>(p, reinterpret_cast<const InT *>(stage + sb * 32 * kLaneStage + lane * kLaneStage),
+                n = q3_full<InT, SymT>(p, reinterpret_cast<const InT *>(stage + sb * 32 * kLaneStage + lane * 16),
                                        cur.gi0, cur.sbase, lane, slot, wcount, colbase, hbase, false, 0);
             if (n == kQ3Redo) {
-                uint32_t f, l;
-                n = q3_chunk<InT, SymT>(p, c, lane, s_codes, slot, wcount, w, s_hist, false, 0, f, l);
-                // partial chunks: fold the 8-bit window counters right away
-                if (p.cap >= 16) q3_hist_flush<SymT>(w.hw0, w.hw1, p.r, s_hist, lane);
+                const Q3Res rr = q3_chunk_slow<InT, SymT>(&p, c0 + k, lane, s_codes, slot, wcount, s_hist);
+                n = rr.n;
+                w.flags |= rr.flags;
             }
             wcount += n;
             cur = nxt;

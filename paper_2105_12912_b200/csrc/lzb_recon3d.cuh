@@ -78,7 +78,7 @@ __device__ __forceinline__ bool r3_needs_wide(const R3Params &p, uint64_t r0, ui
 template <typename SymT, typename OutT, typename I>
 __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch, uint32_t k,
                                          uint64_t r0, uint64_t r1, uint32_t lane, OutT &vmin,
-                                         OutT &vmax, bool &overflow) {
+                                         OutT &vmax, bool &overflow, const SymT *stg = nullptr) {
     const uint32_t ly = lane & 7, lz0 = (lane >> 3) * 2;
     const SymT *cs = static_cast<const SymT *>(p.codes) + ch.base;
     I v0[8], v1[8];
@@ -92,7 +92,8 @@ __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch,
             I(&v)[8] = h ? v1 : v0;
             const SymT *src = cs + 8 * (ly + 8 * (lz0 + h));
             if constexpr (sizeof(SymT) == 2) {
-                uint4 a = __ldg(reinterpret_cast<const uint4 *>(src));
+                uint4 a = stg ? reinterpret_cast<const uint4 *>(stg)[32 * h]
+                              : __ldg(reinterpret_cast<const uint4 *>(src));
                 uint32_t w[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
@@ -100,8 +101,14 @@ __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch,
                     v[2 * j + 1] = (I)(int32_t)(w[j] >> 16) - p.r;
                 }
             } else {
-                uint4 a = __ldg(reinterpret_cast<const uint4 *>(src));
-                uint4 b = __ldg(reinterpret_cast<const uint4 *>(src) + 1);
+                uint4 a, b;
+                if (stg) {
+                    a = reinterpret_cast<const uint4 *>(stg)[32 * (2 * h)];
+                    b = reinterpret_cast<const uint4 *>(stg)[32 * (2 * h + 1)];
+                } else {
+                    a = __ldg(reinterpret_cast<const uint4 *>(src));
+                    b = __ldg(reinterpret_cast<const uint4 *>(src) + 1);
+                }
                 uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
                 for (int j = 0; j < 8; j++) v[j] = (I)(int64_t)w[j] - p.r;
@@ -176,9 +183,30 @@ __device__ __noinline__ void r3_chunk_wide(const R3Params *pp, uint64_t c, uint3
     *ovf = o;
 }
 
+// the lane's two code rows of a full chunk -> its stage slot (cp.async)
+template <typename SymT>
+__device__ __forceinline__ void r3_prefetch(const R3Params &p, const f3::Chunk &ch, uint32_t lane,
+                                            uint32_t saddr) {
+    const SymT *cs = static_cast<const SymT *>(p.codes) + ch.base;
+    const uint32_t ly = lane & 7, lz0 = (lane >> 3) * 2;
+    constexpr int V = 16 / sizeof(SymT);  // symbols per 16-byte copy
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int k = 0; k < 8 / V; k++)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr + 512 * (h * (8 / V) + k)),
+                         "l"(cs + 8 * (ly + 8 * (lz0 + h)) + V * k)
+                         : "memory");
+}
+
 template <typename SymT, typename OutT>
 __global__ void __launch_bounds__(kR3Threads, 2) k_reconstruct3d8(const __grid_constant__ R3Params p) {
-    const uint32_t lane = lane_id();
+    // per-warp double buffer of the next chunk's code rows (16 symbols per lane)
+    __shared__ __align__(16) SymT s_stage[kR3Warps][2][32 * 16];
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    // piece-major: 16-byte piece k of lane l at byte k * 512 + 16 l (conflict-free)
+    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(&s_stage[warp][0][0]) + lane * 16;
+    constexpr uint32_t kBuf = 32 * 16 * sizeof(SymT);
     OutT vmin = (OutT)INFINITY, vmax = (OutT)-INFINITY;
     bool overflow = false;
     while (true) {
@@ -189,19 +217,37 @@ __global__ void __launch_bounds__(kR3Threads, 2) k_reconstruct3d8(const __grid_c
         const uint64_t c0 = t * kR3TileChunks;
         const uint64_t c1 = umin64(c0 + kR3TileChunks, p.nchunks);
         const uint64_t r0 = p.tile_start[t], r1 = p.tile_start[t + 1];
+        f3::Chunk cur = f3::chunk_of(p.g, c0);
+        bool cur_pf = cur.full && (cur.base & 7) == 0;
+        if (cur_pf) r3_prefetch<SymT>(p, cur, lane, stage_s);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        uint32_t sb = 0;
         for (uint64_t c = c0; c < c1; c++) {
             const uint32_t k = (uint32_t)(c - c0);
+            f3::Chunk nxt;
+            bool nxt_pf = false;
+            if (c + 1 < c1) {
+                nxt = f3::chunk_of(p.g, c + 1);
+                nxt_pf = nxt.full && (nxt.base & 7) == 0;
+                if (nxt_pf) r3_prefetch<SymT>(p, nxt, lane, stage_s + (sb ^ 1) * kBuf);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
             if (r1 > r0 && r3_needs_wide(p, r0, r1, k)) {
                 OutT mmv[2] = {vmin, vmax};
                 r3_chunk_wide<SymT, OutT>(&p, c, k, r0, r1, lane, mmv, &overflow);
                 vmin = mmv[0];
                 vmax = mmv[1];
             } else {
-                const f3::Chunk ch = f3::chunk_of(p.g, c);
-                r3_chunk<SymT, OutT, int32_t>(p, ch, k, r0, r1, lane, vmin, vmax, overflow);
+                r3_chunk<SymT, OutT, int32_t>(p, cur, k, r0, r1, lane, vmin, vmax, overflow,
+                                              cur_pf ? reinterpret_cast<const SymT *>(reinterpret_cast<const unsigned char *>(&s_stage[warp][sb][0]) + lane * 16) : nullptr);
             }
+            cur = nxt;
+            cur_pf = nxt_pf;
+            sb ^= 1;
         }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         OutT a = __shfl_xor_sync(f3::kFull, vmin, o), b = __shfl_xor_sync(f3::kFull, vmax, o);
