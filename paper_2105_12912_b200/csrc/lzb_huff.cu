@@ -252,6 +252,345 @@ __global__ void k_huff_fixup(EncParams p) {
     }
 }
 
+// ----------------------------------------------------------------------------
+// K3 fast path (u16 symbols, code words <= 32 bits, table in shared memory):
+// warp-independent tiles, no CTA barriers, few shared atomics.  A warp tile
+// is 1024 symbols; lane l owns the 32 consecutive symbols [32 l, 32 l + 32),
+// i.e. the four 16-byte pieces 4l..4l+3 of the cp.async stage (stored
+// XOR-swizzled so the lane reads are conflict-free).  Tiles are statically
+// assigned (tile t to warp t mod NW of a persistent grid), so the next tile
+// is prefetched while the current one is packed.  Per tile:
+//   pass 1: bit count per lane (length table) -> warp scan -> the tile's
+//           aggregate is published for the look-back right away;
+//   pass 2: each lane packs its code words into a 32-bit accumulator and
+//           stores every completed word; only its first word (shared with
+//           the previous lane when it starts mid-word) and its last partial
+//           word go through red.shared.or;
+//   resolve the tile's global bit offset (decoupled look-back, usually ready),
+//   store the full words with the bit phase applied and keep the <= 2 partial
+//   boundary words (head / tail) for k_huff_fixup_w.
+// ----------------------------------------------------------------------------
+constexpr int kWSyms = 32;                 // symbols per lane
+constexpr int kWTile = 32 * kWSyms;        // 1024 symbols per warp tile
+constexpr int kWWarps = 8;
+
+__device__ __forceinline__ uint32_t sym16(const uint4 &v, int k) {
+    const uint32_t w = k < 2 ? v.x : k < 4 ? v.y : k < 6 ? v.z : v.w;
+    return (k & 1) ? (w >> 16) : (w & 0xFFFFu);
+}
+
+struct EncWParams {
+    const uint16_t *sym;
+    uint64_t n;
+    const uint8_t *lengths;
+    const uint64_t *codes;
+    uint32_t cap;
+    uint8_t *out;
+    uint64_t bit_offset;
+    lzb_dstatus *st;
+    uint32_t *cnt;         // per warp tile bit count (+1 zero entry)
+    uint16_t *lcnt;        // per warp tile x lane: bits of the lane's 32 symbols
+    uint64_t *toff;        // exclusive scan of cnt: tile bit offsets, toff[ntiles] = total
+    uint64_t *lb;          // scan look-back words
+    unsigned int *ticket;  // scan ticket
+    uint32_t *frag;        // per warp tile: [head partial word, tail partial word]
+    uint64_t ntiles;
+    uint32_t wwords;       // per-warp word buffer (u32)
+};
+
+// Pass A: bit count of every warp tile (order-independent, so lane l simply
+// takes the 16-byte pieces l, l+32, l+64, l+96: coalesced 16-byte loads).
+// Also the DataError checks (symbol >= cap, symbol without a code word).
+__global__ void __launch_bounds__(256) k_huff_count_w(const __grid_constant__ EncWParams p) {
+    __shared__ uint8_t s_len[4096];
+    for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) s_len[i] = p.lengths[i];
+    __syncthreads();
+    const uint32_t lane = lane_id();
+    const uint64_t NW = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t capm1 = p.cap - 1;
+    const bool aligned_in = (reinterpret_cast<uintptr_t>(p.sym) & 15) == 0;
+    uint32_t mx = 0, mnL = 64;
+    for (uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; t < p.ntiles; t += NW) {
+        const bool full = aligned_in && (t + 1) * kWTile <= p.n;
+        uint32_t pc[4] = {0, 0, 0, 0};  // bits of pieces lane, lane+32, lane+64, lane+96
+        if (full) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(p.sym + t * kWTile);
+            uint4 v[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) v[j] = __ldcs(src + j * 32 + lane);
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+                const uint32_t sv = sym16(v[i >> 3], i & 7);
+                const uint32_t L = s_len[sv < capm1 ? sv : capm1];
+                mx = sv > mx ? sv : mx;
+                mnL = L < mnL ? L : mnL;
+                pc[i >> 3] += L;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                for (uint32_t k = 0; k < 8; k++) {
+                    const uint64_t g = t * kWTile + (uint64_t)(j * 32 + lane) * 8 + k;
+                    if (g >= p.n) break;
+                    const uint32_t sv = p.sym[g];
+                    const uint32_t L = s_len[sv < capm1 ? sv : capm1];
+                    mx = sv > mx ? sv : mx;
+                    mnL = L < mnL ? L : mnL;
+                    pc[j] += L;
+                }
+            }
+        }
+        // encode lane l owns pieces 4l..4l+3: piece q sits in lane q & 31, slot q >> 5 = l >> 3
+        const uint32_t p01 = pc[0] | (pc[1] << 16), p23 = pc[2] | (pc[3] << 16);
+        uint32_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const uint32_t src = 4 * (lane & 7) + k;
+            const uint32_t a01 = __shfl_sync(0xffffffffu, p01, src);
+            const uint32_t a23 = __shfl_sync(0xffffffffu, p23, src);
+            const uint32_t sel = lane >> 3;
+            const uint32_t w = sel < 2 ? a01 : a23;
+            mine += (sel & 1) ? (w >> 16) : (w & 0xFFFFu);
+        }
+        p.lcnt[t * 32 + lane] = (uint16_t)mine;
+        const uint32_t nb = __reduce_add_sync(0xffffffffu, mine);
+        if (lane == 0) p.cnt[t] = nb;
+    }
+    const bool bad = mx > capm1 || mnL == 0;
+    if (__any_sync(0xffffffffu, bad) && lane == 0) set_status(p.st, LZB_E_DATA);
+}
+
+// exclusive scan of the ntiles + 1 tile counts -> u64 bit offsets
+__global__ void __launch_bounds__(256) k_huff_scan_w(const __grid_constant__ EncWParams p) {
+    __shared__ uint64_t s_t, s_ex;
+    __shared__ uint64_t s_scan[33];
+    const uint64_t n = p.ntiles + 1;
+    if (threadIdx.x == 0) s_t = atomicAdd(p.ticket, 1u);
+    __syncthreads();
+    const uint64_t t = s_t;
+    const uint64_t base = t * 2048 + (uint64_t)threadIdx.x * 8;
+    uint64_t v[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        v[k] = base + k < n ? p.cnt[base + k] : 0;
+        sum += v[k];
+    }
+    uint64_t total;
+    const uint64_t off = block_exclusive_scan<uint64_t>(sum, s_scan, &total);
+    if ((threadIdx.x >> 5) == 0) {
+        const uint64_t ex = lookback_warp(p.lb, t, total);
+        if (lane_id() == 0) s_ex = ex;
+    }
+    __syncthreads();
+    uint64_t run = s_ex + off;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        if (base + k < n) p.toff[base + k] = run;
+        run += v[k];
+    }
+}
+
+// stage slot of 16-byte piece q (0..127): conflict-free for lane l reading 4l+k
+__device__ __forceinline__ uint32_t wswz(uint32_t q) { return q ^ ((q >> 3) & 7u); }
+
+// Pack one lane's 32 code words at tile-relative bit `off`: a 32-bit
+// accumulator, completed words stored with predicated st.shared (interior
+// words belong to this lane alone) or red.shared.or (the first word when the
+// lane starts mid-word); the final partial word is OR-ed.  No branches, so
+// the warp never diverges.
+// Pack one lane's 32 code words at tile-relative bit `off` with a 32-bit
+// accumulator.  Every word the lane COMPLETES is stored plainly (only the lane
+// holding a word's last bit completes it; bits of earlier lanes in that word
+// are zero here and are OR-ed in afterwards); the lane's final partial word is
+// returned for a red.shared.or after a __syncwarp.  Branch-free.
+template <bool FULL>
+__device__ __forceinline__ void enc_pack_lane(const uint4 (&v)[4], uint32_t nv, uint32_t off,
+                                              uint32_t words_s, const uint64_t *s_tab,
+                                              uint32_t capm1, uint32_t &last_addr,
+                                              uint32_t &last_val, uint32_t &last_n) {
+    uint32_t n = off & 31, cur = 0;
+    uint32_t waddr = words_s + ((off >> 5) << 2);
+#pragma unroll
+    for (int i = 0; i < kWSyms; i++) {
+        const uint32_t sv = sym16(v[i >> 3], i & 7);
+        const uint64_t e = s_tab[sv < capm1 ? sv : capm1];
+        uint32_t L = (uint32_t)(e >> 32);
+        uint32_t c = (uint32_t)e;  // left-aligned; 0 when L == 0
+        if (!FULL) {
+            L = (uint32_t)i < nv ? L : 0u;
+            c = L ? c : 0u;
+        }
+        cur |= c >> n;
+        const uint32_t nn = n + L;
+        const uint32_t f = nn >= 32 ? 1u : 0u;
+        asm volatile("{\n\t.reg .pred ps;\n\tsetp.ne.u32 ps, %2, 0;\n\t@ps st.shared.u32 [%0], %1;\n\t}"
+                     ::"r"(waddr), "r"(cur), "r"(f)
+                     : "memory");
+        const uint32_t rem = __funnelshift_lc(0u, c, 32 - n);  // bits that did not fit
+        cur = f ? rem : cur;
+        waddr += f << 2;
+        n = nn - (f << 5);
+    }
+    last_addr = waddr;
+    last_val = cur;
+    last_n = n;
+}
+
+__global__ void __launch_bounds__(kWWarps * 32, 2) k_huff_encode_w(const __grid_constant__ EncWParams p) {
+    extern __shared__ __align__(16) unsigned char ew_smem[];
+    // [table: cap x u64 (left-aligned code | len << 32)][lens: cap x u8]
+    // [stage: warps x 2 x 2 KB][words: warps x wwords u32]
+    uint64_t *s_tab = reinterpret_cast<uint64_t *>(ew_smem);
+    uint8_t *s_len = reinterpret_cast<uint8_t *>(s_tab + p.cap);
+    unsigned char *stage_all = ew_smem + (((size_t)p.cap * 9 + 15) & ~(size_t)15);
+    uint32_t *words_all = reinterpret_cast<uint32_t *>(stage_all + kWWarps * 2 * kWTile * 2);
+    for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) {
+        const uint32_t L = p.lengths[i];
+        const uint32_t cal = (L && L <= 32) ? (uint32_t)(p.codes[i] << (32 - L)) : 0u;
+        s_tab[i] = (uint64_t)cal | ((uint64_t)L << 32);
+        s_len[i] = (uint8_t)L;
+    }
+    __syncthreads();
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    const uint64_t NW = (uint64_t)gridDim.x * kWWarps;
+    uint64_t t = (uint64_t)blockIdx.x * kWWarps + warp;
+    unsigned char *stage = stage_all + warp * 2 * kWTile * 2;
+    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+    uint32_t *words = words_all + warp * p.wwords;
+    const uint32_t words_s = (uint32_t)__cvta_generic_to_shared(words);
+    const uint32_t capm1 = p.cap - 1;
+    const bool aligned_out = (reinterpret_cast<uintptr_t>(p.out) & 3) == 0;
+    const bool aligned_in = (reinterpret_cast<uintptr_t>(p.sym) & 15) == 0;
+
+    auto is_full = [&](uint64_t tt) { return aligned_in && (tt + 1) * kWTile <= p.n; };
+    auto prefetch = [&](uint64_t tt, uint32_t buf) {
+        const unsigned char *src = reinterpret_cast<const unsigned char *>(p.sym + tt * kWTile);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint32_t q = j * 32 + lane;  // coalesced global pieces
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(stage_s + buf * kWTile * 2 + wswz(q) * 16),
+                         "l"(src + q * 16)
+                         : "memory");
+        }
+    };
+    if (t < p.ntiles && is_full(t)) prefetch(t, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    uint32_t sb = 0;
+    // the lane count and tile offset are loaded one tile ahead (latency)
+    uint32_t nb_nx = t < p.ntiles ? p.lcnt[t * 32 + lane] : 0u;
+    uint64_t ex_nx = t < p.ntiles ? p.toff[t] : 0ull;
+    for (; t < p.ntiles; t += NW) {
+        const uint64_t tn = t + NW;
+        const uint32_t nb = nb_nx;
+        const uint64_t ex = ex_nx;
+        if (tn < p.ntiles) {
+            nb_nx = p.lcnt[tn * 32 + lane];
+            ex_nx = p.toff[tn];
+            if (is_full(tn)) prefetch(tn, sb ^ 1);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        const bool full = is_full(t);
+        const uint64_t b0 = t * kWTile + (uint64_t)lane * kWSyms;
+        // ---- the lane's 32 symbols ----
+        uint4 v[4];
+        uint32_t nv = kWSyms;
+        if (full) {
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                v[k] = *reinterpret_cast<const uint4 *>(stage + sb * kWTile * 2 + wswz(4 * lane + k) * 16);
+        } else {
+            nv = b0 >= p.n ? 0u : (uint32_t)umin64(kWSyms, p.n - b0);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                uint32_t w[4];
+#pragma unroll
+                for (int h = 0; h < 4; h++) {
+                    const uint32_t i0 = 8 * k + 2 * h;
+                    const uint32_t lo = i0 < nv ? (uint32_t)p.sym[b0 + i0] : 0u;
+                    const uint32_t hi = i0 + 1 < nv ? (uint32_t)p.sym[b0 + i0 + 1] : 0u;
+                    w[h] = lo | (hi << 16);
+                }
+                v[k] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+        // ---- lane bit offsets from the count pass ----
+        uint32_t inc = nb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += a;
+        }
+        const uint32_t tile_bits = __shfl_sync(0xffffffffu, inc, 31);
+        const uint32_t off = inc - nb;
+        const uint32_t nwords = (tile_bits + 31) >> 5;
+        for (uint32_t i = lane; i <= nwords; i += 32) words[i] = 0;
+        __syncwarp();
+        // ---- pass 2: accumulate, store completed words (branch-free) ----
+        uint32_t la, lv, ln;
+        if (full) enc_pack_lane<true>(v, kWSyms, off, words_s, s_tab, capm1, la, lv, ln);
+        else enc_pack_lane<false>(v, nv, off, words_s, s_tab, capm1, la, lv, ln);
+        __syncwarp();
+        if (ln) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(la), "r"(lv) : "memory");
+        __syncwarp();
+        // ---- store with the tile's bit phase ----
+        const uint64_t G = ex + p.bit_offset;
+        const uint32_t sft = (uint32_t)(G & 31);
+        const uint64_t wbase = G >> 5;
+        const uint64_t endbit = G + tile_bits;
+        const uint32_t nout = tile_bits ? (uint32_t)(((endbit + 31) >> 5) - wbase) : 0u;
+        for (uint32_t jw = lane; jw < nout; jw += 32) {
+            const uint32_t cw = jw < nwords ? words[jw] : 0u;
+            const uint32_t pw = jw > 0 ? words[jw - 1] : 0u;
+            const uint32_t val = sft ? ((pw << (32 - sft)) | (cw >> sft)) : cw;
+            const uint64_t gw = wbase + jw;
+            const bool head = jw == 0 && sft != 0;
+            const bool tail = jw == nout - 1 && (endbit & 31) != 0;
+            if (!head && !tail) {
+                if (aligned_out) reinterpret_cast<uint32_t *>(p.out)[gw] = bswap32(val);
+                else store_word_bytes(p.out, gw * 4, val, ~0ull);
+            } else {
+                // a single-word tile keeps its one partial word as the head
+                if (head) p.frag[2 * t] = val;
+                else p.frag[2 * t + 1] = val;
+            }
+        }
+        __syncwarp();
+        sb ^= 1;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// Partial boundary words of the warp tiles.  Tile t covers global bits
+// [G_t, E_t) (inclusive look-back prefixes + bit_offset).  A partial head
+// word of t (G_t % 32 != 0) is shared with the partial tail of t-1 (every
+// tile but the last spans > 32 bits), so the head owner writes both; a
+// partial tail is written by its own tile only when no tile follows.
+__global__ void k_huff_fixup_w(const __grid_constant__ EncWParams p) {
+    const uint64_t total = p.bit_offset + p.toff[p.ntiles];
+    const uint64_t nbytes = (total + 7) / 8;
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.st->u[0] = p.toff[p.ntiles];
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < p.ntiles;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t G = p.bit_offset + p.toff[t];
+        const uint64_t E = p.bit_offset + p.toff[t + 1];
+        if (E == G) continue;
+        const uint64_t hw = G >> 5, tw = (E - 1) >> 5;
+        const bool head = (G & 31) != 0;
+        const bool tail = (E & 31) != 0 && !(head && tw == hw);
+        if (head) {
+            uint32_t v = p.frag[2 * t];
+            if (t > 0) {  // the previous tile's partial tail (or its single-word head)
+                const uint64_t Gp = p.bit_offset + p.toff[t - 1];
+                const bool prev_single = (Gp & 31) != 0 && (Gp >> 5) == hw;
+                v |= prev_single ? p.frag[2 * (t - 1)] : p.frag[2 * (t - 1) + 1];
+            }
+            store_word_bytes(p.out, hw * 4, v, nbytes);
+        }
+        if (tail && t + 1 == p.ntiles) store_word_bytes(p.out, tw * 4, p.frag[2 * t + 1], nbytes);
+    }
+}
+
 // ============================================================================
 // K5 decode
 // ============================================================================
@@ -940,7 +1279,63 @@ extern "C" size_t lzb_huff_encode_scratch_bytes(uint64_t n) {
     s.take<uint64_t>(nt ? nt : 1);
     s.take<unsigned int>(4);
     s.take<uint64_t>(4 * (nt ? nt : 1));
-    return s.bytes();
+    ScratchSize w;  // warp-tile path
+    uint64_t ntw = (n + kWTile - 1) / kWTile;
+    w.take<uint32_t>(ntw + 1);
+    w.take<uint16_t>(32 * (ntw ? ntw : 1));
+    w.take<uint64_t>(ntw + 1);
+    w.take<uint64_t>((ntw + 1 + 2047) / 2048 + 1);
+    w.take<unsigned int>(4);
+    w.take<uint32_t>(2 * (ntw ? ntw : 1));
+    return s.bytes() > w.bytes() ? s.bytes() : w.bytes();
+}
+
+static int huff_encode_w(const void *sym, uint64_t n, const uint8_t *lengths, const uint64_t *codes,
+                         uint32_t cap, uint32_t maxlen, uint8_t *out, uint64_t bit_offset,
+                         lzb_dstatus *st, void *scratch, size_t scratch_bytes, cudaStream_t s) {
+    const uint64_t ntw = (n + kWTile - 1) / kWTile;
+    Scratch sc(scratch, scratch_bytes);
+    EncWParams p;
+    const uint64_t nscan = (ntw + 1 + 2047) / 2048;
+    p.cnt = sc.take<uint32_t>(ntw + 1);
+    p.lcnt = sc.take<uint16_t>(32 * ntw);
+    p.toff = sc.take<uint64_t>(ntw + 1);
+    p.lb = sc.take<uint64_t>(nscan + 1);
+    p.ticket = sc.take<unsigned int>(4);
+    p.frag = sc.take<uint32_t>(2 * ntw);
+    if (!p.frag) return LZB_E_ARG;
+    LZB_CUDA_TRY(cudaMemsetAsync(p.lb, 0, (nscan + 1) * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.ticket, 0, 4 * sizeof(unsigned int), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.cnt + ntw, 0, sizeof(uint32_t), s));
+    p.sym = static_cast<const uint16_t *>(sym);
+    p.n = n;
+    p.lengths = lengths;
+    p.codes = codes;
+    p.cap = cap;
+    p.out = out;
+    p.bit_offset = bit_offset;
+    p.st = st;
+    p.ntiles = ntw;
+    p.wwords = (32 * maxlen + 2 + 3) & ~3u;
+    const size_t smem = (((size_t)cap * 9 + 15) & ~(size_t)15) + (size_t)kWWarps * 2 * kWTile * 2 +
+                        (size_t)kWWarps * p.wwords * 4;
+    LZB_CUDA_TRY(cudaFuncSetAttribute(k_huff_encode_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_huff_encode_w, kWWarps * 32, smem));
+    if (per_sm < 1) return LZB_E_ARG;
+    uint64_t grid = (uint64_t)dev_sms() * per_sm;
+    const uint64_t need = (ntw + kWWarps - 1) / kWWarps;
+    if (grid > need) grid = need;
+    const int sms = dev_sms();
+    k_huff_count_w<<<(unsigned)umin64((ntw + 7) / 8, (uint64_t)sms * 8), 256, 0, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    k_huff_scan_w<<<(unsigned)nscan, 256, 0, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    k_huff_encode_w<<<(unsigned)grid, kWWarps * 32, smem, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    k_huff_fixup_w<<<(unsigned)umin64((ntw + 255) / 256, 4096), 256, 0, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
 }
 
 static int huff_encode_impl(const void *sym, int sym_bytes, uint64_t n, const uint8_t *lengths,
@@ -953,6 +1348,10 @@ static int huff_encode_impl(const void *sym, int sym_bytes, uint64_t n, const ui
     LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     if (n == 0) return LZB_OK;
     if (!sym || !out) return LZB_E_ARG;
+    if (sym_bytes == 2 && maxlen >= 1 && maxlen <= 32 && cap <= 4096 &&
+        (reinterpret_cast<uintptr_t>(sym) & 1) == 0)
+        return huff_encode_w(sym, n, lengths, codes, cap, maxlen, out, bit_offset, st, scratch,
+                             scratch_bytes, s);
     uint64_t nt = (n + kETile - 1) / kETile;
     Scratch sc(scratch, scratch_bytes);
     EncParams p;
