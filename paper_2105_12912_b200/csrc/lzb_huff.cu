@@ -611,6 +611,9 @@ struct DecTables {
     // decoded from the 12-bit window (up to 7): count | bits consumed << 3.
     uint16_t lutc[kLutSize];
     uint8_t lut1[kLutSize];  // length of the first code word (0: > 12 bits or invalid)
+    // Six-symbol LUT for the final decode (u16 books): the code words greedily
+    // decoded from the 12-bit window, up to six: s[0..5], then n | used << 3.
+    uint4 lut6[kLutSize];
     uint64_t first[65];
     uint64_t cnt[65];
     uint32_t off[65];
@@ -896,6 +899,27 @@ __global__ void k_dec_tables(const uint8_t *lengths, uint32_t cap, uint32_t maxl
         }
         tab->lutc[v] = (uint16_t)(cn | (cu << 3));
         tab->lut1[v] = (uint8_t)(n ? ((e >> 2) & 15u) : 0u);
+        // six-symbol entry
+        uint32_t sy[6] = {0, 0, 0, 0, 0, 0};
+        uint32_t su = 0, sn = 0;
+        if (cap <= 65536) {
+            while (sn < 6) {
+                bool found = false;
+                for (uint32_t L = 1; L + su <= (uint32_t)kLutBits && L <= s_max; L++) {
+                    const uint32_t code = (v >> (kLutBits - su - L)) & ((1u << L) - 1u);
+                    const uint64_t f = tab->first[L], k = tab->cnt[L];
+                    if (k && code >= f && code - f < k) {
+                        sy[sn++] = syms[tab->off[L] + (uint32_t)(code - f)];
+                        su += L;
+                        found = true;
+                        break;
+                    }
+                }
+                if (!found) break;
+            }
+        }
+        tab->lut6[v] = make_uint4(sy[0] | (sy[1] << 16), sy[2] | (sy[3] << 16), sy[4] | (sy[5] << 16),
+                                  sn | (su << 3));
     }
 }
 
@@ -1223,6 +1247,167 @@ __global__ void __launch_bounds__(kFThreads) k_dec_final(DecParams p) {
     }
 }
 
+// Final decode, u16 symbols: lanes decode their subsequences in lock-step
+// rounds of kRK symbols.  A 12-bit lookup yields up to six symbols (lut6),
+// written to the lane's stage row; the first round starts at column
+// (offset & 7) so every later round is 8-symbol aligned in the output and the
+// warp writes the 32 rows with 16-byte stores (only a lane's first and last
+// pieces are partial).  The 4-word bit window advances without branches; a
+// lane prefetches its stream four 128-byte lines ahead into L1.
+constexpr int kF6Threads = 512;
+constexpr int kRK = 64;          // symbols per lane per round
+constexpr int kRow = kRK + 8;    // stage row (u16): overflow of <= 5 symbols + slack
+
+struct Win6 {
+    uint64_t wi;                  // word index of w0
+    uint32_t w0, w1, w2, w3, sh;  // w3 raw (byte-swapped when it moves to w2)
+    __device__ __forceinline__ void init(const DecParams &p, uint64_t q) {
+        const uint64_t a = q + p.head;
+        wi = a >> 5;
+        sh = (uint32_t)(a & 31);
+        w0 = bswap_load(p, wi);
+        w1 = bswap_load(p, wi + 1);
+        w2 = bswap_load(p, wi + 2);
+        w3 = wi + 3 < p.nwords ? __ldg(&p.words[wi + 3]) : 0u;
+    }
+    __device__ __forceinline__ uint32_t peek12() const {
+        return __funnelshift_l(w1, w0, sh) >> (32 - kLutBits);
+    }
+    __device__ __forceinline__ void consume(const DecParams &p, uint32_t L) {  // L <= 32
+        sh += L;
+        const bool adv = sh >= 32;
+        if (adv) {  // predicated moves; the load is issued for ~2 words later
+            sh -= 32;
+            wi++;
+            w0 = w1;
+            w1 = w2;
+            w2 = bswap32(w3);
+            w3 = wi + 3 < p.nwords ? __ldg(&p.words[wi + 3]) : 0u;
+            if (((wi + 3) & 31) == 0 && wi + 131 < p.nwords)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(&p.words[wi + 131]));
+        }
+    }
+};
+
+__global__ void __launch_bounds__(kF6Threads, 1) k_dec_final6(DecParams p) {
+    extern __shared__ __align__(16) unsigned char f6_smem[];
+    uint4 *s_lut = reinterpret_cast<uint4 *>(f6_smem);
+    uint8_t *s_l1 = reinterpret_cast<uint8_t *>(s_lut + kLutSize);
+    uint16_t *s_stage = reinterpret_cast<uint16_t *>(s_l1 + kLutSize);
+    uint64_t *s_base = reinterpret_cast<uint64_t *>(s_stage + (kF6Threads / 32) * 32 * kRow);
+    uint32_t *s_cs = reinterpret_cast<uint32_t *>(s_base + kF6Threads);  // col start | col end << 16
+    __shared__ DecCanon s_can;
+    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) {
+        s_lut[i] = p.tab->lut6[i];
+        s_l1[i] = p.tab->lut1[i];
+    }
+    load_canon(s_can, p.tab);
+    __syncthreads();
+    if (p.st->code) return;  // corrupt stream: leave the output untouched
+    const DecCanon *tab = &s_can;
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    uint16_t *out = static_cast<uint16_t *>(p.out);
+    const bool vec_out = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    uint16_t *row = s_stage + (warp * 32 + lane) * kRow;
+    const uint32_t row_s = (uint32_t)__cvta_generic_to_shared(row);
+    uint64_t *wbase = s_base + warp * 32;
+    uint32_t *wcs = s_cs + warp * 32;
+    const uint64_t tstride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t tb = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); tb < p.T;
+         tb += tstride) {
+        const uint64_t t = tb + lane;
+        Win6 r;
+        uint64_t t0 = 0, base = 0;
+        uint32_t rel = 0, stop = 0, k = 0, cstart = 0;
+        bool live = false;
+        if (t < p.T) {
+            const uint32_t e = p.ent0[t];
+            if (e != kExitInvalid && e != kExitEnd) {
+                t0 = t * p.S;
+                stop = (uint32_t)(((t == p.T - 1) ? p.bit_len : umin64(t0 + p.S, p.bit_len)) - t0);
+                rel = e;
+                r.init(p, t0 + rel);
+                const uint64_t o = p.off0[t];
+                cstart = k = (uint32_t)(o & 7);
+                base = o - k;
+                live = rel < stop;
+            }
+        }
+        const uint32_t lim = stop >= (uint32_t)kLutBits ? stop - kLutBits : 0;
+        bool any_live = __any_sync(0xffffffffu, live);
+        while (any_live) {
+            bool go = live && k < (uint32_t)kRK;
+            while (__any_sync(0xffffffffu, go)) {
+                if (go) {
+                    const uint32_t pk = r.peek12();
+                    const uint4 e = s_lut[pk];
+                    uint32_t n = e.w & 7u, adv = e.w >> 3;
+                    uint32_t s01 = e.x;
+                    if (n == 0 || rel > lim) {  // long code word, invalid prefix or stream tail
+                        uint32_t L = s_l1[pk], sym = e.x & 0xFFFFu;
+                        if (!L) L = decode_long(p, tab, t0 + rel, sym);
+                        n = 1;
+                        adv = L;
+                        s01 = sym;
+                        if (L == 0) {  // cannot happen after a successful map pass
+                            n = 0;
+                            adv = 0;
+                            rel = stop;
+                        }
+                    }
+                    const uint32_t a = row_s + 2 * k;
+                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)s01));
+                    asm volatile("st.shared.u16 [%0+2], %1;" ::"r"(a), "h"((unsigned short)(s01 >> 16)));
+                    asm volatile("st.shared.u16 [%0+4], %1;" ::"r"(a), "h"((unsigned short)e.y));
+                    asm volatile("st.shared.u16 [%0+6], %1;" ::"r"(a), "h"((unsigned short)(e.y >> 16)));
+                    asm volatile("st.shared.u16 [%0+8], %1;" ::"r"(a), "h"((unsigned short)e.z));
+                    asm volatile("st.shared.u16 [%0+10], %1;" ::"r"(a), "h"((unsigned short)(e.z >> 16)));
+                    k += n;
+                    rel += adv;
+                    if (adv <= 32) r.consume(p, adv);
+                    else r.init(p, t0 + rel);
+                    go = rel < stop && k < (uint32_t)kRK;
+                }
+            }
+            live = live && rel < stop;
+            // ---- write-out of the round: columns [cstart, min(k, kRK)) of each row ----
+            const uint32_t cend = k < (uint32_t)kRK ? k : (uint32_t)kRK;
+            wbase[lane] = base;
+            wcs[lane] = cstart | (cend << 16);
+            __syncwarp();
+#pragma unroll
+            for (int m = 0; m < (32 * kRK / 8) / 32; m++) {
+                const uint32_t i = m * 32 + lane;
+                const uint32_t rw = i / (kRK / 8), c0 = (i % (kRK / 8)) * 8;
+                const uint32_t cs = wcs[rw];
+                const uint32_t lo = cs & 0xFFFFu, hi = cs >> 16;
+                if (c0 + 8 <= lo || c0 >= hi) continue;
+                const uint64_t ob = wbase[rw] + c0;
+                const uint16_t *src = s_stage + (warp * 32 + rw) * kRow + c0;
+                if (vec_out && c0 >= lo && c0 + 8 <= hi && ob + 8 <= p.count) {
+                    *reinterpret_cast<uint4 *>(out + ob) = *reinterpret_cast<const uint4 *>(src);
+                } else {
+                    for (uint32_t c = 0; c < 8; c++)
+                        if (c0 + c >= lo && c0 + c < hi && ob + c < p.count) out[ob + c] = src[c];
+                }
+            }
+            __syncwarp();
+            // carry the overflow (<= 5 symbols) to the next round
+            if (k > (uint32_t)kRK) {
+                for (uint32_t c = kRK; c < k; c++) row[c - kRK] = row[c];
+            }
+            k = k > (uint32_t)kRK ? k - kRK : 0u;
+            base += kRK;
+            cstart = 0;
+            __syncwarp();
+            any_live = __any_sync(0xffffffffu, live || k > 0);
+            if (!live && k > 0) {  // leftover overflow of a finished lane: one more round
+                // handled by the next iteration: go stays false, write-out flushes [0, k)
+            }
+        }
+    }
+}
+
 // ----------------------------------------------------------------------------
 struct DecLayout {
     uint32_t S, P, G;
@@ -1497,9 +1682,17 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
     {
         const unsigned fg = (unsigned)umin64((L.T + kFThreads - 1) / kFThreads, (uint64_t)sms * 4);
         const size_t fsm = kLutSize * sizeof(uint64_t) + (size_t)(kFThreads / 32) * 32 * (kStage + 1) * sym_bytes;
-        auto kern = sym_bytes == 2 ? k_dec_final<uint16_t> : k_dec_final<uint32_t>;
-        LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-        kern<<<fg, kFThreads, fsm, s>>>(p);
+        if (sym_bytes == 2 && cap <= 65536) {
+            const size_t f6 = (size_t)kLutSize * 17 + (size_t)kF6Threads * kRow * 2 +
+                              (size_t)kF6Threads * 12;
+            LZB_CUDA_TRY(cudaFuncSetAttribute(k_dec_final6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f6));
+            const unsigned g6 = (unsigned)umin64((L.T + kF6Threads - 1) / kF6Threads, (uint64_t)sms);
+            k_dec_final6<<<g6, kF6Threads, f6, s>>>(p);
+        } else {
+            auto kern = sym_bytes == 2 ? k_dec_final<uint16_t> : k_dec_final<uint32_t>;
+            LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+            kern<<<fg, kFThreads, fsm, s>>>(p);
+        }
     }
     LZB_LAUNCH_CHECK();
     return LZB_OK;
