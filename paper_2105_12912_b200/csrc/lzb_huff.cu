@@ -1247,16 +1247,18 @@ __global__ void __launch_bounds__(kFThreads) k_dec_final(DecParams p) {
     }
 }
 
-// Final decode, u16 symbols: lanes decode their subsequences in lock-step
-// rounds of kRK symbols.  A 12-bit lookup yields up to six symbols (lut6),
-// written to the lane's stage row; the first round starts at column
-// (offset & 7) so every later round is 8-symbol aligned in the output and the
-// warp writes the 32 rows with 16-byte stores (only a lane's first and last
-// pieces are partial).  The 4-word bit window advances without branches; a
-// lane prefetches its stream four 128-byte lines ahead into L1.
+// Final decode, u16 symbols.  Lanes decode their subsequences in lock-step
+// batches of kFSteps lookups (every live lane steps each time, no waiting for
+// slower lanes); a 12-bit lookup yields up to six symbols (lut6), written to
+// the lane's stage row.  After each batch the warp flushes every row's
+// complete 8-symbol pieces with 16-byte stores: a lane's output offset is
+// made 8-aligned by starting its row at column (offset & 7), so only its very
+// first and last pieces are partial.  Pieces are distributed over the lanes
+// by a warp scan of the per-row piece counts.  The 4-word bit window advances
+// without branches, and each lane prefetches its stream 512 bytes ahead.
 constexpr int kF6Threads = 512;
-constexpr int kRK = 64;          // symbols per lane per round
-constexpr int kRow = kRK + 8;    // stage row (u16): overflow of <= 5 symbols + slack
+constexpr int kFSteps = 8;       // lookups per batch (<= 48 symbols per lane)
+constexpr int kRow = 64 + 8;     // stage row (u16): carry <= 7 + 48 symbols + slack
 
 struct Win6 {
     uint64_t wi;                  // word index of w0
@@ -1276,16 +1278,16 @@ struct Win6 {
     __device__ __forceinline__ void consume(const DecParams &p, uint32_t L) {  // L <= 32
         sh += L;
         const bool adv = sh >= 32;
-        if (adv) {  // predicated moves; the load is issued for ~2 words later
-            sh -= 32;
-            wi++;
-            w0 = w1;
-            w1 = w2;
-            w2 = bswap32(w3);
-            w3 = wi + 3 < p.nwords ? __ldg(&p.words[wi + 3]) : 0u;
-            if (((wi + 3) & 31) == 0 && wi + 131 < p.nwords)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(&p.words[wi + 131]));
-        }
+        uint32_t nw = 0;
+        if (adv && wi + 4 < p.nwords) nw = __ldg(&p.words[wi + 4]);
+        if (adv && ((wi + 4) & 31) == 0 && wi + 132 < p.nwords)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(&p.words[wi + 132]));
+        w0 = adv ? w1 : w0;
+        w1 = adv ? w2 : w1;
+        w2 = adv ? bswap32(w3) : w2;
+        w3 = adv ? nw : w3;
+        wi += adv ? 1 : 0;
+        sh -= adv ? 32 : 0;
     }
 };
 
@@ -1295,7 +1297,8 @@ __global__ void __launch_bounds__(kF6Threads, 1) k_dec_final6(DecParams p) {
     uint8_t *s_l1 = reinterpret_cast<uint8_t *>(s_lut + kLutSize);
     uint16_t *s_stage = reinterpret_cast<uint16_t *>(s_l1 + kLutSize);
     uint64_t *s_base = reinterpret_cast<uint64_t *>(s_stage + (kF6Threads / 32) * 32 * kRow);
-    uint32_t *s_cs = reinterpret_cast<uint32_t *>(s_base + kF6Threads);  // col start | col end << 16
+    uint32_t *s_pre = reinterpret_cast<uint32_t *>(s_base + kF6Threads);   // piece prefix per row
+    uint32_t *s_rng = s_pre + kF6Threads;                                  // lo | hi << 16
     __shared__ DecCanon s_can;
     for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) {
         s_lut[i] = p.tab->lut6[i];
@@ -1308,17 +1311,19 @@ __global__ void __launch_bounds__(kF6Threads, 1) k_dec_final6(DecParams p) {
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     uint16_t *out = static_cast<uint16_t *>(p.out);
     const bool vec_out = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    uint16_t *row = s_stage + (warp * 32 + lane) * kRow;
+    uint16_t *wstage = s_stage + warp * 32 * kRow;
+    uint16_t *row = wstage + lane * kRow;
     const uint32_t row_s = (uint32_t)__cvta_generic_to_shared(row);
     uint64_t *wbase = s_base + warp * 32;
-    uint32_t *wcs = s_cs + warp * 32;
+    uint32_t *wpre = s_pre + warp * 32;
+    uint32_t *wrng = s_rng + warp * 32;
     const uint64_t tstride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t tb = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); tb < p.T;
          tb += tstride) {
         const uint64_t t = tb + lane;
         Win6 r;
         uint64_t t0 = 0, base = 0;
-        uint32_t rel = 0, stop = 0, k = 0, cstart = 0;
+        uint32_t rel = 0, stop = 0, k = 0, lo = 0;
         bool live = false;
         if (t < p.T) {
             const uint32_t e = p.ent0[t];
@@ -1328,32 +1333,28 @@ __global__ void __launch_bounds__(kF6Threads, 1) k_dec_final6(DecParams p) {
                 rel = e;
                 r.init(p, t0 + rel);
                 const uint64_t o = p.off0[t];
-                cstart = k = (uint32_t)(o & 7);
+                lo = k = (uint32_t)(o & 7);
                 base = o - k;
                 live = rel < stop;
             }
         }
         const uint32_t lim = stop >= (uint32_t)kLutBits ? stop - kLutBits : 0;
-        bool any_live = __any_sync(0xffffffffu, live);
-        while (any_live) {
-            bool go = live && k < (uint32_t)kRK;
-            while (__any_sync(0xffffffffu, go)) {
-                if (go) {
+        bool more = __any_sync(0xffffffffu, live);
+        while (more) {
+            // ---- a batch of lookups ----
+            for (int st = 0; st < kFSteps; st++) {
+                if (live) {
                     const uint32_t pk = r.peek12();
                     const uint4 e = s_lut[pk];
                     uint32_t n = e.w & 7u, adv = e.w >> 3;
                     uint32_t s01 = e.x;
-                    if (n == 0 || rel > lim) {  // long code word, invalid prefix or stream tail
+                    if (n == 0 || rel > lim) {  // long code word, invalid prefix or subsequence tail
                         uint32_t L = s_l1[pk], sym = e.x & 0xFFFFu;
                         if (!L) L = decode_long(p, tab, t0 + rel, sym);
-                        n = 1;
+                        n = L ? 1u : 0u;
                         adv = L;
                         s01 = sym;
-                        if (L == 0) {  // cannot happen after a successful map pass
-                            n = 0;
-                            adv = 0;
-                            rel = stop;
-                        }
+                        if (L == 0) rel = stop;  // cannot happen after a successful map pass
                     }
                     const uint32_t a = row_s + 2 * k;
                     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)s01));
@@ -1366,44 +1367,49 @@ __global__ void __launch_bounds__(kF6Threads, 1) k_dec_final6(DecParams p) {
                     rel += adv;
                     if (adv <= 32) r.consume(p, adv);
                     else r.init(p, t0 + rel);
-                    go = rel < stop && k < (uint32_t)kRK;
+                    live = rel < stop;
                 }
             }
-            live = live && rel < stop;
-            // ---- write-out of the round: columns [cstart, min(k, kRK)) of each row ----
-            const uint32_t cend = k < (uint32_t)kRK ? k : (uint32_t)kRK;
-            wbase[lane] = base;
-            wcs[lane] = cstart | (cend << 16);
-            __syncwarp();
+            // ---- flush complete pieces (all of them once the lane is done) ----
+            const uint32_t np = live ? (k >> 3) : ((k + 7) >> 3);
+            uint32_t inc = np;
 #pragma unroll
-            for (int m = 0; m < (32 * kRK / 8) / 32; m++) {
-                const uint32_t i = m * 32 + lane;
-                const uint32_t rw = i / (kRK / 8), c0 = (i % (kRK / 8)) * 8;
-                const uint32_t cs = wcs[rw];
-                const uint32_t lo = cs & 0xFFFFu, hi = cs >> 16;
-                if (c0 + 8 <= lo || c0 >= hi) continue;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= (uint32_t)o) inc += v;
+            }
+            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+            wbase[lane] = base;
+            wpre[lane] = inc - np;
+            wrng[lane] = lo | (k << 16);
+            __syncwarp();
+            for (uint32_t g = lane; g < tot; g += 32) {
+                // row = last j with pre[j] <= g
+                uint32_t rw = 0;
+#pragma unroll
+                for (int b = 16; b > 0; b >>= 1)
+                    if (wpre[rw + b] <= g) rw += b;
+                const uint32_t c0 = (g - wpre[rw]) * 8;
+                const uint32_t rg = wrng[rw];
+                const uint32_t rlo = rg & 0xFFFFu, rhi = rg >> 16;
                 const uint64_t ob = wbase[rw] + c0;
-                const uint16_t *src = s_stage + (warp * 32 + rw) * kRow + c0;
-                if (vec_out && c0 >= lo && c0 + 8 <= hi && ob + 8 <= p.count) {
+                const uint16_t *src = wstage + rw * kRow + c0;
+                if (vec_out && c0 >= rlo && c0 + 8 <= rhi && ob + 8 <= p.count) {
                     *reinterpret_cast<uint4 *>(out + ob) = *reinterpret_cast<const uint4 *>(src);
                 } else {
                     for (uint32_t c = 0; c < 8; c++)
-                        if (c0 + c >= lo && c0 + c < hi && ob + c < p.count) out[ob + c] = src[c];
+                        if (c0 + c >= rlo && c0 + c < rhi && ob + c < p.count) out[ob + c] = src[c];
                 }
             }
             __syncwarp();
-            // carry the overflow (<= 5 symbols) to the next round
-            if (k > (uint32_t)kRK) {
-                for (uint32_t c = kRK; c < k; c++) row[c - kRK] = row[c];
-            }
-            k = k > (uint32_t)kRK ? k - kRK : 0u;
-            base += kRK;
-            cstart = 0;
+            // carry the incomplete piece (<= 7 symbols) to the row start
+            const uint32_t done = np * 8 < k ? np * 8 : k;
+            for (uint32_t c = done; c < k; c++) row[c - done] = row[c];
+            k -= done;
+            base += done;
+            lo = 0;
             __syncwarp();
-            any_live = __any_sync(0xffffffffu, live || k > 0);
-            if (!live && k > 0) {  // leftover overflow of a finished lane: one more round
-                // handled by the next iteration: go stays false, write-out flushes [0, k)
-            }
+            more = __any_sync(0xffffffffu, live);
         }
     }
 }
@@ -1684,7 +1690,7 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
         const size_t fsm = kLutSize * sizeof(uint64_t) + (size_t)(kFThreads / 32) * 32 * (kStage + 1) * sym_bytes;
         if (sym_bytes == 2 && cap <= 65536) {
             const size_t f6 = (size_t)kLutSize * 17 + (size_t)kF6Threads * kRow * 2 +
-                              (size_t)kF6Threads * 12;
+                              (size_t)kF6Threads * 16;
             LZB_CUDA_TRY(cudaFuncSetAttribute(k_dec_final6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f6));
             const unsigned g6 = (unsigned)umin64((L.T + kF6Threads - 1) / kF6Threads, (uint64_t)sms);
             k_dec_final6<<<g6, kF6Threads, f6, s>>>(p);
