@@ -1256,9 +1256,9 @@ __global__ void __launch_bounds__(kFThreads) k_dec_final(DecParams p) {
 // first and last pieces are partial.  Pieces are distributed over the lanes
 // by a warp scan of the per-row piece counts.  The 4-word bit window advances
 // without branches, and each lane prefetches its stream 512 bytes ahead.
-constexpr int kF6Threads = 512;
-constexpr int kFSteps = 8;       // lookups per batch (<= 48 symbols per lane)
-constexpr int kRow = 64 + 8;     // stage row (u16): carry <= 7 + 48 symbols + slack
+constexpr int kF6Threads = 1024;
+constexpr int kFSteps = 4;       // lookups per batch (<= 24 symbols per lane)
+constexpr int kRow = 40;          // stage row (u16): carry <= 7 + 24 symbols + 5 slack
 
 struct Win6 {
     uint64_t wi;                  // word index of w0
