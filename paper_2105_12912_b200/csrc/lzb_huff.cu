@@ -614,6 +614,10 @@ struct DecTables {
     // Six-symbol LUT for the final decode (u16 books): the code words greedily
     // decoded from the 12-bit window, up to six: s[0..5], then n | used << 3.
     uint4 lut6[kLutSize];
+    // Boundary LUT for the map pass: n | used << 4 | starts << 8, where bit i
+    // of `starts` marks a code word starting at window offset i (up to 12
+    // complete code words greedily decoded from the 12-bit window).
+    uint32_t lutb[kLutSize];
     uint64_t first[65];
     uint64_t cnt[65];
     uint32_t off[65];
@@ -918,6 +922,25 @@ __global__ void k_dec_tables(const uint8_t *lengths, uint32_t cap, uint32_t maxl
                 if (!found) break;
             }
         }
+        {
+            uint32_t bu = 0, bn = 0, bm = 0;
+            while (bn < 12) {
+                bool found = false;
+                for (uint32_t L = 1; L + bu <= (uint32_t)kLutBits && L <= s_max; L++) {
+                    const uint32_t code = (v >> (kLutBits - bu - L)) & ((1u << L) - 1u);
+                    const uint64_t f = tab->first[L], k = tab->cnt[L];
+                    if (k && code >= f && code - f < k) {
+                        bm |= 1u << bu;
+                        bu += L;
+                        bn++;
+                        found = true;
+                        break;
+                    }
+                }
+                if (!found) break;
+            }
+            tab->lutb[v] = bn | (bu << 4) | (bm << 8);
+        }
         tab->lut6[v] = make_uint4(sy[0] | (sy[1] << 16), sy[2] | (sy[3] << 16), sy[4] | (sy[5] << 16),
                                   sn | (su << 3));
     }
@@ -1077,6 +1100,214 @@ __global__ void __launch_bounds__(kMThreads) k_dec_maps(DecParams p) {
     }
 }
 
+struct Win6 {
+    uint64_t wi;                  // word index of w0
+    uint32_t w0, w1, w2, w3, sh;  // w3 raw (byte-swapped when it moves to w2)
+    __device__ __forceinline__ void init(const DecParams &p, uint64_t q) {
+        const uint64_t a = q + p.head;
+        wi = a >> 5;
+        sh = (uint32_t)(a & 31);
+        w0 = bswap_load(p, wi);
+        w1 = bswap_load(p, wi + 1);
+        w2 = bswap_load(p, wi + 2);
+        w3 = wi + 3 < p.nwords ? __ldg(&p.words[wi + 3]) : 0u;
+    }
+    __device__ __forceinline__ uint32_t peek12() const {
+        return __funnelshift_l(w1, w0, sh) >> (32 - kLutBits);
+    }
+    __device__ __forceinline__ void consume(const DecParams &p, uint32_t L) {  // L <= 32
+        sh += L;
+        const bool adv = sh >= 32;
+        uint32_t nw = 0;
+        if (adv && wi + 4 < p.nwords) nw = __ldg(&p.words[wi + 4]);
+        if (adv && ((wi + 4) & 31) == 0 && wi + 132 < p.nwords)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(&p.words[wi + 132]));
+        w0 = adv ? w1 : w0;
+        w1 = adv ? w2 : w1;
+        w2 = adv ? bswap32(w3) : w2;
+        w3 = adv ? nw : w3;
+        wi += adv ? 1 : 0;
+        sh -= adv ? 32 : 0;
+    }
+};
+
+// Phase maps, v2.  A warp takes 32 consecutive subsequences.
+//  A) lane = subsequence: decode from phase 0 to the boundary with the
+//     boundary LUT (up to 12 code words per lookup), recording the code-word
+//     starts of the first kMW bits in a 128-bit bitmap;
+//  B) for each of the 32 subsequences in turn, lane = phase 1..P-1: decode
+//     single code words until the position is a recorded start of phase 0
+//     (merged: the rest of the decode is phase 0's) -- Huffman codes
+//     self-synchronise within a few code words.  A phase that has not merged
+//     within kMW bits is decoded to the boundary on its own (fixed-length
+//     books never merge; correct, just slower).
+constexpr int kMW = 128;
+constexpr int kM2Threads = 256;
+
+struct MapRow {
+    uint64_t bm0, bm1;
+    uint32_t count, exit;  // phase-0 result (exit packed as in maps)
+};
+
+__device__ __forceinline__ bool mw_test(const MapRow &m, uint32_t q) {
+    return q < 64 ? ((m.bm0 >> q) & 1ull) : ((m.bm1 >> (q - 64)) & 1ull);
+}
+__device__ __forceinline__ uint32_t mw_rank(const MapRow &m, uint32_t q) {  // starts < q
+    return q <= 64 ? __popcll(q == 64 ? m.bm0 : (m.bm0 & ((1ull << q) - 1ull)))
+                   : __popcll(m.bm0) + __popcll(m.bm1 & ((1ull << (q - 64)) - 1ull));
+}
+
+// Decode code words from stream-relative `rel` of subsequence start t0 until
+// rel >= stop; `cnt` counts them.  bulk: boundary LUT while the window stays
+// inside the subsequence.  Returns false on an invalid code word.
+__device__ __forceinline__ bool map_run(const DecParams &p, const uint32_t *s_b, const uint8_t *s_l1,
+                                        const DecCanon *tab, Win6 &r, uint64_t t0, uint32_t &rel,
+                                        uint32_t stop, uint32_t endrel, uint32_t &cnt) {
+    const uint32_t lim = stop >= (uint32_t)kLutBits ? stop - kLutBits : 0;
+    while (rel < stop) {
+        const uint32_t pk = r.peek12();
+        const uint32_t e = s_b[pk];
+        uint32_t n = e & 15u, used = (e >> 4) & 15u;
+        if (n == 0 || rel + kLutBits > stop) {
+            uint32_t L = s_l1[pk], sym;
+            if (!L) L = decode_long(p, tab, t0 + rel, sym);
+            if (L == 0 || rel + L > endrel) return false;
+            n = 1;
+            used = L;
+        }
+        cnt += n;
+        rel += used;
+        if (used <= 32) r.consume(p, used);
+        else r.init(p, t0 + rel);
+    }
+    return true;
+}
+
+__global__ void __launch_bounds__(kM2Threads) k_dec_maps2(DecParams p) {
+    __shared__ uint32_t s_b[kLutSize];
+    __shared__ uint8_t s_l1[kLutSize];
+    __shared__ DecCanon s_can;
+    __shared__ MapRow s_row[kM2Threads];
+    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) {
+        s_b[i] = p.tab->lutb[i];
+        s_l1[i] = p.tab->lut1[i];
+    }
+    load_canon(s_can, p.tab);
+    __syncthreads();
+    const DecCanon *tab = &s_can;
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    MapRow *wrow = s_row + warp * 32;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t tb = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); tb < p.T;
+         tb += stride) {
+        // ---------------- A: phase 0, one lane per subsequence ----------------
+        {
+            const uint64_t t = tb + lane;
+            MapRow m;
+            m.bm0 = m.bm1 = 0;
+            m.count = 0;
+            m.exit = kExitInvalid;
+            if (t < p.T) {
+                const uint64_t t0 = t * p.S;
+                const bool last = t == p.T - 1;
+                const uint32_t stop = (uint32_t)((last ? p.bit_len : t0 + p.S) - t0);
+                const uint32_t endrel = (uint32_t)umin64(p.bit_len - t0, 0xFFFFFFF0u);
+                const uint32_t lim = stop >= (uint32_t)kLutBits ? stop - kLutBits : 0;
+                Win6 r;
+                r.init(p, t0);
+                uint32_t rel = 0, cnt = 0;
+                bool ok = true;
+                // window part: record every code-word start below kMW
+                while (ok && rel < stop && rel < (uint32_t)kMW) {
+                    const uint32_t pk = r.peek12();
+                    const uint32_t e = s_b[pk];
+                    uint32_t n = e & 15u, used = (e >> 4) & 15u, starts = e >> 8;
+                    if (n == 0 || rel + kLutBits > stop) {
+                        uint32_t L = s_l1[pk], sym;
+                        if (!L) L = decode_long(p, tab, t0 + rel, sym);
+                        if (L == 0 || rel + L > endrel) { ok = false; break; }
+                        n = 1;
+                        used = L;
+                        starts = 1;
+                    }
+                    if (rel < 64) {
+                        m.bm0 |= (uint64_t)starts << rel;
+                        if (rel > 52) m.bm1 |= (uint64_t)starts >> (64 - rel);
+                    } else {
+                        m.bm1 |= (uint64_t)starts << (rel - 64);
+                    }
+                    cnt += n;
+                    rel += used;
+                    if (used <= 32) r.consume(p, used);
+                    else r.init(p, t0 + rel);
+                }
+                if (ok) ok = map_run(p, s_b, s_l1, tab, r, t0, rel, stop, endrel, cnt);
+                if (ok) {
+                    uint32_t ex;
+                    if (last) ex = (rel == stop) ? kExitEnd : kExitInvalid;
+                    else ex = rel - stop;
+                    m.exit = ex;
+                    m.count = cnt;
+                }
+                p.maps[t * p.P] = m.exit == kExitInvalid ? kExitInvalid : ((m.count << 8) | m.exit);
+            }
+            wrow[lane] = m;
+        }
+        __syncwarp();
+        // ---------------- B: phases 1..P-1 of each subsequence ----------------
+        const uint32_t nrows = (uint32_t)umin64(32, p.T - tb);
+        for (uint32_t j = 0; j < nrows; j++) {
+            const uint64_t t = tb + j;
+            const uint64_t t0 = t * p.S;
+            const bool last = t == p.T - 1;
+            const uint32_t stop = (uint32_t)((last ? p.bit_len : t0 + p.S) - t0);
+            const uint32_t endrel = (uint32_t)umin64(p.bit_len - t0, 0xFFFFFFF0u);
+            const MapRow m = wrow[j];
+            for (uint32_t ph = 1 + lane; ph < p.P; ph += 32) {
+                uint32_t out = kExitInvalid;
+                if (ph < p.S && t0 + ph <= p.bit_len) {
+                    Win6 r;
+                    r.init(p, t0 + ph);
+                    uint32_t rel = ph, cnt = 0;
+                    bool ok = true, merged = false;
+                    const uint32_t wend = stop < (uint32_t)kMW ? stop : (uint32_t)kMW;
+                    while (rel < wend) {
+                        if (mw_test(m, rel)) {
+                            merged = true;
+                            break;
+                        }
+                        uint32_t L = s_l1[r.peek12()], sym;
+                        if (!L) L = decode_long(p, tab, t0 + rel, sym);
+                        if (L == 0 || rel + L > endrel) {
+                            ok = false;
+                            break;
+                        }
+                        cnt++;
+                        rel += L;
+                        if (L <= 32) r.consume(p, L);
+                        else r.init(p, t0 + rel);
+                    }
+                    if (ok && merged) {
+                        if (m.exit != kExitInvalid)
+                            out = ((cnt + m.count - mw_rank(m, rel)) << 8) | m.exit;
+                    } else if (ok) {
+                        // not merged inside the window: decode on to the boundary
+                        ok = map_run(p, s_b, s_l1, tab, r, t0, rel, stop, endrel, cnt);
+                        if (ok) {
+                            uint32_t ex;
+                            if (last) ex = (rel == stop) ? kExitEnd : kExitInvalid;
+                            else ex = rel - stop;
+                            out = ex == kExitInvalid ? kExitInvalid : ((cnt << 8) | ex);
+                        }
+                    }
+                }
+                p.maps[t * p.P + ph] = out;
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // Level-1/2 composition: thread per (group, phase).  in: n_in maps of P entries
 // (32-bit or 64-bit packed (count << 8) | exit).
 template <typename InT>
@@ -1205,7 +1436,7 @@ __global__ void __launch_bounds__(kFThreads) k_dec_final(DecParams p) {
                 if (go) {
                     const uint64_t e = s_lut[r.peek12()];
                     const uint32_t n = lm_count(e);
-                    if (n && k <= (uint32_t)kStage - 3 && rel <= lim) {
+                    if (n && k <= (uint32_t)kStage - 3 && rel + kLutBits <= stop) {
                         stg[k] = (SymT)lm_sym(e, 0);
                         stg[k + 1] = (SymT)lm_sym(e, 1);
                         stg[k + 2] = (SymT)lm_sym(e, 2);
@@ -1260,36 +1491,6 @@ constexpr int kF6Threads = 1024;
 constexpr int kFSteps = 4;       // lookups per batch (<= 24 symbols per lane)
 constexpr int kRow = 40;          // stage row (u16): carry <= 7 + 24 symbols + 5 slack
 
-struct Win6 {
-    uint64_t wi;                  // word index of w0
-    uint32_t w0, w1, w2, w3, sh;  // w3 raw (byte-swapped when it moves to w2)
-    __device__ __forceinline__ void init(const DecParams &p, uint64_t q) {
-        const uint64_t a = q + p.head;
-        wi = a >> 5;
-        sh = (uint32_t)(a & 31);
-        w0 = bswap_load(p, wi);
-        w1 = bswap_load(p, wi + 1);
-        w2 = bswap_load(p, wi + 2);
-        w3 = wi + 3 < p.nwords ? __ldg(&p.words[wi + 3]) : 0u;
-    }
-    __device__ __forceinline__ uint32_t peek12() const {
-        return __funnelshift_l(w1, w0, sh) >> (32 - kLutBits);
-    }
-    __device__ __forceinline__ void consume(const DecParams &p, uint32_t L) {  // L <= 32
-        sh += L;
-        const bool adv = sh >= 32;
-        uint32_t nw = 0;
-        if (adv && wi + 4 < p.nwords) nw = __ldg(&p.words[wi + 4]);
-        if (adv && ((wi + 4) & 31) == 0 && wi + 132 < p.nwords)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(&p.words[wi + 132]));
-        w0 = adv ? w1 : w0;
-        w1 = adv ? w2 : w1;
-        w2 = adv ? bswap32(w3) : w2;
-        w3 = adv ? nw : w3;
-        wi += adv ? 1 : 0;
-        sh -= adv ? 32 : 0;
-    }
-};
 
 __global__ void __launch_bounds__(kF6Threads, 1) k_dec_final6(DecParams p) {
     extern __shared__ __align__(16) unsigned char f6_smem[];
@@ -1348,7 +1549,7 @@ __global__ void __launch_bounds__(kF6Threads, 1) k_dec_final6(DecParams p) {
                     const uint4 e = s_lut[pk];
                     uint32_t n = e.w & 7u, adv = e.w >> 3;
                     uint32_t s01 = e.x;
-                    if (n == 0 || rel > lim) {  // long code word, invalid prefix or subsequence tail
+                    if (n == 0 || rel + kLutBits > stop) {  // long code word, invalid prefix or subsequence tail
                         uint32_t L = s_l1[pk], sym = e.x & 0xFFFFu;
                         if (!L) L = decode_long(p, tab, t0 + rel, sym);
                         n = L ? 1u : 0u;
@@ -1671,7 +1872,7 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
     const int sms = dev_sms();
     // phases >= the book's real max length cannot be entries (P = maxlen hint;
     // k_dec_tables flags a hint that disagrees with the lengths as corrupt).
-    k_dec_maps<<<(unsigned)umin64((L.T + kMThreads - 1) / kMThreads, (uint64_t)sms * 4), kMThreads, 0, s>>>(p);
+    k_dec_maps2<<<(unsigned)umin64((L.T + kM2Threads - 1) / kM2Threads, (uint64_t)sms * 8), kM2Threads, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
     k_dec_compose<uint32_t><<<(unsigned)umin64((L.ng1 * L.P + 255) / 256, (uint64_t)sms * 32), 256, 0, s>>>(
         p.maps, L.T, L.P, L.G, p.g1, L.ng1);
