@@ -103,9 +103,12 @@ __device__ __forceinline__ uint32_t lpos(const Chunk &k, uint32_t lx, uint32_t l
 // ---------------------------------------------------------------------------
 // Lorenzo deltas in registers (nested first differences, zero prepend)
 // ---------------------------------------------------------------------------
+// The lane masks are applied as multiply-adds by a 0/1 factor (one IMAD
+// instead of a select + add per element and step).
 template <typename I>
 __device__ __forceinline__ void deltas(I (&v0)[8], I (&v1)[8], uint32_t lane) {
-    const uint32_t ly = lane & 7;
+    const I fy = (lane & 7) ? I(1) : I(0);
+    const I fz = lane >= 8 ? I(1) : I(0);
     // x
 #pragma unroll
     for (int k = 7; k >= 1; k--) {
@@ -117,17 +120,15 @@ __device__ __forceinline__ void deltas(I (&v0)[8], I (&v1)[8], uint32_t lane) {
     for (int k = 0; k < 8; k++) {
         I a = __shfl_up_sync(kFull, v0[k], 1, 8);
         I b = __shfl_up_sync(kFull, v1[k], 1, 8);
-        if (ly) {
-            v0[k] -= a;
-            v1[k] -= b;
-        }
+        v0[k] -= a * fy;
+        v1[k] -= b * fy;
     }
     // z: row1 - row0 in lane; row0 - row1 of lane - 8
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         I up = __shfl_up_sync(kFull, v1[k], 8);
         v1[k] -= v0[k];
-        if (lane >= 8) v0[k] -= up;
+        v0[k] -= up * fz;
     }
 }
 
@@ -142,27 +143,24 @@ __device__ __forceinline__ void psums(I (&v0)[8], I (&v1)[8], uint32_t lane) {
     }
 #pragma unroll
     for (int o = 1; o < 8; o <<= 1) {
+        const I f = ly >= (uint32_t)o ? I(1) : I(0);
 #pragma unroll
         for (int k = 0; k < 8; k++) {
             I a = __shfl_up_sync(kFull, v0[k], o, 8);
             I b = __shfl_up_sync(kFull, v1[k], o, 8);
-            if (ly >= (uint32_t)o) {
-                v0[k] += a;
-                v1[k] += b;
-            }
+            v0[k] += a * f;
+            v1[k] += b * f;
         }
     }
     // z: pair (row0, row1) per lane, then across the four 8-lane groups
+    const I f8 = lane >= 8 ? I(1) : I(0), f16 = lane >= 16 ? I(1) : I(0);
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         v1[k] += v0[k];
         I carry = v1[k];  // inclusive total of this lane's pair
         I s = carry;
-#pragma unroll
-        for (int o = 8; o < 32; o <<= 1) {
-            I a = __shfl_up_sync(kFull, s, o);
-            if (lane >= (uint32_t)o) s += a;
-        }
+        s += __shfl_up_sync(kFull, s, 8) * f8;
+        s += __shfl_up_sync(kFull, s, 16) * f16;
         I excl = s - carry;
         v0[k] += excl;
         v1[k] += excl;

@@ -75,10 +75,36 @@ __device__ __forceinline__ bool r3_needs_wide(const R3Params &p, uint64_t r0, ui
     return __any_sync(f3::kFull, wide);
 }
 
+// The tile's outliers held in registers (lane i: record i, i < 32): apply
+// those of chunk k.  Usually at most the chunk origin.
+template <typename I>
+__device__ __forceinline__ void r3_add_reg(uint32_t rkey, int32_t rd, uint32_t nrec, uint32_t k,
+                                           uint32_t lane, I (&v0)[8], I (&v1)[8]) {
+    uint32_t m = __ballot_sync(f3::kFull, lane < nrec && (rkey >> 9) == k);
+    const uint32_t ly = lane & 7, lz0 = (lane >> 3) * 2;
+    while (m) {
+        const uint32_t i = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t key = __shfl_sync(f3::kFull, rkey, i);
+        const int32_t d = __shfl_sync(f3::kFull, rd, i);
+        const uint32_t lx = key & 7, oy = (key >> 3) & 7, oz = (key >> 6) & 7;
+        const bool mine = oy == ly && (oz & ~1u) == lz0;
+        const bool r1 = oz & 1u;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const I add = (mine && (uint32_t)j == lx) ? (I)d : (I)0;
+            v0[j] += r1 ? (I)0 : add;
+            v1[j] += r1 ? add : (I)0;
+        }
+    }
+}
+
 template <typename SymT, typename OutT, typename I>
 __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch, uint32_t k,
                                          uint64_t r0, uint64_t r1, uint32_t lane, OutT &vmin,
-                                         OutT &vmax, bool &overflow, const SymT *stg = nullptr) {
+                                         OutT &vmax, bool &overflow, const SymT *stg = nullptr,
+                                         bool reg_out = false, uint32_t rkey = 0, int32_t rd = 0,
+                                         uint32_t nrec = 0) {
     const uint32_t ly = lane & 7, lz0 = (lane >> 3) * 2;
     const SymT *cs = static_cast<const SymT *>(p.codes) + ch.base;
     I v0[8], v1[8];
@@ -121,7 +147,8 @@ __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch,
             v1[j] = ((m1 >> j) & 1u) ? (I)(int64_t)cs[f3::lpos(ch, j, ly, lz0 + 1)] - p.r : (I)0;
         }
     }
-    if (r1 > r0) r3_add_outliers<I>(p, r0, r1, k, lane, v0, v1);
+    if (reg_out) r3_add_reg<I>(rkey, rd, nrec, k, lane, v0, v1);
+    else if (r1 > r0) r3_add_outliers<I>(p, r0, r1, k, lane, v0, v1);
     if constexpr (sizeof(I) == 8) {
         // prefix-sum magnitude guard (P/reconstruct.py:48-53), f64 sum per chunk
         double s = 0.0;
@@ -142,9 +169,9 @@ __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch,
 #pragma unroll
         for (int j = 0; j < 8; j++) {
             o[j] = (OutT)__dmul_rn((double)v[j], p.two_eb);
-            if ((mm >> j) & 1u) {
-                vmin = o[j] < vmin ? o[j] : vmin;
-                vmax = o[j] > vmax ? o[j] : vmax;
+            if ((mm >> j) & 1u) {  // outputs are never NaN: plain min/max instructions
+                vmin = fmin(vmin, o[j]);
+                vmax = fmax(vmax, o[j]);
             }
         }
         if (fast && p.vec_ok) {
@@ -200,7 +227,7 @@ __device__ __forceinline__ void r3_prefetch(const R3Params &p, const f3::Chunk &
 }
 
 template <typename SymT, typename OutT>
-__global__ void __launch_bounds__(kR3Threads, 2) k_reconstruct3d8(const __grid_constant__ R3Params p) {
+__global__ void __launch_bounds__(kR3Threads, 3) k_reconstruct3d8(const __grid_constant__ R3Params p) {
     // per-warp double buffer of the next chunk's code rows (16 symbols per lane)
     __shared__ __align__(16) SymT s_stage[kR3Warps][2][32 * 16];
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -217,6 +244,26 @@ __global__ void __launch_bounds__(kR3Threads, 2) k_reconstruct3d8(const __grid_c
         const uint64_t c0 = t * kR3TileChunks;
         const uint64_t c1 = umin64(c0 + kR3TileChunks, p.nchunks);
         const uint64_t r0 = p.tile_start[t], r1 = p.tile_start[t + 1];
+        // outliers of the tile: up to 32 in registers (one per lane), with a
+        // per-chunk mask of chunks that need the exact int64 path
+        const uint64_t nr64 = r1 - r0;
+        const bool reg_out = nr64 <= 32;
+        const uint32_t nrec = reg_out ? (uint32_t)nr64 : 0u;
+        uint32_t rkey = 0xFFFFFFFFu;
+        int32_t rd = 0;
+        uint32_t wide_mask = 0;
+        if (reg_out) {
+            bool wide = false;
+            if (lane < nrec) {
+                rkey = (uint32_t)p.brec[2 * (r0 + lane)];
+                const int64_t d = (int64_t)p.brec[2 * (r0 + lane) + 1];
+                wide = d >= (1ll << 20) || d <= -(1ll << 20);
+                rd = (int32_t)d;
+            }
+            const uint32_t wm = __ballot_sync(f3::kFull, wide);
+            for (uint32_t m = wm; m; m &= m - 1)
+                wide_mask |= 1u << (__shfl_sync(f3::kFull, rkey, __ffs(m) - 1) >> 9);
+        }
         f3::Chunk cur = f3::chunk_of(p.g, c0);
         bool cur_pf = cur.full && (cur.base & 7) == 0;
         if (cur_pf) r3_prefetch<SymT>(p, cur, lane, stage_s);
@@ -233,14 +280,17 @@ __global__ void __launch_bounds__(kR3Threads, 2) k_reconstruct3d8(const __grid_c
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
             asm volatile("cp.async.wait_group 1;" ::: "memory");
-            if (r1 > r0 && r3_needs_wide(p, r0, r1, k)) {
+            const bool wide = reg_out ? ((wide_mask >> k) & 1u) != 0
+                                      : (r1 > r0 && r3_needs_wide(p, r0, r1, k));
+            if (wide) {
                 OutT mmv[2] = {vmin, vmax};
                 r3_chunk_wide<SymT, OutT>(&p, c, k, r0, r1, lane, mmv, &overflow);
                 vmin = mmv[0];
                 vmax = mmv[1];
             } else {
                 r3_chunk<SymT, OutT, int32_t>(p, cur, k, r0, r1, lane, vmin, vmax, overflow,
-                                              cur_pf ? reinterpret_cast<const SymT *>(reinterpret_cast<const unsigned char *>(&s_stage[warp][sb][0]) + lane * 16) : nullptr);
+                                              cur_pf ? reinterpret_cast<const SymT *>(reinterpret_cast<const unsigned char *>(&s_stage[warp][sb][0]) + lane * 16) : nullptr,
+                                              reg_out, rkey, rd, nrec);
             }
             cur = nxt;
             cur_pf = nxt_pf;
@@ -251,8 +301,8 @@ __global__ void __launch_bounds__(kR3Threads, 2) k_reconstruct3d8(const __grid_c
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         OutT a = __shfl_xor_sync(f3::kFull, vmin, o), b = __shfl_xor_sync(f3::kFull, vmax, o);
-        vmin = a < vmin ? a : vmin;
-        vmax = b > vmax ? b : vmax;
+        vmin = fmin(vmin, a);
+        vmax = fmax(vmax, b);
     }
     if (lane == 0 && vmin <= vmax) {
         atomicMin(&p.mm[0], r3_dkey((double)vmin));
