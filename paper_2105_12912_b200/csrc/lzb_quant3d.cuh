@@ -515,39 +515,62 @@ __global__ void __launch_bounds__(kQ3Threads, 2) k_quantize3d8(const __grid_cons
     Q3Warp<InT> w;
     w.hw0 = w.hw1 = 0;
     w.flags = 0;
-    while (true) {
+    // Tiles are claimed one ahead so the first chunk of the next tile is
+    // prefetched while the last chunk of the current one is processed.
+    auto claim = [&]() -> uint64_t {
         uint64_t t = 0;
         if (lane == 0) t = atomicAdd(p.ticket, 1u);
-        t = __shfl_sync(f3::kFull, t, 0);
-        if (t >= p.ntiles) break;
+        return __shfl_sync(f3::kFull, t, 0);
+    };
+    uint64_t t = claim();
+    uint64_t t_next = t < p.ntiles ? claim() : p.ntiles;
+    uint32_t bx = 0, by = 0, bz = 0;
+    auto tile_origin = [&](uint64_t tt) {
+        const uint64_t c0 = tt * kQ3TileChunks;
+        const uint64_t rowc = c0 / p.g.nbx;
+        bx = (uint32_t)(c0 - rowc * p.g.nbx);
+        by = (uint32_t)(rowc % p.g.nby);
+        bz = (uint32_t)(rowc / p.g.nby);
+    };
+    Q3Loc cur;
+    cur.full = false;
+    if (t < p.ntiles) {
+        tile_origin(t);
+        cur = q3_loc(p, bx, by, bz, lane_off);
+        if (cur.full) q3_prefetch<InT>(p, cur, stage_s);
+    }
+    cp_async_commit();
+    uint32_t sb = 0;
+    while (t < p.ntiles) {
         const uint64_t c0 = t * kQ3TileChunks;
-        const uint64_t c1 = umin64(c0 + kQ3TileChunks, p.nchunks);
+        const uint32_t nk = (uint32_t)(umin64(c0 + kQ3TileChunks, p.nchunks) - c0);
         uint64_t *slot = p.slots + t * 2 * kQ3Slot;
         uint32_t wcount = 0;
-        const uint64_t rowc = c0 / p.g.nbx;
-        uint32_t bx = (uint32_t)(c0 - rowc * p.g.nbx);
-        uint32_t by = (uint32_t)(rowc % p.g.nby), bz = (uint32_t)(rowc / p.g.nby);
-        const uint32_t nk = (uint32_t)(c1 - c0);
-        Q3Loc cur = q3_loc(p, bx, by, bz, lane_off);
-        if (cur.full) q3_prefetch<InT>(p, cur, stage_s);
-        cp_async_commit();
-        uint32_t sb = 0;
         for (uint32_t k = 0; k < nk; k++) {
-            // prefetch the next chunk of the tile into the other stage buffer
+            // the next chunk: same tile, else the first chunk of the next tile
             Q3Loc nxt = cur;
-            if (++bx < (uint32_t)p.g.nbx) {  // same chunk row: increment
-                nxt.gi0 += 8;
-                nxt.sbase += 512;
-                nxt.full = nxt.row_full && (bx * 8 + 8 <= p.g.nx);
-            } else {
-                bx = 0;
-                if (++by == (uint32_t)p.g.nby) {
-                    by = 0;
-                    ++bz;
+            bool have_next = true;
+            if (k + 1 < nk) {
+                if (++bx < (uint32_t)p.g.nbx) {  // same chunk row: increment
+                    nxt.gi0 += 8;
+                    nxt.sbase += 512;
+                    nxt.full = nxt.row_full && (bx * 8 + 8 <= p.g.nx);
+                } else {
+                    bx = 0;
+                    if (++by == (uint32_t)p.g.nby) {
+                        by = 0;
+                        ++bz;
+                    }
+                    nxt = q3_loc(p, bx, by, bz, lane_off);
                 }
+            } else if (t_next < p.ntiles) {
+                tile_origin(t_next);
                 nxt = q3_loc(p, bx, by, bz, lane_off);
+            } else {
+                have_next = false;
+                nxt.full = false;
             }
-            if (k + 1 < nk && nxt.full) q3_prefetch<InT>(p, nxt, stage_s + (sb ^ 1) * 32 * kLaneStage);
+            if (have_next && nxt.full) q3_prefetch<InT>(p, nxt, stage_s + (sb ^ 1) * 32 * kLaneStage);
             cp_async_commit();
             cp_async_wait1();  // this chunk's rows have landed
             uint32_t n = kQ3Redo;
@@ -567,6 +590,8 @@ __global__ void __launch_bounds__(kQ3Threads, 2) k_quantize3d8(const __grid_cons
             p.tile_cnt[t] = wcount;
             if (wcount > (uint32_t)kQ3Slot) p.over_list[atomicAdd(p.n_over, 1u)] = (uint32_t)t;
         }
+        t = t_next;
+        if (t < p.ntiles) t_next = claim();
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
