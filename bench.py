@@ -47,6 +47,8 @@ CONFIGS = {
                workload="C5: 3D float32 2048x2048x2048 synthetic smooth field, rel eb 1e-4"),
     "c5s": dict(shape=(512, 512, 512), gen="smooth", eb=1e-4,
                 workload="C5s: 3D float32 512^3 smooth (C5 per-element behaviour, profiling size)"),
+    "c5q": dict(shape=(512, 2048, 2048), gen="smooth", eb=1e-4,
+                workload="C5q: 3D float32 512x2048x2048 smooth (C5 per-element and decode-layout behaviour, profiling size)"),
     "c1": dict(shape=(100, 500, 500), gen="smooth", eb=1e-4,
                workload="C1: 3D float32 100x500x500 (Hurricane shape) smooth, rel eb 1e-4"),
     "c2": dict(shape=(1800, 3600), gen="smooth", eb=1e-4,

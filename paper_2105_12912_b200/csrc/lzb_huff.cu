@@ -598,8 +598,6 @@ constexpr int kLutBits = 12;
 constexpr uint32_t kLutSize = 1u << kLutBits;
 constexpr uint8_t kExitInvalid = 0xFF;
 constexpr uint8_t kExitEnd = 0xFE;
-constexpr int kMaxPaths = 4;
-constexpr uint32_t kMergeWin = 128;  // bits in which phases look for a merge
 
 struct DecTables {
     // Multi-symbol LUT on the next 12 bits: up to three complete code words
@@ -610,9 +608,10 @@ struct DecTables {
     // Count-only LUT for the phase-map pass: all complete code words greedily
     // decoded from the 12-bit window (up to 7): count | bits consumed << 3.
     uint16_t lutc[kLutSize];
-    uint8_t lut1[kLutSize];  // length of the first code word (0: > 12 bits or invalid)
+    uint8_t lut1[kLutSize];  // first code word: len <= 12, or 0x80 | shortest long len, 0 invalid
     // Six-symbol LUT for the final decode (u16 books): the code words greedily
-    // decoded from the 12-bit window, up to six: s[0..5], then n | used << 3.
+    // decoded from the 12-bit window, up to six: s[0..5], then
+    // n | used << 3 | starts << 8 (bit i of starts: a code word starts at i).
     uint4 lut6[kLutSize];
     // Boundary LUT for the map pass: n | used << 4 | starts << 8, where bit i
     // of `starts` marks a code word starting at window offset i (up to 12
@@ -668,6 +667,8 @@ struct DecParams {
     uint64_t *off1;
     uint8_t *ent0;     // per subsequence
     uint64_t *off0;
+    uint16_t *cp;      // v3: per microblock (count << 8) | chain entry offset
+    uint64_t *irr;     // v3: per subsequence, entry phases that join the chain late
 };
 
 __device__ __forceinline__ uint32_t bswap_load(const DecParams &p, uint64_t w) {
@@ -684,32 +685,6 @@ __device__ __forceinline__ uint64_t peek64(const DecParams &p, uint64_t q) {
     uint64_t nx = bswap_load(p, w + 2);
     return (hi << b) | (nx >> (32 - b));
 }
-
-struct BitReader {
-    uint64_t buf;  // MSB aligned
-    int nb;        // valid bits in buf (>= 32 after refill)
-    uint64_t nextw;
-    uint64_t pos;  // absolute stream bit of buf's MSB
-
-    __device__ __forceinline__ void init(const DecParams &p, uint64_t q) {
-        uint64_t a = q + p.head;
-        uint64_t w = a >> 5;
-        uint32_t b = a & 31;
-        buf = (((uint64_t)bswap_load(p, w) << 32) | bswap_load(p, w + 1)) << b;
-        nb = 64 - b;
-        nextw = w + 2;
-        pos = q;
-    }
-    __device__ __forceinline__ void consume(const DecParams &p, uint32_t L) {
-        buf <<= L;
-        nb -= L;
-        pos += L;
-        if (nb < 32) {
-            buf |= (uint64_t)bswap_load(p, nextw++) << (32 - nb);
-            nb += 32;
-        }
-    }
-};
 
 __device__ __forceinline__ uint32_t lm_count(uint64_t e) { return (uint32_t)(e & 3u); }
 __device__ __forceinline__ uint32_t lm_len(uint64_t e, int i) { return (uint32_t)(e >> (2 + 4 * i)) & 15u; }
@@ -752,30 +727,10 @@ struct Win {
 __device__ __forceinline__ uint32_t decode_long(const DecParams &p, const DecCanon *tab, uint64_t q,
                                                 uint32_t &sym) {
     const uint64_t v = peek64(p, q);
-    for (uint32_t L = kLutBits + 1; L <= tab->maxlen; L++) {
+    // from length 1: books with cap > 65536 have no symbols in the LUTs
+    for (uint32_t L = 1; L <= tab->maxlen; L++) {
         const uint64_t c = v >> (64 - L);
         const uint64_t f = tab->first[L], k = tab->cnt[L];
-        if (k && c >= f && c - f < k) {
-            sym = p.syms[tab->off[L] + (uint32_t)(c - f)];
-            return L;
-        }
-    }
-    return 0;
-}
-
-// Decode one code word at the reader.  Returns len (0 = invalid), *sym.
-__device__ __forceinline__ uint32_t decode_one(const DecParams &p, const uint64_t *lutm,
-                                               const DecCanon *tab, BitReader &r, uint32_t &sym) {
-    const uint64_t e = lutm[r.buf >> (64 - kLutBits)];
-    if (lm_count(e)) {
-        sym = lm_sym(e, 0);
-        return lm_len(e, 0);
-    }
-    // long code (> 12 bits) or invalid prefix: canonical tables on 64 peeked bits
-    uint64_t v = (r.nb >= 64) ? r.buf : peek64(p, r.pos);
-    for (uint32_t L = kLutBits + 1; L <= tab->maxlen; L++) {
-        uint64_t c = v >> (64 - L);
-        uint64_t f = tab->first[L], k = tab->cnt[L];
         if (k && c >= f && c - f < k) {
             sym = p.syms[tab->off[L] + (uint32_t)(c - f)];
             return L;
@@ -902,10 +857,25 @@ __global__ void k_dec_tables(const uint8_t *lengths, uint32_t cap, uint32_t maxl
             if (!found) break;
         }
         tab->lutc[v] = (uint16_t)(cn | (cu << 3));
-        tab->lut1[v] = (uint8_t)(n ? ((e >> 2) & 15u) : 0u);
+        {  // first code word: its length if <= 12 bits, else 0x80 | the shortest
+           // length of a code word with this 12-bit prefix, 0 = invalid prefix
+            uint32_t l1 = 0;
+            for (uint32_t L = 1; L <= s_max && !l1; L++) {
+                const uint64_t f = tab->first[L], k = tab->cnt[L];
+                if (!k) continue;
+                if (L <= (uint32_t)kLutBits) {
+                    const uint32_t code = v >> (kLutBits - L);
+                    if (code >= f && code - f < k) l1 = L;
+                } else {  // some code of length L, in [f, f + k), has the prefix v
+                    const uint32_t sh = L - kLutBits;
+                    if ((f >> sh) <= v && v <= ((f + (k - 1)) >> sh)) l1 = 0x80u | L;
+                }
+            }
+            tab->lut1[v] = (uint8_t)l1;
+        }
         // six-symbol entry
         uint32_t sy[6] = {0, 0, 0, 0, 0, 0};
-        uint32_t su = 0, sn = 0;
+        uint32_t su = 0, sn = 0, sm = 0;
         if (cap <= 65536) {
             while (sn < 6) {
                 bool found = false;
@@ -914,6 +884,7 @@ __global__ void k_dec_tables(const uint8_t *lengths, uint32_t cap, uint32_t maxl
                     const uint64_t f = tab->first[L], k = tab->cnt[L];
                     if (k && code >= f && code - f < k) {
                         sy[sn++] = syms[tab->off[L] + (uint32_t)(code - f)];
+                        sm |= 1u << su;
                         su += L;
                         found = true;
                         break;
@@ -942,369 +913,7 @@ __global__ void k_dec_tables(const uint8_t *lengths, uint32_t cap, uint32_t maxl
             tab->lutb[v] = bn | (bu << 4) | (bm << 8);
         }
         tab->lut6[v] = make_uint4(sy[0] | (sy[1] << 16), sy[2] | (sy[3] << 16), sy[4] | (sy[5] << 16),
-                                  sn | (su << 3));
-    }
-}
-
-struct Path {
-    uint64_t bm[kMergeWin / 64];
-    uint32_t exit;  // packed exit code
-    uint32_t count;
-};
-
-__device__ __forceinline__ bool bm_test(const uint64_t *bm, uint32_t q) {
-    return (bm[q >> 6] >> (q & 63)) & 1ull;
-}
-__device__ __forceinline__ uint32_t bm_rank(const uint64_t *bm, uint32_t q) {  // set bits < q
-    uint32_t r = 0;
-#pragma unroll
-    for (uint32_t i = 0; i < kMergeWin / 64; i++) {
-        if (q >= 64 * (i + 1)) r += __popcll(bm[i]);
-        else if (q > 64 * i) r += __popcll(bm[i] & ((1ull << (q - 64 * i)) - 1ull));
-    }
-    return r;
-}
-
-// Phase maps: thread per subsequence, positions relative to the subsequence
-// start (32-bit).  Written as a warp-uniform state machine: every lane runs
-// the same phase and the step loop re-converges the warp at each step
-// (__any_sync), so lanes decode in lock-step instead of drifting apart after a
-// rare long code word.  Modes per lane and phase:
-//   1 merge window: one code word per step, record starts, look for merges
-//   2 bulk:         count-only LUT, up to seven code words per 12-bit lookup
-//   3 tail:         one code word per step up to the subsequence boundary
-constexpr int kMThreads = 512;
-__global__ void __launch_bounds__(kMThreads) k_dec_maps(DecParams p) {
-    __shared__ uint8_t s_len1[kLutSize];
-    __shared__ uint16_t s_cnt[kLutSize];
-    __shared__ DecCanon s_can;
-    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) {
-        s_len1[i] = p.tab->lut1[i];
-        s_cnt[i] = p.tab->lutc[i];
-    }
-    load_canon(s_can, p.tab);
-    __syncthreads();
-    const DecCanon *tab = &s_can;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t tb = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); tb < p.T;
-         tb += stride) {
-        const uint64_t t = tb + lane_id();
-        const bool act = t < p.T;
-        const uint64_t t0 = t * p.S;
-        const bool last = (t == p.T - 1);
-        const uint32_t stop = act ? (uint32_t)((last ? p.bit_len : t0 + p.S) - t0) : 0;
-        const uint32_t endrel = act ? (uint32_t)umin64(p.bit_len - t0, 0xFFFFFFF0u) : 0;
-        const uint32_t lim = stop >= (uint32_t)kLutBits ? stop - kLutBits : 0;
-        Path paths[kMaxPaths];
-        int npaths = 0;
-        for (uint32_t ph = 0; ph < p.P; ph++) {
-            // ---- per-lane phase setup ----
-            uint32_t out = kExitInvalid;
-            int mode = 0;
-            Path mine;
-#pragma unroll
-            for (int i = 0; i < (int)(kMergeWin / 64); i++) mine.bm[i] = 0;
-            Win r;
-            uint32_t rel = ph, steps = 0;
-            if (act && ph < p.S && t0 + ph <= p.bit_len) {
-                int hit = -1;
-                for (int k = 0; k < npaths; k++)
-                    if (ph < kMergeWin && bm_test(paths[k].bm, ph)) { hit = k; break; }
-                if (hit >= 0) {
-                    out = ((paths[hit].count - bm_rank(paths[hit].bm, ph)) << 8) | paths[hit].exit;
-                } else {
-                    r.init(p, t0 + ph);
-                    mode = 1;
-                }
-            }
-            // ---- lock-step decode ----
-            while (__any_sync(0xffffffffu, mode != 0)) {
-                if (mode == 2) {
-                    if (rel > lim) {
-                        mode = 3;
-                    } else {
-                        const uint32_t c = s_cnt[r.peek12()];
-                        if (c & 7u) {
-                            const uint32_t used = c >> 3;
-                            r.consume(p, used);
-                            rel += used;
-                            steps += c & 7u;
-                        } else {
-                            uint32_t sym;
-                            const uint32_t L = decode_long(p, tab, t0 + rel, sym);
-                            if (L == 0 || rel + L > endrel) {
-                                out = kExitInvalid;
-                                mode = 0;
-                            } else {
-                                if (L <= 32) r.consume(p, L);
-                                else r.init(p, t0 + rel + L);
-                                rel += L;
-                                steps++;
-                            }
-                        }
-                    }
-                } else if (mode == 1 || mode == 3) {
-                    if (rel >= stop) {
-                        // reached the boundary: exit phase (or END for the last subsequence)
-                        uint32_t ex;
-                        if (last) ex = (rel == stop) ? kExitEnd : kExitInvalid;
-                        else ex = rel - stop;
-                        out = ex == kExitInvalid ? kExitInvalid : ((steps << 8) | ex);
-                        if (npaths < kMaxPaths && ex != kExitInvalid) {
-                            mine.exit = ex;
-                            mine.count = steps;
-                            paths[npaths++] = mine;
-                        }
-                        mode = 0;
-                    } else if (mode == 1 && rel >= kMergeWin) {
-                        mode = 2;
-                    } else {
-                        bool merged = false;
-                        if (mode == 1) {
-                            for (int k = 0; k < npaths; k++) {
-                                if (bm_test(paths[k].bm, rel)) {
-                                    out = ((steps + paths[k].count - bm_rank(paths[k].bm, rel)) << 8) |
-                                          paths[k].exit;
-                                    merged = true;
-                                    break;
-                                }
-                            }
-                            if (!merged) mine.bm[rel >> 6] |= 1ull << (rel & 63);
-                        }
-                        if (merged) {
-                            mode = 0;
-                        } else {
-                            uint32_t L = s_len1[r.peek12()];
-                            if (!L) {
-                                uint32_t sym;
-                                L = decode_long(p, tab, t0 + rel, sym);
-                            }
-                            if (L == 0 || rel + L > endrel) {
-                                out = kExitInvalid;
-                                mode = 0;
-                            } else {
-                                if (L <= 32) r.consume(p, L);
-                                else r.init(p, t0 + rel + L);
-                                rel += L;
-                                steps++;
-                            }
-                        }
-                    }
-                }
-            }
-            if (act) {
-                if ((out & 0xFF) == kExitInvalid) out = kExitInvalid;
-                p.maps[t * p.P + ph] = out;
-            }
-        }
-    }
-}
-
-struct Win6 {
-    uint64_t wi;                  // word index of w0
-    uint32_t w0, w1, w2, w3, sh;  // w3 raw (byte-swapped when it moves to w2)
-    __device__ __forceinline__ void init(const DecParams &p, uint64_t q) {
-        const uint64_t a = q + p.head;
-        wi = a >> 5;
-        sh = (uint32_t)(a & 31);
-        w0 = bswap_load(p, wi);
-        w1 = bswap_load(p, wi + 1);
-        w2 = bswap_load(p, wi + 2);
-        w3 = wi + 3 < p.nwords ? __ldg(&p.words[wi + 3]) : 0u;
-    }
-    __device__ __forceinline__ uint32_t peek12() const {
-        return __funnelshift_l(w1, w0, sh) >> (32 - kLutBits);
-    }
-    __device__ __forceinline__ void consume(const DecParams &p, uint32_t L) {  // L <= 32
-        sh += L;
-        const bool adv = sh >= 32;
-        uint32_t nw = 0;
-        if (adv && wi + 4 < p.nwords) nw = __ldg(&p.words[wi + 4]);
-        if (adv && ((wi + 4) & 31) == 0 && wi + 132 < p.nwords)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(&p.words[wi + 132]));
-        w0 = adv ? w1 : w0;
-        w1 = adv ? w2 : w1;
-        w2 = adv ? bswap32(w3) : w2;
-        w3 = adv ? nw : w3;
-        wi += adv ? 1 : 0;
-        sh -= adv ? 32 : 0;
-    }
-};
-
-// Phase maps, v2.  A warp takes 32 consecutive subsequences.
-//  A) lane = subsequence: decode from phase 0 to the boundary with the
-//     boundary LUT (up to 12 code words per lookup), recording the code-word
-//     starts of the first kMW bits in a 128-bit bitmap;
-//  B) for each of the 32 subsequences in turn, lane = phase 1..P-1: decode
-//     single code words until the position is a recorded start of phase 0
-//     (merged: the rest of the decode is phase 0's) -- Huffman codes
-//     self-synchronise within a few code words.  A phase that has not merged
-//     within kMW bits is decoded to the boundary on its own (fixed-length
-//     books never merge; correct, just slower).
-constexpr int kMW = 128;
-constexpr int kM2Threads = 256;
-
-struct MapRow {
-    uint64_t bm0, bm1;
-    uint32_t count, exit;  // phase-0 result (exit packed as in maps)
-};
-
-__device__ __forceinline__ bool mw_test(const MapRow &m, uint32_t q) {
-    return q < 64 ? ((m.bm0 >> q) & 1ull) : ((m.bm1 >> (q - 64)) & 1ull);
-}
-__device__ __forceinline__ uint32_t mw_rank(const MapRow &m, uint32_t q) {  // starts < q
-    return q <= 64 ? __popcll(q == 64 ? m.bm0 : (m.bm0 & ((1ull << q) - 1ull)))
-                   : __popcll(m.bm0) + __popcll(m.bm1 & ((1ull << (q - 64)) - 1ull));
-}
-
-// Decode code words from stream-relative `rel` of subsequence start t0 until
-// rel >= stop; `cnt` counts them.  bulk: boundary LUT while the window stays
-// inside the subsequence.  Returns false on an invalid code word.
-__device__ __forceinline__ bool map_run(const DecParams &p, const uint32_t *s_b, const uint8_t *s_l1,
-                                        const DecCanon *tab, Win6 &r, uint64_t t0, uint32_t &rel,
-                                        uint32_t stop, uint32_t endrel, uint32_t &cnt) {
-    const uint32_t lim = stop >= (uint32_t)kLutBits ? stop - kLutBits : 0;
-    while (rel < stop) {
-        const uint32_t pk = r.peek12();
-        const uint32_t e = s_b[pk];
-        uint32_t n = e & 15u, used = (e >> 4) & 15u;
-        if (n == 0 || rel + kLutBits > stop) {
-            uint32_t L = s_l1[pk], sym;
-            if (!L) L = decode_long(p, tab, t0 + rel, sym);
-            if (L == 0 || rel + L > endrel) return false;
-            n = 1;
-            used = L;
-        }
-        cnt += n;
-        rel += used;
-        if (used <= 32) r.consume(p, used);
-        else r.init(p, t0 + rel);
-    }
-    return true;
-}
-
-__global__ void __launch_bounds__(kM2Threads) k_dec_maps2(DecParams p) {
-    __shared__ uint32_t s_b[kLutSize];
-    __shared__ uint8_t s_l1[kLutSize];
-    __shared__ DecCanon s_can;
-    __shared__ MapRow s_row[kM2Threads];
-    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) {
-        s_b[i] = p.tab->lutb[i];
-        s_l1[i] = p.tab->lut1[i];
-    }
-    load_canon(s_can, p.tab);
-    __syncthreads();
-    const DecCanon *tab = &s_can;
-    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    MapRow *wrow = s_row + warp * 32;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t tb = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); tb < p.T;
-         tb += stride) {
-        // ---------------- A: phase 0, one lane per subsequence ----------------
-        {
-            const uint64_t t = tb + lane;
-            MapRow m;
-            m.bm0 = m.bm1 = 0;
-            m.count = 0;
-            m.exit = kExitInvalid;
-            if (t < p.T) {
-                const uint64_t t0 = t * p.S;
-                const bool last = t == p.T - 1;
-                const uint32_t stop = (uint32_t)((last ? p.bit_len : t0 + p.S) - t0);
-                const uint32_t endrel = (uint32_t)umin64(p.bit_len - t0, 0xFFFFFFF0u);
-                const uint32_t lim = stop >= (uint32_t)kLutBits ? stop - kLutBits : 0;
-                Win6 r;
-                r.init(p, t0);
-                uint32_t rel = 0, cnt = 0;
-                bool ok = true;
-                // window part: record every code-word start below kMW
-                while (ok && rel < stop && rel < (uint32_t)kMW) {
-                    const uint32_t pk = r.peek12();
-                    const uint32_t e = s_b[pk];
-                    uint32_t n = e & 15u, used = (e >> 4) & 15u, starts = e >> 8;
-                    if (n == 0 || rel + kLutBits > stop) {
-                        uint32_t L = s_l1[pk], sym;
-                        if (!L) L = decode_long(p, tab, t0 + rel, sym);
-                        if (L == 0 || rel + L > endrel) { ok = false; break; }
-                        n = 1;
-                        used = L;
-                        starts = 1;
-                    }
-                    if (rel < 64) {
-                        m.bm0 |= (uint64_t)starts << rel;
-                        if (rel > 52) m.bm1 |= (uint64_t)starts >> (64 - rel);
-                    } else {
-                        m.bm1 |= (uint64_t)starts << (rel - 64);
-                    }
-                    cnt += n;
-                    rel += used;
-                    if (used <= 32) r.consume(p, used);
-                    else r.init(p, t0 + rel);
-                }
-                if (ok) ok = map_run(p, s_b, s_l1, tab, r, t0, rel, stop, endrel, cnt);
-                if (ok) {
-                    uint32_t ex;
-                    if (last) ex = (rel == stop) ? kExitEnd : kExitInvalid;
-                    else ex = rel - stop;
-                    m.exit = ex;
-                    m.count = cnt;
-                }
-                p.maps[t * p.P] = m.exit == kExitInvalid ? kExitInvalid : ((m.count << 8) | m.exit);
-            }
-            wrow[lane] = m;
-        }
-        __syncwarp();
-        // ---------------- B: phases 1..P-1 of each subsequence ----------------
-        const uint32_t nrows = (uint32_t)umin64(32, p.T - tb);
-        for (uint32_t j = 0; j < nrows; j++) {
-            const uint64_t t = tb + j;
-            const uint64_t t0 = t * p.S;
-            const bool last = t == p.T - 1;
-            const uint32_t stop = (uint32_t)((last ? p.bit_len : t0 + p.S) - t0);
-            const uint32_t endrel = (uint32_t)umin64(p.bit_len - t0, 0xFFFFFFF0u);
-            const MapRow m = wrow[j];
-            for (uint32_t ph = 1 + lane; ph < p.P; ph += 32) {
-                uint32_t out = kExitInvalid;
-                if (ph < p.S && t0 + ph <= p.bit_len) {
-                    Win6 r;
-                    r.init(p, t0 + ph);
-                    uint32_t rel = ph, cnt = 0;
-                    bool ok = true, merged = false;
-                    const uint32_t wend = stop < (uint32_t)kMW ? stop : (uint32_t)kMW;
-                    while (rel < wend) {
-                        if (mw_test(m, rel)) {
-                            merged = true;
-                            break;
-                        }
-                        uint32_t L = s_l1[r.peek12()], sym;
-                        if (!L) L = decode_long(p, tab, t0 + rel, sym);
-                        if (L == 0 || rel + L > endrel) {
-                            ok = false;
-                            break;
-                        }
-                        cnt++;
-                        rel += L;
-                        if (L <= 32) r.consume(p, L);
-                        else r.init(p, t0 + rel);
-                    }
-                    if (ok && merged) {
-                        if (m.exit != kExitInvalid)
-                            out = ((cnt + m.count - mw_rank(m, rel)) << 8) | m.exit;
-                    } else if (ok) {
-                        // not merged inside the window: decode on to the boundary
-                        ok = map_run(p, s_b, s_l1, tab, r, t0, rel, stop, endrel, cnt);
-                        if (ok) {
-                            uint32_t ex;
-                            if (last) ex = (rel == stop) ? kExitEnd : kExitInvalid;
-                            else ex = rel - stop;
-                            out = ex == kExitInvalid ? kExitInvalid : ((cnt << 8) | ex);
-                        }
-                    }
-                }
-                p.maps[t * p.P + ph] = out;
-            }
-        }
-        __syncwarp();
+                                  sn | (su << 3) | (sm << 8));
     }
 }
 
@@ -1478,142 +1087,7 @@ __global__ void __launch_bounds__(kFThreads) k_dec_final(DecParams p) {
     }
 }
 
-// Final decode, u16 symbols.  Lanes decode their subsequences in lock-step
-// batches of kFSteps lookups (every live lane steps each time, no waiting for
-// slower lanes); a 12-bit lookup yields up to six symbols (lut6), written to
-// the lane's stage row.  After each batch the warp flushes every row's
-// complete 8-symbol pieces with 16-byte stores: a lane's output offset is
-// made 8-aligned by starting its row at column (offset & 7), so only its very
-// first and last pieces are partial.  Pieces are distributed over the lanes
-// by a warp scan of the per-row piece counts.  The 4-word bit window advances
-// without branches, and each lane prefetches its stream 512 bytes ahead.
-constexpr int kF6Threads = 1024;
-constexpr int kFSteps = 4;       // lookups per batch (<= 24 symbols per lane)
-constexpr int kRow = 40;          // stage row (u16): carry <= 7 + 24 symbols + 5 slack
-
-
-__global__ void __launch_bounds__(kF6Threads, 1) k_dec_final6(DecParams p) {
-    extern __shared__ __align__(16) unsigned char f6_smem[];
-    uint4 *s_lut = reinterpret_cast<uint4 *>(f6_smem);
-    uint8_t *s_l1 = reinterpret_cast<uint8_t *>(s_lut + kLutSize);
-    uint16_t *s_stage = reinterpret_cast<uint16_t *>(s_l1 + kLutSize);
-    uint64_t *s_base = reinterpret_cast<uint64_t *>(s_stage + (kF6Threads / 32) * 32 * kRow);
-    uint32_t *s_pre = reinterpret_cast<uint32_t *>(s_base + kF6Threads);   // piece prefix per row
-    uint32_t *s_rng = s_pre + kF6Threads;                                  // lo | hi << 16
-    __shared__ DecCanon s_can;
-    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) {
-        s_lut[i] = p.tab->lut6[i];
-        s_l1[i] = p.tab->lut1[i];
-    }
-    load_canon(s_can, p.tab);
-    __syncthreads();
-    if (p.st->code) return;  // corrupt stream: leave the output untouched
-    const DecCanon *tab = &s_can;
-    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    uint16_t *out = static_cast<uint16_t *>(p.out);
-    const bool vec_out = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    uint16_t *wstage = s_stage + warp * 32 * kRow;
-    uint16_t *row = wstage + lane * kRow;
-    const uint32_t row_s = (uint32_t)__cvta_generic_to_shared(row);
-    uint64_t *wbase = s_base + warp * 32;
-    uint32_t *wpre = s_pre + warp * 32;
-    uint32_t *wrng = s_rng + warp * 32;
-    const uint64_t tstride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t tb = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); tb < p.T;
-         tb += tstride) {
-        const uint64_t t = tb + lane;
-        Win6 r;
-        uint64_t t0 = 0, base = 0;
-        uint32_t rel = 0, stop = 0, k = 0, lo = 0;
-        bool live = false;
-        if (t < p.T) {
-            const uint32_t e = p.ent0[t];
-            if (e != kExitInvalid && e != kExitEnd) {
-                t0 = t * p.S;
-                stop = (uint32_t)(((t == p.T - 1) ? p.bit_len : umin64(t0 + p.S, p.bit_len)) - t0);
-                rel = e;
-                r.init(p, t0 + rel);
-                const uint64_t o = p.off0[t];
-                lo = k = (uint32_t)(o & 7);
-                base = o - k;
-                live = rel < stop;
-            }
-        }
-        const uint32_t lim = stop >= (uint32_t)kLutBits ? stop - kLutBits : 0;
-        bool more = __any_sync(0xffffffffu, live);
-        while (more) {
-            // ---- a batch of lookups ----
-            for (int st = 0; st < kFSteps; st++) {
-                if (live) {
-                    const uint32_t pk = r.peek12();
-                    const uint4 e = s_lut[pk];
-                    uint32_t n = e.w & 7u, adv = e.w >> 3;
-                    uint32_t s01 = e.x;
-                    if (n == 0 || rel + kLutBits > stop) {  // long code word, invalid prefix or subsequence tail
-                        uint32_t L = s_l1[pk], sym = e.x & 0xFFFFu;
-                        if (!L) L = decode_long(p, tab, t0 + rel, sym);
-                        n = L ? 1u : 0u;
-                        adv = L;
-                        s01 = sym;
-                        if (L == 0) rel = stop;  // cannot happen after a successful map pass
-                    }
-                    const uint32_t a = row_s + 2 * k;
-                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)s01));
-                    asm volatile("st.shared.u16 [%0+2], %1;" ::"r"(a), "h"((unsigned short)(s01 >> 16)));
-                    asm volatile("st.shared.u16 [%0+4], %1;" ::"r"(a), "h"((unsigned short)e.y));
-                    asm volatile("st.shared.u16 [%0+6], %1;" ::"r"(a), "h"((unsigned short)(e.y >> 16)));
-                    asm volatile("st.shared.u16 [%0+8], %1;" ::"r"(a), "h"((unsigned short)e.z));
-                    asm volatile("st.shared.u16 [%0+10], %1;" ::"r"(a), "h"((unsigned short)(e.z >> 16)));
-                    k += n;
-                    rel += adv;
-                    if (adv <= 32) r.consume(p, adv);
-                    else r.init(p, t0 + rel);
-                    live = rel < stop;
-                }
-            }
-            // ---- flush complete pieces (all of them once the lane is done) ----
-            const uint32_t np = live ? (k >> 3) : ((k + 7) >> 3);
-            uint32_t inc = np;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= (uint32_t)o) inc += v;
-            }
-            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-            wbase[lane] = base;
-            wpre[lane] = inc - np;
-            wrng[lane] = lo | (k << 16);
-            __syncwarp();
-            for (uint32_t g = lane; g < tot; g += 32) {
-                // row = last j with pre[j] <= g
-                uint32_t rw = 0;
-#pragma unroll
-                for (int b = 16; b > 0; b >>= 1)
-                    if (wpre[rw + b] <= g) rw += b;
-                const uint32_t c0 = (g - wpre[rw]) * 8;
-                const uint32_t rg = wrng[rw];
-                const uint32_t rlo = rg & 0xFFFFu, rhi = rg >> 16;
-                const uint64_t ob = wbase[rw] + c0;
-                const uint16_t *src = wstage + rw * kRow + c0;
-                if (vec_out && c0 >= rlo && c0 + 8 <= rhi && ob + 8 <= p.count) {
-                    *reinterpret_cast<uint4 *>(out + ob) = *reinterpret_cast<const uint4 *>(src);
-                } else {
-                    for (uint32_t c = 0; c < 8; c++)
-                        if (c0 + c >= rlo && c0 + c < rhi && ob + c < p.count) out[ob + c] = src[c];
-                }
-            }
-            __syncwarp();
-            // carry the incomplete piece (<= 7 symbols) to the row start
-            const uint32_t done = np * 8 < k ? np * 8 : k;
-            for (uint32_t c = done; c < k; c++) row[c - done] = row[c];
-            k -= done;
-            base += done;
-            lo = 0;
-            __syncwarp();
-            more = __any_sync(0xffffffffu, live);
-        }
-    }
-}
+#include "lzb_dec3.cuh"
 
 // ----------------------------------------------------------------------------
 struct DecLayout {
@@ -1624,14 +1098,8 @@ struct DecLayout {
 static DecLayout dec_layout(uint64_t bit_len, uint32_t maxlen) {
     DecLayout L;
     L.P = maxlen < 1 ? 1 : maxlen;
-    // enough subsequences to fill the GPU (~2 threads per 148*2048 lanes), S >= 4*P
-    uint64_t S = bit_len / (148ull * 2048ull);
-    if (S < 256) S = 256;
-    if (S > 8192) S = 8192;
-    while (S < 4ull * L.P) S *= 2;
-    S = (S + 31) / 32 * 32;
-    L.S = (uint32_t)S;
-    L.T = bit_len ? (bit_len + S - 1) / S : 1;
+    L.S = kS3;  // one warp per subsequence, one lane per 128-bit microblock (lzb_dec3.cuh)
+    L.T = bit_len ? (bit_len + L.S - 1) / L.S : 1;
     L.G = 256;
     L.ng1 = (L.T + L.G - 1) / L.G;
     L.ng2 = (L.ng1 + L.G - 1) / L.G;
@@ -1650,6 +1118,8 @@ static void dec_scratch(Sc &s, const DecLayout &L, uint32_t cap) {
     s.template take<uint8_t>(L.ng1);
     s.template take<uint64_t>(L.ng1);
     s.template take<uint8_t>(L.T);
+    s.template take<uint64_t>(L.T);
+    s.template take<uint16_t>(L.T * 32);
     s.template take<uint64_t>(L.T);
 }
 
@@ -1866,13 +1336,15 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
     p.off1 = sc.take<uint64_t>(L.ng1);
     p.ent0 = sc.take<uint8_t>(L.T);
     p.off0 = sc.take<uint64_t>(L.T);
-    if (!p.off0) return LZB_E_ARG;
+    p.cp = sc.take<uint16_t>(L.T * 32);
+    p.irr = sc.take<uint64_t>(L.T);
+    if (!p.irr) return LZB_E_ARG;
     p.st = st;
     p.out = sym;
     const int sms = dev_sms();
     // phases >= the book's real max length cannot be entries (P = maxlen hint;
     // k_dec_tables flags a hint that disagrees with the lengths as corrupt).
-    k_dec_maps2<<<(unsigned)umin64((L.T + kM2Threads - 1) / kM2Threads, (uint64_t)sms * 8), kM2Threads, 0, s>>>(p);
+    k_dec_maps3<<<(unsigned)umin64((L.T + kD3Warps - 1) / kD3Warps, (uint64_t)sms * 16), kD3Warps * 32, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
     k_dec_compose<uint32_t><<<(unsigned)umin64((L.ng1 * L.P + 255) / 256, (uint64_t)sms * 32), 256, 0, s>>>(
         p.maps, L.T, L.P, L.G, p.g1, L.ng1);
@@ -1890,11 +1362,11 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
         const unsigned fg = (unsigned)umin64((L.T + kFThreads - 1) / kFThreads, (uint64_t)sms * 4);
         const size_t fsm = kLutSize * sizeof(uint64_t) + (size_t)(kFThreads / 32) * 32 * (kStage + 1) * sym_bytes;
         if (sym_bytes == 2 && cap <= 65536) {
-            const size_t f6 = (size_t)kLutSize * 17 + (size_t)kF6Threads * kRow * 2 +
-                              (size_t)kF6Threads * 16;
-            LZB_CUDA_TRY(cudaFuncSetAttribute(k_dec_final6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f6));
-            const unsigned g6 = (unsigned)umin64((L.T + kF6Threads - 1) / kF6Threads, (uint64_t)sms);
-            k_dec_final6<<<g6, kF6Threads, f6, s>>>(p);
+            const size_t f7 = (size_t)kLutSize * (sizeof(uint4) + 1) + (size_t)kF7Warps * kF7Slots * 2 +
+                              (size_t)kF7Warps * 2 * kStgWords * 4;
+            LZB_CUDA_TRY(cudaFuncSetAttribute(k_dec_final7, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f7));
+            const unsigned g7 = (unsigned)umin64((L.T + kF7Warps - 1) / kF7Warps, (uint64_t)sms);
+            k_dec_final7<<<g7, kF7Warps * 32, f7, s>>>(p);
         } else {
             auto kern = sym_bytes == 2 ? k_dec_final<uint16_t> : k_dec_final<uint32_t>;
             LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));

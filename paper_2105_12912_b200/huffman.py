@@ -93,14 +93,17 @@ def decode(stream: BitStream, book: Codebook) -> np.ndarray:
     data = _to_device(np.asarray(stream.data, np.uint8), np.uint8)
     lens = _to_device(book.lengths, np.uint8)
     maxlen = int(book.lengths.max())
-    out = torch.empty(stream.count, dtype=torch.int32, device="cuda")
+    sb = 2 if book.cap <= 65536 else 4  # u16 symbols take the staged warp decoder
+    out = torch.empty(stream.count, dtype=torch.int16 if sb == 2 else torch.int32, device="cuda")
     st = N.empty_bytes(N.STATUS_BYTES)
     ds = L.lzb_huff_decode_scratch_bytes(stream.bit_len, maxlen, book.cap)
     scr = N.empty_bytes(ds)
     N.check_rc(L.lzb_huff_decode(data.data_ptr(), stream.bit_len, stream.count, lens.data_ptr(),
-                                 book.cap, maxlen, out.data_ptr(), 4, st.data_ptr(),
+                                 book.cap, maxlen, out.data_ptr(), sb, st.data_ptr(),
                                  scr.data_ptr(), ds, N.stream_ptr()), "huff_decode")
     (s,) = N.read_status(st)
     if s.code:
         raise CorruptArchiveError("bit stream does not decode to its declared symbols")
+    if sb == 2:
+        return out.cpu().numpy().view(np.uint16).astype(np.uint32)
     return out.cpu().numpy().view(np.uint32)

@@ -206,3 +206,32 @@ def test_partial_sum_random_2d_3d_with_outliers(cuda):
         q, o = lzb.quantize.construct_grid(lzb.PrequantGrid(dims, pre.reshape(-1)), cfg, spec)
         back = lzb.reconstruct_grid(q, o, cfg, spec)
         assert np.array_equal(back.codes, pre.reshape(-1))
+
+
+def test_huffman_decode_layouts(cuda):
+    """Streams whose lengths straddle the decoder's 128-bit microblocks and
+    4096-bit subsequences, smooth-like (geometric), slowly synchronising
+    (near-uniform, ~8 bits) and deep (> 12-bit code words) books, u16 and u32
+    symbols -- every decode equals the encoded stream."""
+    import paper_2105_12912_b200 as lzb
+
+    rng = np.random.default_rng(2026)
+    books = []
+    g = np.array([int(1e6 * 0.55 ** abs(i - 512)) + 1 for i in range(1024)], np.int64)
+    books.append(g)                                                   # smooth, ~2 bits
+    books.append(rng.integers(50, 200, 300).astype(np.int64))        # ~8 bits, slow sync
+    books.append(np.array([2 ** (20 - i // 3) for i in range(60)], np.int64))  # deep
+    books.append(np.array([1000, 1], np.int64))                      # 1-bit codes
+    for counts in books:
+        p = counts / counts.sum()
+        book = lzb.Codebook.from_counts(counts)
+        for n in (1, 2, 63, 64, 65, 2047, 2048, 2049, 4095, 4096, 4097, 40000, 250_000):
+            stream = rng.choice(len(counts), size=n, p=p).astype(np.uint32)
+            bk = lzb.Codebook.from_counts(np.bincount(stream, minlength=len(counts)))
+            bs = lzb.encode(stream, bk)
+            assert np.array_equal(lzb.decode(bs, bk), stream), (len(counts), n)
+    # u32 symbols (cap > 65536)
+    cap = 1 << 17
+    stream = (rng.geometric(0.3, 100_000) + 70000).astype(np.uint32) % cap
+    bk = lzb.Codebook.from_counts(np.bincount(stream, minlength=cap))
+    assert np.array_equal(lzb.decode(lzb.encode(stream, bk), bk), stream)
