@@ -24,8 +24,25 @@
 
 #include "lzb_common.cuh"
 #include "lzb_quant3d.cuh"
+#include "lzb_quant3t.cuh"
 
 namespace lzb {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda);
+// a cached function pointer, nullptr if the driver lacks it.
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        tried = true;
+    }
+    return fn;
+}
 
 constexpr int kQThreads = 256;
 constexpr int kTile = 4096;  // max elements per tile (16 per thread)
@@ -699,6 +716,32 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
         size_t smem = (size_t)kQ3Warps * 2 * 32 * 16 * (dtype == 0 ? 4 : 8) +
                       (size_t)kQ3Warps * 512 * code_bytes + (size_t)kQ3Warps * 16 * 32 * 4 +
                       (size_t)cap * 4;
+        const bool tma = dtype == 0 && code_bytes == 2 && q3.vec_ok && (g.nbx % 8 == 0) && tma_encode();
+        if (tma) {
+            T1Params tp;
+            tp.q = q3;
+            tp.tpr = (uint32_t)(g.nbx / 8);
+            CUtensorMap map;
+            cuuint64_t dims[3] = {g.nx, g.ny, g.nz};
+            cuuint64_t strides[2] = {g.nx * 4, g.nx * g.ny * 4};
+            cuuint32_t box[3] = {32, 8, 8};
+            cuuint32_t estr[3] = {1, 1, 1};
+            if (tma_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(x), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return LZB_E_CUDA;
+            const size_t tsm = (size_t)kT1Stages * kT1Tile + 1024 + (size_t)kT1Warps * 16 * 32 * 4 +
+                               (size_t)kT1Warps * 512 * 2 + (size_t)cap * 4;
+            LZB_CUDA_TRY(cudaFuncSetAttribute(k_quantize3d8_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+            int per_sm = 0;
+            LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantize3d8_tma, kT1Threads, tsm));
+            if (per_sm < 1) per_sm = 1;
+            const uint64_t grid = umin64((uint64_t)device_sms() * per_sm, q3.ntiles);
+            tp.step_q = (uint32_t)((grid ? grid : 1) / tp.tpr);
+            tp.step_rem = (uint32_t)((grid ? grid : 1) % tp.tpr);
+            k_quantize3d8_tma<<<(unsigned)(grid ? grid : 1), kT1Threads, tsm, s>>>(tp, map);
+            LZB_LAUNCH_CHECK();
+        }
         auto launch = [&](auto kern) -> int {
             LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int per_sm = 0;
@@ -709,7 +752,9 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
             LZB_LAUNCH_CHECK();
             return LZB_OK;
         };
-        if (dtype == 0)
+        if (tma)
+            rc = LZB_OK;
+        else if (dtype == 0)
             rc = code_bytes == 2 ? launch(k_quantize3d8<float, uint16_t>) : launch(k_quantize3d8<float, uint32_t>);
         else
             rc = code_bytes == 2 ? launch(k_quantize3d8<double, uint16_t>) : launch(k_quantize3d8<double, uint32_t>);

@@ -223,3 +223,36 @@ def test_corruption_raises(cuda):
     struct.pack_into("<Q", blob, o + 16, struct.unpack_from("<Q", blob, o)[0])  # duplicate index
     with pytest.raises(lzb.CorruptArchiveError):
         lzb.decompress(bytes(blob))
+
+
+def test_tma_tile_path_3d(cuda):
+    """ChunkSpec(8,8,8) f32 grids whose chunk rows hold whole 8-chunk tiles
+    (nx a multiple of 64) take K1's TMA path: smooth, noisy (non-origin and
+    > 4-per-chunk outliers), partial y/z chunk layers, values on exact rounding
+    ties and values too large for the int32 fast path -- all byte-identical to
+    the oracle."""
+    lzb = _lzb()
+    rng = np.random.default_rng(64)
+    cases = []
+    cases.append((smooth((24, 32, 128)), dict(eb=1e-4)))
+    cases.append((smooth((21, 19, 64)), dict(eb=1e-3)))                        # partial y/z chunks
+    noisy = (rng.standard_normal((16, 16, 192)) * 50).astype(np.float32)
+    cases.append((noisy, dict(eb=1e-4, cap=64)))                               # many outliers
+    cases.append((noisy, dict(eb=1e-2, cap=4)))
+    ties = (np.round(rng.uniform(-300, 300, (8, 8, 64))) + 0.5).astype(np.float32) * np.float32(0.5)
+    cases.append((ties, dict(eb=0.25, eb_mode="abs")))                         # x / (2 eb) on a .5 tie
+    big = smooth((16, 8, 64)) * np.float32(1e4)
+    cases.append((big, dict(eb=1e-9, eb_mode="abs", cap=1024)))                # |q| >= 2^22: exact path
+    for vals, kw in cases:
+        f = lzb.Field.from_array(vals)
+        d = f.dims
+        try:
+            ref = O.compress(f.values, d.as_tuple(), f.vmin, f.vmax, **kw)
+        except Exception as ex:  # the reference raises (e.g. overflow): so must we
+            with pytest.raises(Exception) as ei:
+                lzb.compress(f, **kw)
+            assert type(ei.value).__name__ == type(ex).__name__
+            continue
+        got = lzb.compress(f, **kw)
+        assert got == ref, (vals.shape, kw)
+        assert np.array_equal(lzb.decompress(got).values, O.decompress(ref)[0])
