@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 
 #include "../../include/lzb.h"
@@ -15,6 +16,23 @@
 #define LZB_LAUNCH_CHECK() LZB_CUDA_TRY(cudaGetLastError())
 
 namespace lzb {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda);
+// a cached function pointer, nullptr if the driver lacks it.
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        tried = true;
+    }
+    return fn;
+}
+
 
 constexpr int kNumSMs = 148;  // B200; launch sizes are re-derived from the device at runtime
 

@@ -28,22 +28,6 @@
 
 namespace lzb {
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda);
-// a cached function pointer, nullptr if the driver lacks it.
-static PFN_cuTensorMapEncodeTiled_v12000 tma_encode() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        void *f = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-        tried = true;
-    }
-    return fn;
-}
-
 constexpr int kQThreads = 256;
 constexpr int kTile = 4096;  // max elements per tile (16 per thread)
 constexpr int kSeg = kTile / kQThreads;

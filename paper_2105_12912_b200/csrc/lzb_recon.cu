@@ -21,6 +21,8 @@
 // written in grid order (coalesced along x) with a fused min/max/finite
 // reduction.  Prefix sums along different axes commute, so the order of the
 // three passes does not matter for the (exact integer) result.
+#include <string.h>
+
 #include "lzb_common.cuh"
 #include "lzb_recon3d.cuh"
 
@@ -726,20 +728,40 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
             r3.ticket = &tick[1];
             const size_t osz = dtype == 0 ? 4 : 8;
             r3.vec_ok = (g.nx % (16 / osz) == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
+            // f32 output through TMA tensor stores (8x8x8 boxes) when the
+            // driver exposes the tensor-map encoder and no int64 copy is asked for
+            CUtensorMap ymap;
+            memset(&ymap, 0, sizeof(ymap));
+            bool tma = dtype == 0 && !prequant_out && r3.vec_ok && tma_encode() != nullptr;
+            if (tma) {
+                cuuint64_t dims[3] = {g.nx, g.ny, g.nz};
+                cuuint64_t strides[2] = {g.nx * 4, g.nx * g.ny * 4};
+                cuuint32_t box[3] = {8, 8, 8};
+                cuuint32_t estr[3] = {1, 1, 1};
+                tma = tma_encode()(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, y, dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            }
+            const size_t ysm = tma ? (size_t)kR3Warps * 4096 : 0;
             auto launch = [&](auto kern) -> int {
+                if (ysm) LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ysm));
                 int per_sm = 0;
-                LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kR3Threads, 0));
+                LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kR3Threads, ysm));
                 if (per_sm < 1) per_sm = 1;
                 uint64_t grid = umin64((uint64_t)sm * per_sm, (L.ntiles + kR3Warps - 1) / kR3Warps);
-                kern<<<(unsigned)(grid ? grid : 1), kR3Threads, 0, s>>>(r3);
+                kern<<<(unsigned)(grid ? grid : 1), kR3Threads, ysm, s>>>(r3, ymap);
                 LZB_LAUNCH_CHECK();
                 return LZB_OK;
             };
             int rc;
             if (code_bytes == 2)
-                rc = dtype == 0 ? launch(k_reconstruct3d8<uint16_t, float>) : launch(k_reconstruct3d8<uint16_t, double>);
+                rc = dtype == 0 ? (tma ? launch(k_reconstruct3d8<uint16_t, float, true>)
+                                       : launch(k_reconstruct3d8<uint16_t, float, false>))
+                                : launch(k_reconstruct3d8<uint16_t, double, false>);
             else
-                rc = dtype == 0 ? launch(k_reconstruct3d8<uint32_t, float>) : launch(k_reconstruct3d8<uint32_t, double>);
+                rc = dtype == 0 ? (tma ? launch(k_reconstruct3d8<uint32_t, float, true>)
+                                       : launch(k_reconstruct3d8<uint32_t, float, false>))
+                                : launch(k_reconstruct3d8<uint32_t, double, false>);
             if (rc) return rc;
             unsigned gf = (unsigned)umin64((n + 255) / 256, (uint64_t)sm * 8);
             if (dtype == 0) k_first_nonfinite<float><<<gf, 256, 0, s>>>((const float *)y, n, mm);

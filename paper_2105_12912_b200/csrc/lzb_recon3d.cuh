@@ -104,7 +104,7 @@ __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch,
                                          uint64_t r0, uint64_t r1, uint32_t lane, OutT &vmin,
                                          OutT &vmax, bool &overflow, const SymT *stg = nullptr,
                                          bool reg_out = false, uint32_t rkey = 0, int32_t rd = 0,
-                                         uint32_t nrec = 0) {
+                                         uint32_t nrec = 0, uint32_t ybuf_s = 0) {
     const uint32_t ly = lane & 7, lz0 = (lane >> 3) * 2;
     const SymT *cs = static_cast<const SymT *>(p.codes) + ch.base;
     I v0[8], v1[8];
@@ -174,7 +174,15 @@ __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch,
                 vmax = fmax(vmax, o[j]);
             }
         }
-        if (fast && p.vec_ok) {
+        if (fast && ybuf_s) {  // into the warp's TMA store tile: row ly + 8 lz, 32 bytes
+            if constexpr (sizeof(OutT) == 4) {
+                const uint32_t a = ybuf_s + (ly + 8 * (lz0 + h)) * 32;
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(o[0]), "f"(o[1]), "f"(o[2]),
+                             "f"(o[3]));
+                asm volatile("st.shared.v4.f32 [%0+16], {%1, %2, %3, %4};" ::"r"(a), "f"(o[4]), "f"(o[5]),
+                             "f"(o[6]), "f"(o[7]));
+            }
+        } else if (fast && p.vec_ok) {
             if constexpr (sizeof(OutT) == 4) {
                 float4 *dst = reinterpret_cast<float4 *>(yo + gi);
                 dst[0] = make_float4(o[0], o[1], o[2], o[3]);
@@ -226,10 +234,28 @@ __device__ __forceinline__ void r3_prefetch(const R3Params &p, const f3::Chunk &
                          : "memory");
 }
 
-template <typename SymT, typename OutT>
-__global__ void __launch_bounds__(kR3Threads, 3) k_reconstruct3d8(const __grid_constant__ R3Params p) {
+// TMA store of one finished chunk (8x8x8 f32 box) from the warp's tile buffer
+__device__ __forceinline__ void r3_tma_store(const CUtensorMap *map, uint32_t src, uint64_t x, uint64_t y,
+                                             uint64_t z) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"((int)x), "r"((int)y), "r"((int)z), "r"(src)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// TMA: full f32 chunks leave through a per-warp double-buffered shared tile
+// and one TMA tensor store each (the 32-byte row fragments of a chunk are
+// scattered over 64 rows; as plain stores they saturate L1).
+template <typename SymT, typename OutT, bool TMA>
+__global__ void __launch_bounds__(kR3Threads, TMA ? 2 : 3)
+    k_reconstruct3d8(const __grid_constant__ R3Params p, const __grid_constant__ CUtensorMap ymap) {
     // per-warp double buffer of the next chunk's code rows (16 symbols per lane)
     __shared__ __align__(16) SymT s_stage[kR3Warps][2][32 * 16];
+    // TMA: per-warp double-buffered 2 KB output tiles (dynamic shared memory)
+    extern __shared__ __align__(128) float s_y[];
+    const uint32_t ybase_s = (uint32_t)__cvta_generic_to_shared(s_y) + (threadIdx.x >> 5) * 4096;
+    uint32_t nb = 0;  // TMA store tiles issued by this warp
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     // piece-major: 16-byte piece k of lane l at byte k * 512 + 16 l (conflict-free)
     const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(&s_stage[warp][0][0]) + lane * 16;
@@ -288,9 +314,22 @@ __global__ void __launch_bounds__(kR3Threads, 3) k_reconstruct3d8(const __grid_c
                 vmin = mmv[0];
                 vmax = mmv[1];
             } else {
+                const bool tma = TMA && cur.full;
+                uint32_t yb = 0;
+                if (tma) {
+                    yb = ybase_s + (nb & 1u) * 2048;
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    __syncwarp();
+                }
                 r3_chunk<SymT, OutT, int32_t>(p, cur, k, r0, r1, lane, vmin, vmax, overflow,
                                               cur_pf ? reinterpret_cast<const SymT *>(reinterpret_cast<const unsigned char *>(&s_stage[warp][sb][0]) + lane * 16) : nullptr,
-                                              reg_out, rkey, rd, nrec);
+                                              reg_out, rkey, rd, nrec, yb);
+                if (tma) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) r3_tma_store(&ymap, yb, cur.x0, cur.y0, cur.z0);
+                    nb++;
+                }
             }
             cur = nxt;
             cur_pf = nxt_pf;
@@ -298,6 +337,7 @@ __global__ void __launch_bounds__(kR3Threads, 3) k_reconstruct3d8(const __grid_c
         }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+    if (TMA && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         OutT a = __shfl_xor_sync(f3::kFull, vmin, o), b = __shfl_xor_sync(f3::kFull, vmax, o);
