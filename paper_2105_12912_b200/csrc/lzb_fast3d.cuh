@@ -95,6 +95,31 @@ __device__ __forceinline__ Chunk chunk_of(const Geom &g, uint64_t c) {
     return k;
 }
 
+// chunk at coordinates (bx, by, bz): no divisions
+__device__ __forceinline__ Chunk chunk_at(const Geom &g, uint64_t bx, uint64_t by, uint64_t bz) {
+    Chunk k;
+    k.x0 = bx * 8;
+    k.y0 = by * 8;
+    k.z0 = bz * 8;
+    k.ex = (uint32_t)umin64(8, g.nx - k.x0);
+    k.ey = (uint32_t)umin64(8, g.ny - k.y0);
+    k.ez = (uint32_t)umin64(8, g.nz - k.z0);
+    k.full = (k.ex == 8) & (k.ey == 8) & (k.ez == 8);
+    k.base = g.nx * g.ny * 8 * bz + g.nx * (uint64_t)k.ez * 8 * by + (uint64_t)k.ez * k.ey * 8 * bx;
+    return k;
+}
+
+// next chunk ordinal: x-chunks fastest, then y, then z
+__device__ __forceinline__ void chunk_step(const Geom &g, uint64_t &bx, uint64_t &by, uint64_t &bz) {
+    if (++bx == g.nbx) {
+        bx = 0;
+        if (++by == g.nby) {
+            by = 0;
+            ++bz;
+        }
+    }
+}
+
 // local stream position of (lx, ly, lz) inside the chunk
 __device__ __forceinline__ uint32_t lpos(const Chunk &k, uint32_t lx, uint32_t ly, uint32_t lz) {
     return lx + k.ex * (ly + k.ey * lz);

@@ -167,12 +167,20 @@ __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch,
         const uint64_t gi = ch.x0 + p.g.nx * ((ch.y0 + ly) + p.g.ny * (ch.z0 + lz0 + h));
         OutT o[8];
 #pragma unroll
-        for (int j = 0; j < 8; j++) {
-            o[j] = (OutT)__dmul_rn((double)v[j], p.two_eb);
-            if ((mm >> j) & 1u) {  // outputs are never NaN: plain min/max instructions
+        for (int j = 0; j < 8; j++) o[j] = (OutT)__dmul_rn((double)v[j], p.two_eb);
+        if (fast) {  // outputs are never NaN: plain min/max instructions
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
                 vmin = fmin(vmin, o[j]);
                 vmax = fmax(vmax, o[j]);
             }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if ((mm >> j) & 1u) {
+                    vmin = fmin(vmin, o[j]);
+                    vmax = fmax(vmax, o[j]);
+                }
         }
         if (fast && ybuf_s) {  // into the warp's TMA store tile: row ly + 8 lz, 32 bytes
             if constexpr (sizeof(OutT) == 4) {
@@ -290,7 +298,8 @@ __global__ void __launch_bounds__(kR3Threads, TMA ? 2 : 3)
             for (uint32_t m = wm; m; m &= m - 1)
                 wide_mask |= 1u << (__shfl_sync(f3::kFull, rkey, __ffs(m) - 1) >> 9);
         }
-        f3::Chunk cur = f3::chunk_of(p.g, c0);
+        uint64_t cbx = c0 % p.g.nbx, cby = (c0 / p.g.nbx) % p.g.nby, cbz = (c0 / p.g.nbx) / p.g.nby;
+        f3::Chunk cur = f3::chunk_at(p.g, cbx, cby, cbz);
         bool cur_pf = cur.full && (cur.base & 7) == 0;
         if (cur_pf) r3_prefetch<SymT>(p, cur, lane, stage_s);
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -300,7 +309,8 @@ __global__ void __launch_bounds__(kR3Threads, TMA ? 2 : 3)
             f3::Chunk nxt;
             bool nxt_pf = false;
             if (c + 1 < c1) {
-                nxt = f3::chunk_of(p.g, c + 1);
+                f3::chunk_step(p.g, cbx, cby, cbz);
+                nxt = f3::chunk_at(p.g, cbx, cby, cbz);
                 nxt_pf = nxt.full && (nxt.base & 7) == 0;
                 if (nxt_pf) r3_prefetch<SymT>(p, nxt, lane, stage_s + (sb ^ 1) * kBuf);
             }
