@@ -164,7 +164,6 @@ __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch,
     for (int h = 0; h < 2; h++) {
         const I(&v)[8] = h ? v1 : v0;
         const uint32_t mm = h ? m1 : m0;
-        const uint64_t gi = ch.x0 + p.g.nx * ((ch.y0 + ly) + p.g.ny * (ch.z0 + lz0 + h));
         OutT o[8];
 #pragma unroll
         for (int j = 0; j < 8; j++) o[j] = (OutT)__dmul_rn((double)v[j], p.two_eb);
@@ -191,6 +190,7 @@ __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch,
                              "f"(o[6]), "f"(o[7]));
             }
         } else if (fast && p.vec_ok) {
+            const uint64_t gi = ch.x0 + p.g.nx * ((ch.y0 + ly) + p.g.ny * (ch.z0 + lz0 + h));
             if constexpr (sizeof(OutT) == 4) {
                 float4 *dst = reinterpret_cast<float4 *>(yo + gi);
                 dst[0] = make_float4(o[0], o[1], o[2], o[3]);
@@ -204,6 +204,7 @@ __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch,
 #pragma unroll
                 for (int j = 0; j < 8; j++) p.pre[gi + j] = (int64_t)v[j];
         } else if (mm) {
+            const uint64_t gi = ch.x0 + p.g.nx * ((ch.y0 + ly) + p.g.ny * (ch.z0 + lz0 + h));
 #pragma unroll
             for (int j = 0; j < 8; j++)
                 if ((mm >> j) & 1u) {
@@ -309,8 +310,17 @@ __global__ void __launch_bounds__(kR3Threads, TMA ? 2 : 3)
             f3::Chunk nxt;
             bool nxt_pf = false;
             if (c + 1 < c1) {
-                f3::chunk_step(p.g, cbx, cby, cbz);
-                nxt = f3::chunk_at(p.g, cbx, cby, cbz);
+                if (cbx + 1 < p.g.nbx) {  // same chunk row: advance along x
+                    cbx++;
+                    nxt = cur;
+                    nxt.x0 += 8;
+                    nxt.base += (uint64_t)cur.ez * cur.ey * 8;
+                    nxt.ex = (uint32_t)umin64(8, p.g.nx - nxt.x0);
+                    nxt.full = (nxt.ex == 8) & (nxt.ey == 8) & (nxt.ez == 8);
+                } else {
+                    f3::chunk_step(p.g, cbx, cby, cbz);
+                    nxt = f3::chunk_at(p.g, cbx, cby, cbz);
+                }
                 nxt_pf = nxt.full && (nxt.base & 7) == 0;
                 if (nxt_pf) r3_prefetch<SymT>(p, nxt, lane, stage_s + (sb ^ 1) * kBuf);
             }
