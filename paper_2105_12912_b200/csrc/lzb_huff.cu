@@ -393,16 +393,12 @@ __global__ void __launch_bounds__(256) k_huff_scan_w(const __grid_constant__ Enc
 // stage slot of 16-byte piece q (0..127): conflict-free for lane l reading 4l+k
 __device__ __forceinline__ uint32_t wswz(uint32_t q) { return q ^ ((q >> 3) & 7u); }
 
-// Pack one lane's 32 code words at tile-relative bit `off`: a 32-bit
-// accumulator, completed words stored with predicated st.shared (interior
-// words belong to this lane alone) or red.shared.or (the first word when the
-// lane starts mid-word); the final partial word is OR-ed.  No branches, so
-// the warp never diverges.
 // Pack one lane's 32 code words at tile-relative bit `off` with a 32-bit
-// accumulator.  Every word the lane COMPLETES is stored plainly (only the lane
+// accumulator, two symbols per step when their code words fit 32 bits
+// together.  Every word the lane COMPLETES is stored plainly (only the lane
 // holding a word's last bit completes it; bits of earlier lanes in that word
 // are zero here and are OR-ed in afterwards); the lane's final partial word is
-// returned for a red.shared.or after a __syncwarp.  Branch-free.
+// returned for a red.shared.or after a __syncwarp.
 template <bool FULL>
 __device__ __forceinline__ void enc_pack_lane(const uint4 (&v)[4], uint32_t nv, uint32_t off,
                                               uint32_t words_s, const uint64_t *s_tab,
@@ -410,16 +406,8 @@ __device__ __forceinline__ void enc_pack_lane(const uint4 (&v)[4], uint32_t nv, 
                                               uint32_t &last_val, uint32_t &last_n) {
     uint32_t n = off & 31, cur = 0;
     uint32_t waddr = words_s + ((off >> 5) << 2);
-#pragma unroll
-    for (int i = 0; i < kWSyms; i++) {
-        const uint32_t sv = sym16(v[i >> 3], i & 7);
-        const uint64_t e = s_tab[sv < capm1 ? sv : capm1];
-        uint32_t L = (uint32_t)(e >> 32);
-        uint32_t c = (uint32_t)e;  // left-aligned; 0 when L == 0
-        if (!FULL) {
-            L = (uint32_t)i < nv ? L : 0u;
-            c = L ? c : 0u;
-        }
+    // one accumulator step for a left-aligned code word c of L <= 32 bits
+    auto step = [&](uint32_t c, uint32_t L) {
         cur |= c >> n;
         const uint32_t nn = n + L;
         const uint32_t f = nn >= 32 ? 1u : 0u;
@@ -430,6 +418,29 @@ __device__ __forceinline__ void enc_pack_lane(const uint4 (&v)[4], uint32_t nv, 
         cur = f ? rem : cur;
         waddr += f << 2;
         n = nn - (f << 5);
+    };
+    // symbols in pairs: two code words that fit 32 bits together take one step
+#pragma unroll
+    for (int i = 0; i < kWSyms / 2; i++) {
+        const uint4 &q = v[i >> 2];
+        const uint32_t w = (i & 3) == 0 ? q.x : (i & 3) == 1 ? q.y : (i & 3) == 2 ? q.z : q.w;
+        const uint32_t s0 = min(w & 0xFFFFu, capm1), s1 = min(w >> 16, capm1);
+        const uint64_t e0 = s_tab[s0], e1 = s_tab[s1];
+        uint32_t L0 = (uint32_t)(e0 >> 32), L1 = (uint32_t)(e1 >> 32);
+        uint32_t c0 = (uint32_t)e0, c1 = (uint32_t)e1;  // left-aligned; 0 when L == 0
+        if (!FULL) {
+            L0 = (uint32_t)(2 * i) < nv ? L0 : 0u;
+            c0 = L0 ? c0 : 0u;
+            L1 = (uint32_t)(2 * i + 1) < nv ? L1 : 0u;
+            c1 = L1 ? c1 : 0u;
+        }
+        const uint32_t L = L0 + L1;
+        if (L <= 32) {
+            step(c0 | __funnelshift_rc(c1, 0u, L0), L);  // c1 >> L0 (0 for L0 == 32)
+        } else {
+            step(c0, L0);
+            step(c1, L1);
+        }
     }
     last_addr = waddr;
     last_val = cur;
