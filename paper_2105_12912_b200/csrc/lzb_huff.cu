@@ -616,9 +616,6 @@ struct DecTables {
     // longer than 12 bits or invalid prefix), 2-5/6-9/10-13 their lengths,
     // 16-31/32-47/48-63 their symbols (books with cap > 65536 use count 0).
     uint64_t lutm[kLutSize];
-    // Count-only LUT for the phase-map pass: all complete code words greedily
-    // decoded from the 12-bit window (up to 7): count | bits consumed << 3.
-    uint16_t lutc[kLutSize];
     uint8_t lut1[kLutSize];  // first code word: len <= 12, or 0x80 | shortest long len, 0 invalid
     // Six-symbol LUT for the final decode (u16 books): the code words greedily
     // decoded from the 12-bit window, up to six: s[0..5], then
@@ -827,104 +824,86 @@ __global__ void k_dec_tables(const uint8_t *lengths, uint32_t cap, uint32_t maxl
         }
     }
     __syncthreads();
-    // multi-symbol LUT: greedy decode of up to three code words in 12 bits
-    for (uint32_t v = threadIdx.x; v < kLutSize; v += blockDim.x) {
-        uint64_t e = 0;
-        uint32_t used = 0, n = 0;
-        if (cap <= 65536) {
-            for (int i = 0; i < 3; i++) {
-                bool found = false;
-                for (uint32_t L = 1; L + used <= (uint32_t)kLutBits && L <= s_max; L++) {
-                    const uint32_t code = (v >> (kLutBits - used - L)) & ((1u << L) - 1u);
-                    const uint64_t f = tab->first[L], k = tab->cnt[L];
-                    if (k && code >= f && code - f < k) {
-                        const uint32_t sym = syms[tab->off[L] + (uint32_t)(code - f)];
-                        e |= (uint64_t)L << (2 + 4 * i);
-                        e |= (uint64_t)sym << (16 + 16 * i);
-                        used += L;
-                        n++;
-                        found = true;
-                        break;
-                    }
-                }
-                if (!found) break;
+}
+
+// LUTs over every 12-bit window, one window per thread: a single greedy pass
+// decodes the complete code words inside the window (up to 12); every LUT
+// variant is a prefix of that sequence.
+__global__ void __launch_bounds__(1024) k_dec_luts(DecTables *tab, const uint32_t *syms, uint32_t cap,
+                                                   lzb_dstatus *st) {
+    __shared__ uint64_t s_first[65], s_cnt[65];
+    __shared__ uint32_t s_off[65];
+    for (uint32_t i = threadIdx.x; i < 65; i += blockDim.x) {
+        s_first[i] = tab->first[i];
+        s_cnt[i] = tab->cnt[i];
+        s_off[i] = tab->off[i];
+    }
+    __syncthreads();
+    if (st->code) return;
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= kLutSize) return;
+    const uint32_t maxlen = tab->maxlen;
+    const bool wide_cap = cap > 65536;  // symbols do not fit the u16 LUT fields
+    uint32_t len[12], sym[12], n = 0, used = 0;
+    while (n < 12) {
+        uint32_t L = 0, sy = 0;
+        for (uint32_t l = 1; l + used <= (uint32_t)kLutBits && l <= maxlen; l++) {
+            const uint32_t code = (v >> (kLutBits - used - l)) & ((1u << l) - 1u);
+            const uint64_t f = s_first[l], k = s_cnt[l];
+            if (k && code >= f && code - f < k) {
+                L = l;
+                sy = wide_cap ? 0u : syms[s_off[l] + (uint32_t)(code - f)];
+                break;
             }
         }
-        tab->lutm[v] = e | n;
-        // count-only entry
-        uint32_t cu = 0, cn = 0;
-        while (cn < 7) {
-            bool found = false;
-            for (uint32_t L = 1; L + cu <= (uint32_t)kLutBits && L <= s_max; L++) {
-                const uint32_t code = (v >> (kLutBits - cu - L)) & ((1u << L) - 1u);
-                const uint64_t f = tab->first[L], k = tab->cnt[L];
-                if (k && code >= f && code - f < k) {
-                    cu += L;
-                    cn++;
-                    found = true;
-                    break;
-                }
-            }
-            if (!found) break;
+        if (!L) break;
+        len[n] = L;
+        sym[n] = sy;
+        used += L;
+        n++;
+    }
+    // lutm: up to three code words (count 0 for cap > 65536)
+    {
+        const uint32_t m = wide_cap ? 0u : (n < 3 ? n : 3u);
+        uint64_t e = m;
+        for (uint32_t i = 0; i < m; i++) {
+            e |= (uint64_t)len[i] << (2 + 4 * i);
+            e |= (uint64_t)sym[i] << (16 + 16 * i);
         }
-        tab->lutc[v] = (uint16_t)(cn | (cu << 3));
-        {  // first code word: its length if <= 12 bits, else 0x80 | the shortest
-           // length of a code word with this 12-bit prefix, 0 = invalid prefix
-            uint32_t l1 = 0;
-            for (uint32_t L = 1; L <= s_max && !l1; L++) {
-                const uint64_t f = tab->first[L], k = tab->cnt[L];
-                if (!k) continue;
-                if (L <= (uint32_t)kLutBits) {
-                    const uint32_t code = v >> (kLutBits - L);
-                    if (code >= f && code - f < k) l1 = L;
-                } else {  // some code of length L, in [f, f + k), has the prefix v
-                    const uint32_t sh = L - kLutBits;
-                    if ((f >> sh) <= v && v <= ((f + (k - 1)) >> sh)) l1 = 0x80u | L;
-                }
-            }
-            tab->lut1[v] = (uint8_t)l1;
+        tab->lutm[v] = e;
+    }
+    // lut6: up to six code words, their starts
+    {
+        const uint32_t m = wide_cap ? 0u : (n < 6 ? n : 6u);
+        uint32_t s6[6] = {0, 0, 0, 0, 0, 0}, u = 0, sm = 0;
+        for (uint32_t i = 0; i < m; i++) {
+            s6[i] = sym[i];
+            sm |= 1u << u;
+            u += len[i];
         }
-        // six-symbol entry
-        uint32_t sy[6] = {0, 0, 0, 0, 0, 0};
-        uint32_t su = 0, sn = 0, sm = 0;
-        if (cap <= 65536) {
-            while (sn < 6) {
-                bool found = false;
-                for (uint32_t L = 1; L + su <= (uint32_t)kLutBits && L <= s_max; L++) {
-                    const uint32_t code = (v >> (kLutBits - su - L)) & ((1u << L) - 1u);
-                    const uint64_t f = tab->first[L], k = tab->cnt[L];
-                    if (k && code >= f && code - f < k) {
-                        sy[sn++] = syms[tab->off[L] + (uint32_t)(code - f)];
-                        sm |= 1u << su;
-                        su += L;
-                        found = true;
-                        break;
-                    }
-                }
-                if (!found) break;
-            }
+        tab->lut6[v] = make_uint4(s6[0] | (s6[1] << 16), s6[2] | (s6[3] << 16), s6[4] | (s6[5] << 16),
+                                  m | (u << 3) | (sm << 8));
+    }
+    // lutb: all complete code words (count-only), their starts
+    {
+        uint32_t u = 0, sm = 0;
+        for (uint32_t i = 0; i < n; i++) {
+            sm |= 1u << u;
+            u += len[i];
         }
-        {
-            uint32_t bu = 0, bn = 0, bm = 0;
-            while (bn < 12) {
-                bool found = false;
-                for (uint32_t L = 1; L + bu <= (uint32_t)kLutBits && L <= s_max; L++) {
-                    const uint32_t code = (v >> (kLutBits - bu - L)) & ((1u << L) - 1u);
-                    const uint64_t f = tab->first[L], k = tab->cnt[L];
-                    if (k && code >= f && code - f < k) {
-                        bm |= 1u << bu;
-                        bu += L;
-                        bn++;
-                        found = true;
-                        break;
-                    }
-                }
-                if (!found) break;
-            }
-            tab->lutb[v] = bn | (bu << 4) | (bm << 8);
+        tab->lutb[v] = n | (u << 4) | (sm << 8);
+    }
+    // lut1: first code word: its length if <= 12 bits, else 0x80 | the shortest
+    // length of a code word with this 12-bit prefix, 0 = invalid prefix
+    {
+        uint32_t l1 = n ? len[0] : 0u;
+        for (uint32_t L = kLutBits + 1; L <= maxlen && !l1; L++) {
+            const uint64_t f = s_first[L], k = s_cnt[L];
+            if (!k) continue;
+            const uint32_t sh = L - kLutBits;
+            if ((f >> sh) <= v && v <= ((f + (k - 1)) >> sh)) l1 = 0x80u | L;
         }
-        tab->lut6[v] = make_uint4(sy[0] | (sy[1] << 16), sy[2] | (sy[3] << 16), sy[4] | (sy[5] << 16),
-                                  sn | (su << 3) | (sm << 8));
+        tab->lut1[v] = (uint8_t)l1;
     }
 }
 
@@ -1311,6 +1290,8 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
     uint32_t *syms = sc.take<uint32_t>(cap);
     if (!syms) return LZB_E_ARG;
     k_dec_tables<<<1, 1024, 0, s>>>(lengths, cap, maxlen, tab, syms, st);
+    LZB_LAUNCH_CHECK();
+    k_dec_luts<<<kLutSize / 1024, 1024, 0, s>>>(tab, syms, cap, st);
     LZB_LAUNCH_CHECK();
     if (count == 0) {
         // P/huffman.py:114-117
