@@ -522,31 +522,60 @@ __global__ void k_gen_dequant(const int64_t *q, uint64_t n, double two_eb, OutT 
 }
 
 // ---- field range (P/grid.py:155-202) ----
+// One streaming pass: 16-byte loads, four in flight per thread, min/max in the
+// input precision (exact), the first non-finite offset by an atomic min.
 template <typename InT>
-__global__ void k_field_range(const InT *x, uint64_t n, unsigned long long *mm) {
-    double vmin = INFINITY, vmax = -INFINITY;
+__device__ __forceinline__ void fr_take(InT v, uint64_t i, InT &vmin, InT &vmax, unsigned long long &bad) {
+    if (!isfinite(v)) {
+        if (i < bad) bad = i;
+    } else {
+        vmin = v < vmin ? v : vmin;
+        vmax = v > vmax ? v : vmax;
+    }
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(256) k_field_range(const InT *x, uint64_t n, unsigned long long *mm) {
+    constexpr int V = 16 / sizeof(InT);  // elements per 16-byte load
+    constexpr int U = 4;                 // loads in flight per thread
+    InT vmin = (InT)INFINITY, vmax = (InT)-INFINITY;
     unsigned long long bad = ~0ull;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        double v = (double)x[i];
-        if (!isfinite(v)) {
-            if (i < bad) bad = i;
-        } else {
-            vmin = fmin(vmin, v);
-            vmax = fmax(vmax, v);
+    const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const uint64_t nv = aligned ? n / V : 0;  // whole vectors
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+    const uint4 *xv = reinterpret_cast<const uint4 *>(x);
+    uint64_t b = tid;
+    for (; b + (U - 1) * nt < nv; b += U * nt) {
+        uint4 w[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) w[u] = __ldcs(xv + b + u * nt);
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const InT *e = reinterpret_cast<const InT *>(&w[u]);
+#pragma unroll
+            for (int k = 0; k < V; k++) fr_take<InT>(e[k], (b + u * nt) * V + k, vmin, vmax, bad);
         }
     }
+    for (; b < nv; b += nt) {
+        const uint4 w = __ldcs(xv + b);
+        const InT *e = reinterpret_cast<const InT *>(&w);
+#pragma unroll
+        for (int k = 0; k < V; k++) fr_take<InT>(e[k], b * V + k, vmin, vmax, bad);
+    }
+    for (uint64_t i = nv * V + tid; i < n; i += nt) fr_take<InT>(x[i], i, vmin, vmax, bad);
+    double dmin = (double)vmin, dmax = (double)vmax;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
-        vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+        dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
         unsigned long long ob = __shfl_xor_sync(0xffffffffu, bad, o);
         bad = ob < bad ? ob : bad;
     }
     if (lane_id() == 0) {
-        if (vmin <= vmax) {
-            atomicMin(&mm[0], dkey(vmin));
-            atomicMax(&mm[1], dkey(vmax));
+        if (dmin <= dmax) {
+            atomicMin(&mm[0], dkey(dmin));
+            atomicMax(&mm[1], dkey(dmax));
         }
         if (bad != ~0ull) atomicMin(&mm[2], bad);
     }
