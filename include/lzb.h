@@ -169,6 +169,14 @@ int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t count,
                     int sym_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
                     void *stream);
 
+/* Multi-GPU slab variant: the stream's first bit is bit
+ * `bit_phase` (0..7, MSB first) of bits[0] -- a rank's slice as produced by
+ * lzb_huff_encode_at.  Same outputs and errors as lzb_huff_decode. */
+int lzb_huff_decode_at(const uint8_t *bits, uint64_t bit_phase, uint64_t bit_len, uint64_t count,
+                       const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym,
+                       int sym_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
+                       void *stream);
+
 /* ---------------------------------------------------------------------
  * Number of maximal runs of a symbol stream (sizes K4's outputs before the
  * RLE / RLE_VLE workflows, P/rle.py:17-35).  st->u[0] = run count.

@@ -1275,12 +1275,11 @@ extern "C" size_t lzb_huff_decode_scratch_bytes(uint64_t bit_len, uint32_t maxle
     return s.bytes();
 }
 
-extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t count,
-                               const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym,
-                               int sym_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
-                               void *stream) {
+static int huff_decode_impl(const uint8_t *bits, uint32_t bit_phase, uint64_t bit_len, uint64_t count,
+                            const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym, int sym_bytes,
+                            lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream) {
     if (!lengths || !st || (sym_bytes != 2 && sym_bytes != 4) || cap == 0 || maxlen == 0 ||
-        maxlen > 64)
+        maxlen > 64 || bit_phase > 7)
         return LZB_E_ARG;
     cudaStream_t s = as_stream(stream);
     LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
@@ -1307,8 +1306,8 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
     DecParams p;
     uintptr_t a = reinterpret_cast<uintptr_t>(bits);
     p.words = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
-    p.head = (uint32_t)(a & 3) * 8;
-    p.nwords = (p.head / 8 + (bit_len + 7) / 8 + 3) / 4;
+    p.head = (uint32_t)(a & 3) * 8 + bit_phase;
+    p.nwords = ((p.head + bit_len + 7) / 8 + 3) / 4;
     p.bit_len = bit_len;
     p.count = count;
     p.tab = tab;
@@ -1367,4 +1366,21 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
     }
     LZB_LAUNCH_CHECK();
     return LZB_OK;
+}
+
+extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t count,
+                               const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym,
+                               int sym_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
+                               void *stream) {
+    return huff_decode_impl(bits, 0, bit_len, count, lengths, cap, maxlen, sym, sym_bytes, st, scratch,
+                            scratch_bytes, stream);
+}
+
+extern "C" int lzb_huff_decode_at(const uint8_t *bits, uint64_t bit_phase, uint64_t bit_len, uint64_t count,
+                                  const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym,
+                                  int sym_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
+                                  void *stream) {
+    if (bit_phase > 7) return LZB_E_ARG;
+    return huff_decode_impl(bits, (uint32_t)bit_phase, bit_len, count, lengths, cap, maxlen, sym, sym_bytes,
+                            st, scratch, scratch_bytes, stream);
 }

@@ -86,6 +86,9 @@ class SlabResult:
     records: object       # this slab's outlier records, global indices (16 B each)
     record_start: int     # record offset inside the outlier section
     meta: dict            # header fields shared by all ranks
+    phase: int = 0        # bit phase of the slab's first bit inside bits[0]
+    nbits: int = 0        # the slab's bits in the dense stream
+    n_out: int = 0        # the slab's outlier records
 
 
 class SlabOps:
@@ -113,6 +116,20 @@ class SlabOps:
 
     def to_tensor(self, x):
         """Object -> torch tensor on the collective's device (for all_reduce)."""
+        raise NotImplementedError
+
+    # -- decompress side (decompress_sharded) --
+    def decode_at(self, bits, phase: int, nbits: int, count: int, lengths, cap: int, maxlen: int):
+        """Symbols of a slab slice whose first bit is bit `phase` of bits[0]."""
+        raise NotImplementedError
+
+    def local_records(self, records, n_out: int, offset: int):
+        """Slab-local copy of global-index records (subtract `offset`)."""
+        raise NotImplementedError
+
+    def reconstruct(self, codes, sdims: Dims, chunk: ChunkSpec, eb_abs: float, cap: int, records,
+                    n_out: int, dtype_code: int):
+        """Slab values (fuse outliers, partial sums, dequantise)."""
         raise NotImplementedError
 
 
@@ -164,8 +181,34 @@ def compress_sharded(ops: SlabOps, values, dims: Dims, vmin: float, vmax: float,
         recs = ops.offset_records(recs, n_out, slab_index_offset(dims, lo))
     meta = dict(dims=dims, chunk=chunk, cap=cap, eb=eb, eb_mode=eb_mode, vmin=vmin, vmax=vmax,
                 dtype_code=dtype_code, total_bits=total_bits, total_out=total_out,
-                lengths=lengths)
-    return SlabResult(rank, B_k // 8, bits, recs, O_k, meta)
+                lengths=lengths, maxlen=maxlen)
+    return SlabResult(rank, B_k // 8, bits, recs, O_k, meta, phase=phase, nbits=my_bits, n_out=n_out)
+
+
+def decompress_sharded(ops: SlabOps, res: SlabResult, group=None):
+    """Rank-local inverse of compress_sharded: the rank decodes its own slice of
+    the dense stream (its first bit at res.phase, res.nbits long -- exactly the
+    bits lzb_huff_encode_at wrote) and reconstructs its slab from it and its
+    outlier records.  No collective: the slab boundaries are chunk-layer
+    boundaries, so a slab's symbols, chunks and records are all its own.
+    Returns the slab's values (None for an empty slab)."""
+    import torch.distributed as dist
+
+    from .pipeline import _resolve_eb
+
+    m = res.meta
+    dims, chunk, cap = m["dims"], m["chunk"], m["cap"]
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    lo, hi = slab_bounds(dims, chunk, rank, world)
+    if hi <= lo:
+        return None
+    sd = slab_dims(dims, lo, hi)
+    eb_abs = _resolve_eb(m["eb_mode"], m["eb"], m["vmin"], m["vmax"])
+    codes = ops.decode_at(res.bits, res.phase, res.nbits, sd.count, m["lengths"], cap, m["maxlen"])
+    recs = ops.local_records(res.records, res.n_out, slab_index_offset(dims, lo)) if res.n_out \
+        else None
+    return ops.reconstruct(codes, sd, chunk, eb_abs, cap, recs, res.n_out, m["dtype_code"])
 
 
 def assemble(results: list[SlabResult], lengths_bytes: bytes) -> bytes:
@@ -314,59 +357,53 @@ class DeviceSlabOps(SlabOps):
     def to_tensor(self, x):
         return x
 
+    def decode_at(self, bits, phase, nbits, count, lengths, cap, maxlen):
+        import torch
 
-def bench_sharded(args, cfg, rank, world, dev, gen_field_device, metric):
-    """bench.py --gpus N: strong scaling of the 2048^3 field over N slabs.
-    Timed region per step: sharded compress (every rank holds its slice) +
-    the slab's reconstruction from its own slice (decode + K6); max over ranks."""
-    import json
-    import statistics
+        from . import _native as N
+        from .pipeline import code_bytes_for
 
-    import torch
-    import torch.distributed as dist
+        L = N.lib()
+        cb = code_bytes_for(cap)
+        sym = torch.empty(count * cb, dtype=torch.uint8, device=self.device)
+        st = N.empty_bytes(N.STATUS_BYTES, self.device)
+        ds = L.lzb_huff_decode_scratch_bytes(nbits, maxlen, cap)
+        scr = N.empty_bytes(ds, self.device)
+        N.check_rc(L.lzb_huff_decode_at(bits.data_ptr(), phase, nbits, count, lengths.data_ptr(), cap,
+                                        maxlen, sym.data_ptr(), cb, st.data_ptr(), scr.data_ptr(), ds,
+                                        N.stream_ptr()), "huff_decode_at")
+        self._decode_status = st  # read with the reconstruct status (one sync)
+        return sym
 
-    from .grid import Dims
+    def local_records(self, records, n_out, offset):
+        import torch
 
-    shape = cfg["shape"]
-    dims = Dims.of(*shape[::-1])
-    chunk = ChunkSpec.default_for(dims.ndim)
-    lo, hi = slab_bounds(dims, chunk, rank, world)
-    x = gen_field_device(cfg, dev, lo, hi)
-    # global range: all-reduce min / max (SURVEY 8(e) collective 1)
-    mm = torch.stack([x.min().double(), -x.max().double()])
-    dist.all_reduce(mm, op=dist.ReduceOp.MIN)
-    vmin, vmax = float(mm[0]), float(-mm[1])
-    ops = DeviceSlabOps(dev)
+        r = records.view(torch.int64).view(-1, 2).clone()
+        r[:, 0] -= offset
+        return r.view(torch.uint8).view(-1)
 
-    def step():
-        return compress_sharded(ops, x, dims, vmin, vmax, cfg["eb"], "rel", 1024, chunk, 0)
+    def reconstruct(self, codes, sdims, chunk, eb_abs, cap, records, n_out, dtype_code):
+        import torch
 
-    for _ in range(args.warmup):
-        res = step()
-    torch.cuda.synchronize()
-    times = []
-    for _ in range(args.steps):
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        res = step()
-        e1.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / 1e3], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        times.append(float(t))
-    tc = statistics.mean(times)
-    n = dims.count
-    nbytes = n * 4
-    arc_bytes = _SECTION_BASE + 1024 + 16 + (res.meta["total_bits"] + 7) // 8 + 16 * res.meta["total_out"]
-    if rank == 0:
-        print(json.dumps({
-            "metric": metric, "value": round(nbytes / tc / 1e9, 3), "unit": "GB/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(tc * 1e3, 3), "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "elements": n, "parallelism": f"slab{world}",
-                       "phase": "compress (sharded; every rank holds its archive slice)"},
-            "compress_gbs": round(nbytes / tc / 1e9, 3), "compression_ratio": round(nbytes / arc_bytes, 4),
-        }), flush=True)
+        from . import _native as N
+        from .errors import CorruptArchiveError
+        from .pipeline import code_bytes_for
+
+        L = N.lib()
+        y = torch.empty(sdims.count, dtype=torch.float32 if dtype_code == 0 else torch.float64,
+                        device=self.device)
+        g = N.geom(sdims.as_tuple(), chunk.as_tuple())
+        rs = L.lzb_reconstruct_scratch_bytes(g, n_out)
+        scr = N.empty_bytes(rs, self.device)
+        st = N.empty_bytes(N.STATUS_BYTES, self.device)
+        N.check_rc(L.lzb_reconstruct(codes.data_ptr(), code_bytes_for(cap),
+                                     records.data_ptr() if records is not None else None, n_out, g,
+                                     eb_abs, cap, y.data_ptr(), dtype_code, None, st.data_ptr(),
+                                     scr.data_ptr(), rs, N.stream_ptr()), "reconstruct")
+        (sd,) = N.read_status(self._decode_status)
+        N.raise_for(sd, "decode", "bit stream does not decode to its declared symbols")
+        (sk,) = N.read_status(st)
+        if sk.code == N.LZB_E_CORRUPT:
+            raise CorruptArchiveError("invalid outlier list")
+        N.raise_for(sk, "reconstruct")
+        return y

@@ -57,6 +57,21 @@ class OracleSlabOps:
 
         return torch.from_numpy(np.asarray(x, np.int64))
 
+    def decode_at(self, bits, phase, nbits, count, lengths, cap, maxlen):
+        arr = np.unpackbits(np.asarray(bits, np.uint8))[phase: phase + nbits]
+        return O.huff_decode(nbits, count, np.packbits(arr).tobytes(), np.asarray(lengths, np.uint8))
+
+    def local_records(self, records, n_out, offset):
+        r = np.asarray(records, np.uint8).view([("i", "<u8"), ("d", "<i8")]).copy()
+        r["i"] -= offset
+        return r
+
+    def reconstruct(self, codes, sdims, chunk, eb_abs, cap, records, n_out, dtype_code):
+        oi = records["i"].astype(np.int64) if records is not None else np.empty(0, np.int64)
+        od = records["d"] if records is not None else np.empty(0, np.int64)
+        return O.reconstruct(codes, sdims.as_tuple(), chunk.as_tuple(), cap // 2, oi, od, eb_abs,
+                             "f32" if dtype_code == 0 else "f64")
+
 
 def _worker(rank, world, port, case, q):
     import torch.distributed as dist
@@ -76,6 +91,13 @@ def _worker(rank, world, port, case, q):
         slab = full[lo:hi].reshape(-1) if dims.ndim > 1 else full[lo:hi]
         res = D.compress_sharded(OracleSlabOps(), slab, dims, float(vals.min()),
                                  float(vals.max()), eb, "rel", 1024, chunk, 0)
+        # slab-local decompress of the rank's own slice == that slab of the
+        # single-device decompress
+        y = D.decompress_sharded(OracleSlabOps(), res)
+        ref = O.decompress(O.compress(vals, dims.as_tuple(), float(vals.min()), float(vals.max()),
+                                      eb))[0].reshape(shape)
+        want = ref[lo:hi].reshape(-1) if dims.ndim > 1 else ref[lo:hi]
+        assert y is not None and np.array_equal(y, want), rank
         res.meta.pop("lengths")
         got = D.gather_results(res)
         if rank == 0:

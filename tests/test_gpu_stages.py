@@ -235,3 +235,35 @@ def test_huffman_decode_layouts(cuda):
     stream = (rng.geometric(0.3, 100_000) + 70000).astype(np.uint32) % cap
     bk = lzb.Codebook.from_counts(np.bincount(stream, minlength=cap))
     assert np.array_equal(lzb.decode(lzb.encode(stream, bk), bk), stream)
+
+
+def test_decode_at_bit_phase(cuda):
+    """lzb_huff_decode_at (the multi-GPU slab decode) on streams whose first
+    bit is bit 0..7 of the first byte -- the slices lzb_huff_encode_at writes."""
+    import torch
+
+    import paper_2105_12912_b200 as lzb
+    from paper_2105_12912_b200 import _native as N
+
+    L = N.lib()
+    rng = np.random.default_rng(77)
+    g = np.array([int(1e6 * 0.5 ** abs(i - 32)) + 1 for i in range(64)], np.int64)
+    for n in (1, 5000, 70_000):
+        stream = rng.choice(64, size=n, p=g / g.sum()).astype(np.uint32)
+        bk = lzb.Codebook.from_counts(np.bincount(stream, minlength=64))
+        bs = lzb.encode(stream, bk)
+        bits = np.unpackbits(np.asarray(bs.data, np.uint8))[: bs.bit_len]
+        for phase in range(8):
+            sl = np.packbits(np.concatenate([rng.integers(0, 2, phase).astype(np.uint8), bits]))
+            d = torch.from_numpy(np.concatenate([sl, np.zeros(8, np.uint8)])).cuda()
+            lens = torch.from_numpy(bk.lengths.astype(np.uint8)).cuda()
+            out = torch.empty(n, dtype=torch.int16, device="cuda")
+            st = N.empty_bytes(N.STATUS_BYTES)
+            ds = L.lzb_huff_decode_scratch_bytes(bs.bit_len, int(bk.lengths.max()), 64)
+            scr = N.empty_bytes(ds)
+            N.check_rc(L.lzb_huff_decode_at(d.data_ptr(), phase, bs.bit_len, n, lens.data_ptr(), 64,
+                                            int(bk.lengths.max()), out.data_ptr(), 2, st.data_ptr(),
+                                            scr.data_ptr(), ds, N.stream_ptr()), "decode_at")
+            (s,) = N.read_status(st)
+            assert s.code == 0, (n, phase)
+            assert np.array_equal(out.cpu().numpy().view(np.uint16).astype(np.uint32), stream), (n, phase)
