@@ -1,10 +1,10 @@
 """Summarise a round's ncu captures into profiles/ (run here, after gpurun).
 
-usage: python tools/ncu_summary.py TAG
+usage: python tools/ncu_summary.py TAG [c5q|c5s]
   reads gpurun_out/launches_TAG_c5.csv (launch list of the C5 bench command)
-        gpurun_out/prof_TAG_full_raw.csv (--set full capture on C5s)
-  writes profiles/TAG_launches_c5.csv, profiles/TAG_ncu_full_c5s.md,
-         profiles/ncu_traffic.json (dram bytes per launch, scaled C5s -> C5)
+        gpurun_out/prof_TAG_full_raw.csv (--set full capture on C5q / C5s)
+  writes profiles/TAG_launches_c5.csv, profiles/TAG_ncu_full_<cfg>.md,
+         profiles/ncu_traffic.json (dram bytes per launch, scaled <cfg> -> C5)
 """
 import csv
 import json
@@ -12,7 +12,9 @@ import sys
 from collections import defaultdict
 
 tag = sys.argv[1]
-SCALE = (2048 ** 3) / (512 ** 3)  # C5 elements / C5s elements
+CFG = sys.argv[2] if len(sys.argv) > 2 else "c5q"
+SCALE = {"c5q": 4.0, "c5s": 64.0}[CFG]  # C5 elements / profiled config's elements
+CFG_DESC = {"c5q": "C5q (512x2048x2048 f32, rel eb 1e-4)", "c5s": "C5s (512^3 f32, rel eb 1e-4)"}[CFG]
 STAGES = {
     "K1_quantize": ["k_quantize3d8", "k_q3_"],
     "K3_huff_encode": ["k_huff_count_w", "k_huff_scan_w", "k_huff_encode_w", "k_huff_fixup_w"],
@@ -48,7 +50,7 @@ def g(r, n):
         return float(r[col[n]].replace(",", ""))
     except (KeyError, ValueError):
         return float("nan")
-out = ["# ncu --set full on C5s (512^3 f32, rel eb 1e-4), one launch per kernel", "",
+out = [f"# ncu --set full on {CFG_DESC}, one launch per kernel", "",
        "| kernel | time us | DRAM read MB | DRAM write MB | DRAM GB/s | warps active % | issue active % | regs | top stalls (per issue) |",
        "|---|---|---|---|---|---|---|---|---|"]
 traffic = {}
@@ -73,9 +75,9 @@ for r in rows[2:]:
         if any(p in name for p in pats):
             traffic[stage] = traffic.get(stage, 0.0) + (rd + wr) * 1e6 * SCALE
 out += ["", "DRAM GB/s = (read + write) / duration.  `profiles/ncu_traffic.json` holds the",
-        "per-stage DRAM bytes of these kernels scaled by 64 (C5 / C5s elements)."]
-open(f"profiles/{tag}_ncu_full_c5s.md", "w").write("\n".join(out) + "\n")
-json.dump({k: int(v) for k, v in traffic.items()} | {"_source": f"profiles/{tag}_ncu_full_c5s.md",
-          "_note": "dram__bytes_read.sum + dram__bytes_write.sum of the stage's profiled kernels on C5s x 64"},
+        f"per-stage DRAM bytes of these kernels scaled by {SCALE:g} (C5 / {CFG} elements)."]
+open(f"profiles/{tag}_ncu_full_{CFG}.md", "w").write("\n".join(out) + "\n")
+json.dump({k: int(v) for k, v in traffic.items()} | {"_source": f"profiles/{tag}_ncu_full_{CFG}.md",
+          "_note": f"dram__bytes_read.sum + dram__bytes_write.sum of the stage's profiled kernels on {CFG} x {SCALE:g}"},
           open("profiles/ncu_traffic.json", "w"), indent=1)
 print("\n".join(out))
