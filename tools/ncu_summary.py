@@ -44,12 +44,17 @@ with open(f"profiles/{tag}_launches_c5.csv", "w", newline="") as fh:
 # ---- full capture ----
 rows = list(csv.reader(open(f"gpurun_out/prof_{tag}_full_raw.csv")))
 h = rows[0]
+units = rows[1]
 col = {n: i for i, n in enumerate(h)}
+_SCALE = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6,
+          "second": 1e6, "byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6}
 def g(r, n):
+    """value in us (times) / MB (bytes) / as-is (others), from the units row"""
     try:
-        return float(r[col[n]].replace(",", ""))
+        v = float(r[col[n]].replace(",", ""))
     except (KeyError, ValueError):
         return float("nan")
+    return v * _SCALE.get(units[col[n]], 1.0)
 out = [f"# ncu --set full on {CFG_DESC}, one launch per kernel", "",
        "| kernel | time us | DRAM read MB | DRAM write MB | DRAM GB/s | warps active % | issue active % | regs | top stalls (per issue) |",
        "|---|---|---|---|---|---|---|---|---|"]
