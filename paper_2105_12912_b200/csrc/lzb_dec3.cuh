@@ -58,13 +58,21 @@ __device__ __forceinline__ uint32_t bm2_rank(uint64_t b0, uint64_t b1, uint32_t 
 __device__ __forceinline__ void d3_stage(const DecParams &p, uint64_t t, uint32_t s_addr, uint32_t lane) {
     if (t < p.T) {
         const uint64_t w0 = t * 128;
-        for (uint32_t j = lane; j < kStgWords; j += 32) {
-            const uint64_t w = w0 + j;
-            const bool in = w < p.nwords;
-            const uint32_t *src = p.words + (in ? w : 0);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s_addr + 4 * j), "l"(src),
-                         "r"(in ? 4 : 0)
-                         : "memory");
+        if ((reinterpret_cast<uintptr_t>(p.words) & 15) == 0 && w0 + kStgWords <= p.nwords) {
+            // 34 aligned 16-byte pieces
+            for (uint32_t j = lane; j < kStgWords / 4; j += 32)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s_addr + 16 * j),
+                             "l"(p.words + w0 + 4 * j)
+                             : "memory");
+        } else {
+            for (uint32_t j = lane; j < kStgWords; j += 32) {
+                const uint64_t w = w0 + j;
+                const bool in = w < p.nwords;
+                const uint32_t *src = p.words + (in ? w : 0);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s_addr + 4 * j), "l"(src),
+                             "r"(in ? 4 : 0)
+                             : "memory");
+            }
         }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -559,21 +567,18 @@ __global__ void __launch_bounds__(kF7Warps * 32, 1) k_dec_final7(DecParams p) {
         __syncwarp();
         // coalesced copy-out: unit q <-> output elements g0 + 8q .. g0 + 8q + 7
         const uint64_t g0 = base - sh;
-        const uint32_t nunits = (sh + total + 7) >> 3;
         const uint4 *wv = reinterpret_cast<const uint4 *>(wout);
-        for (uint32_t q = lane; q < nunits; q += 32) {
-            const uint4 v = wv[q];
-            const uint32_t lo = 8 * q;
-            if (lo >= sh && lo + 8 <= sh + total) {
-                *reinterpret_cast<uint4 *>(out + g0 + lo) = v;
-            } else {
-                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                for (uint32_t c = 0; c < 8; c++) {
-                    const uint32_t j = lo + c;
-                    if (j >= sh && j < sh + total) out[g0 + j] = (uint16_t)(w[c >> 1] >> (16 * (c & 1)));
-                }
-            }
+        // whole 16-byte units: unit 0 is partial when sh > 0, the last when
+        // the range does not end on a unit boundary
+        const uint32_t q0 = sh ? 1u : 0u, q1 = (sh + total) >> 3;
+        for (uint32_t q = q0 + lane; q < q1; q += 32)
+            *reinterpret_cast<uint4 *>(out + g0 + 8 * q) = wv[q];
+        // the partial head / tail units, one element per lane
+        {
+            const uint32_t c = lane & 7;
+            const uint32_t j = (lane < 8 ? 0u : 8u * q1) + c;
+            const bool part = lane < 8 ? (sh != 0) : (lane < 16 && ((sh + total) & 7) != 0);
+            if (part && j >= sh && j < sh + total) out[g0 + j] = wout[j];
         }
         __syncwarp();
     }
