@@ -195,6 +195,33 @@ def main():
         lens.append(lzebc.Codebook.from_counts(h).lengths.tolist())
     kats["random_histograms"] = hists
     kats["random_lengths"] = lens
+    # analyze() CSV reports (P/smoothness.py:166-188): seeded madograms of the
+    # prequant and quant-code grids + entropy stats + decision
+    an = []
+    for shape, eb, dmax, seed, cap in (((48, 64), 1e-2, 30, 0, 1024), ((12, 10, 9), 1e-3, 50, 7, 256),
+                                       ((3000,), 1e-4, 200, 3, 1024)):
+        vals = smooth(shape).reshape(-1).astype(np.float32)
+        fld = lzebc.Field.from_array(vals.reshape(shape))
+        rec = lzebc.analyze(fld, lzebc.QuantConfig(eb * fld.value_range, cap), dmax=dmax, seed=seed)
+        an.append([list(shape), eb, dmax, seed, cap, rec.to_csv()])
+    kats["analyze_csv"] = an
+    # the CLI's compress report line on the reference tests' sine field (T/test_cli.py:7-13)
+    from lzebc.cli import run
+    import contextlib
+    import io
+    import tempfile
+    x = np.linspace(0, 20, 64 * 48)
+    data = (np.sin(x) * 100 + x).astype(np.float32)
+    with tempfile.TemporaryDirectory() as td:
+        src = os.path.join(td, "field.f32")
+        with open(src, "wb") as fh:
+            fh.write(data.tobytes())
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            code = run(["compress", "-d", "64,48", "-t", "f32", "-e", "rel:1e-4", src,
+                        os.path.join(td, "a.lz")])
+        assert code == 0
+        kats["cli_compress_line"] = buf.getvalue().strip()
     with open(os.path.join(OUT, "kats.json"), "w") as fh:
         json.dump(kats, fh)
     total = sum(os.path.getsize(os.path.join(OUT, p)) for p in os.listdir(OUT))

@@ -77,8 +77,8 @@ class OutlierList:
         return cls(np.empty(0, np.int64), np.empty(0, np.int64))
 
 
-def prequantize(field: Field, cfg: QuantConfig) -> PrequantGrid:
-    """round-half-away(f64(x) / (2 eb_abs)) on the GPU (P/quantize.py:95-110)."""
+def prequantize_device(field: Field, cfg: QuantConfig):
+    """round-half-away(f64(x) / (2 eb_abs)) on the GPU -> int64 CUDA tensor."""
     import torch
 
     from .pipeline import _as_device_values
@@ -92,7 +92,38 @@ def prequantize(field: Field, cfg: QuantConfig) -> PrequantGrid:
                "prequantize")
     (s,) = N.read_status(st)
     N.raise_for(s, "prequantize")
-    return PrequantGrid(field.dims, out.cpu().numpy())
+    return out
+
+
+def prequantize(field: Field, cfg: QuantConfig) -> PrequantGrid:
+    """round-half-away(f64(x) / (2 eb_abs)) on the GPU (P/quantize.py:95-110)."""
+    return PrequantGrid(field.dims, prequantize_device(field, cfg).cpu().numpy())
+
+
+def quant_grid_device(pre, dims: Dims, cfg: QuantConfig, spec: ChunkSpec):
+    """K1 over a device prequant grid -> (grid-order codes as an int32 CUDA tensor,
+    cap-bin histogram as numpy int64).  Used by analyze (pairs gathered on device)."""
+    import torch
+
+    L = N.lib()
+    n = dims.count
+    codes = torch.empty(n, dtype=torch.int32, device=pre.device)
+    hist = torch.empty(cfg.cap, dtype=torch.int64, device=pre.device)
+    g = N.geom(dims.as_tuple(), spec.as_tuple())
+    cap_out = n
+    outl = torch.empty(2 * max(cap_out, 1), dtype=torch.int64, device=pre.device)
+    qs = L.lzb_quantize_scratch_bytes(g, cap_out)
+    scr = N.empty_bytes(qs, pre.device)
+    st = N.empty_bytes(N.STATUS_BYTES, pre.device)
+    N.check_rc(L.lzb_quantize(pre.data_ptr(), 2, g, 0.5, cfg.cap, codes.data_ptr(), 4,
+                              hist.data_ptr(), outl.data_ptr(), cap_out, st.data_ptr(),
+                              scr.data_ptr(), qs, N.stream_ptr()), "quantize")
+    (s,) = N.read_status(st)
+    N.raise_for(s, "quantize")
+    grid = torch.empty_like(codes)
+    N.check_rc(L.lzb_chunk_major(codes.data_ptr(), grid.data_ptr(), 4, g, 1, N.stream_ptr()),
+               "chunk_major")
+    return grid, hist.cpu().numpy()
 
 
 def chunk_major(codes, dims: Dims, spec: ChunkSpec, direction: int) -> np.ndarray:
