@@ -198,41 +198,83 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
     if (n == 1) {
         if (threadIdx.x == 0) lengths[sc.key[0] & 0xFFFFF] = 1;  // lone symbol -> 1 bit
     } else {
-        // two-queue Huffman merge (sequential; n-1 steps)
+        // two-queue Huffman merge (sequential; n-1 steps); the heads of both
+        // queues are kept in registers
         if (threadIdx.x == 0) {
             uint32_t li = 0, ii = 0, ni = 0;
+            uint64_t lw = sc.key[0] >> 20;  // head leaf weight (li < n)
+            uint64_t iw = 0;                // head internal weight (ii < ni)
             for (uint32_t k = 0; k < n - 1; k++) {
                 uint64_t w[2];
                 uint32_t id[2];
+#pragma unroll
                 for (int t = 0; t < 2; t++) {
-                    bool take_leaf;
-                    if (li >= n) take_leaf = false;
-                    else if (ii >= ni) take_leaf = true;
-                    else take_leaf = (sc.key[li] >> 20) <= sc.wint[ii];  // leaf first on ties
+                    const bool take_leaf = li < n && (ii >= ni || lw <= iw);  // leaf first on ties
                     if (take_leaf) {
-                        w[t] = sc.key[li] >> 20;
+                        w[t] = lw;
                         id[t] = li++;
+                        lw = li < n ? (sc.key[li] >> 20) : 0;
                     } else {
-                        w[t] = sc.wint[ii];
+                        w[t] = iw;
                         id[t] = n + ii++;
+                        iw = ii < ni ? sc.wint[ii] : 0;
                     }
                 }
-                sc.wint[ni] = w[0] + w[1];
+                const uint64_t nw = w[0] + w[1];
+                sc.wint[ni] = nw;
+                if (ii == ni) iw = nw;  // the queue was empty: the new node is its head
                 sc.parent[id[0]] = n + ni;
                 sc.parent[id[1]] = n + ni;
                 ni++;
             }
-            // depths top-down: root is the last internal node
-            const uint32_t root = n + ni - 1;
-            sc.depth[root] = 0;
-            for (int32_t k = (int32_t)ni - 2; k >= 0; k--) {
-                uint32_t d = sc.depth[sc.parent[n + k]] + 1u;
-                sc.depth[n + k] = (uint8_t)(d > 255 ? 255 : d);
-            }
         }
         __syncthreads();
+        // depths (number of ancestors) of the 2n-1 nodes, root = node 2n-2
+        const uint32_t nn = 2 * n - 1, root = nn - 1;
+        if (nn <= 4 * blockDim.x) {  // pointer jumping: ceil(log2(nn)) rounds
+            uint32_t *anc = sc.parent;  // reused as the jump pointers
+            for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) sc.depth[i] = i == root ? 0 : 1;
+            if (threadIdx.x == 0) anc[root] = root;
+            __syncthreads();
+            for (uint32_t span = 1; span < nn; span <<= 1) {
+                uint32_t a_new[4], d_new[4];
+#pragma unroll
+                for (uint32_t c = 0; c < 4; c++) {
+                    const uint32_t i = threadIdx.x + c * blockDim.x;
+                    if (i < nn) {
+                        const uint32_t a = anc[i];
+                        d_new[c] = sc.depth[i] + sc.depth[a];
+                        a_new[c] = anc[a];
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (uint32_t c = 0; c < 4; c++) {
+                    const uint32_t i = threadIdx.x + c * blockDim.x;
+                    if (i < nn) {
+                        sc.depth[i] = (uint8_t)(d_new[c] > 255 ? 255 : d_new[c]);
+                        anc[i] = a_new[c];
+                    }
+                }
+                __syncthreads();
+            }
+        } else {  // large books: top-down walk over the internal nodes
+            if (threadIdx.x == 0) {
+                sc.depth[root] = 0;
+                for (int32_t k = (int32_t)root - 1; k >= (int32_t)n; k--) {
+                    const uint32_t d = sc.depth[sc.parent[k]] + 1u;
+                    sc.depth[k] = (uint8_t)(d > 255 ? 255 : d);
+                }
+            }
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+                const uint32_t d = sc.depth[sc.parent[i]] + 1u;
+                sc.depth[i] = (uint8_t)(d > 255 ? 255 : d);
+            }
+            __syncthreads();
+        }
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-            uint32_t d = sc.depth[sc.parent[i]] + 1u;
+            uint32_t d = sc.depth[i];
             if (d > 64) {
                 s_err = 1;
                 d = 64;

@@ -581,6 +581,7 @@ __global__ void k_huff_fixup_w(const __grid_constant__ EncWParams p) {
     const uint64_t total = p.bit_offset + p.toff[p.ntiles];
     const uint64_t nbytes = (total + 7) / 8;
     if (blockIdx.x == 0 && threadIdx.x == 0) p.st->u[0] = p.toff[p.ntiles];
+    const bool aligned = (reinterpret_cast<uintptr_t>(p.out) & 3) == 0;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < p.ntiles;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t G = p.bit_offset + p.toff[t];
@@ -596,7 +597,8 @@ __global__ void k_huff_fixup_w(const __grid_constant__ EncWParams p) {
                 const bool prev_single = (Gp & 31) != 0 && (Gp >> 5) == hw;
                 v |= prev_single ? p.frag[2 * (t - 1)] : p.frag[2 * (t - 1) + 1];
             }
-            store_word_bytes(p.out, hw * 4, v, nbytes);
+            if (aligned && hw * 4 + 4 <= nbytes) reinterpret_cast<uint32_t *>(p.out)[hw] = bswap32(v);
+            else store_word_bytes(p.out, hw * 4, v, nbytes);
         }
         if (tail && t + 1 == p.ntiles) store_word_bytes(p.out, tw * 4, p.frag[2 * t + 1], nbytes);
     }
