@@ -501,6 +501,7 @@ __global__ void __launch_bounds__(kWWarps * 32, 2) k_huff_encode_w(const __grid_
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
         asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();  // lanes read pieces other lanes copied
         const bool full = is_full(t);
         const uint64_t b0 = t * kWTile + (uint64_t)lane * kWSyms;
         // ---- the lane's 32 symbols ----

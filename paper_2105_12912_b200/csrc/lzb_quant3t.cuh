@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(kT1Threads, 2)
         }
         last = __shfl_sync(f3::kFull, last, 0);
         if (last) {
+            __syncwarp();  // order the lanes' reads after lane 0's acquire
             const uint32_t cl = lane < kT1Warps ? s_cnt[st][lane] : 0u;
             uint32_t inc = cl;
 #pragma unroll
@@ -322,6 +323,7 @@ __global__ void __launch_bounds__(kT1Threads, 2)
                     tslot[2 * k + 1] = s_rec[st][lane][k][1];
                 }
             }
+            __syncwarp();  // every lane's reads of the stage bookkeeping are done
             if (lane == 0) {
                 p.tile_cnt[t] = tot;
                 if (over) p.over_list[atomicAdd(p.n_over, 1u)] = (uint32_t)t;
