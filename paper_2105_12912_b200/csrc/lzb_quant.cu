@@ -700,11 +700,12 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
         size_t smem = (size_t)kQ3Warps * 2 * 32 * 16 * (dtype == 0 ? 4 : 8) +
                       (size_t)kQ3Warps * 512 * code_bytes + (size_t)kQ3Warps * 16 * 32 * 4 +
                       (size_t)cap * 4;
-        const bool tma = dtype == 0 && code_bytes == 2 && q3.vec_ok && (g.nbx % 8 == 0) && tma_encode();
+        const bool tma = dtype == 0 && code_bytes == 2 && q3.vec_ok && (g.nbx % kT1Warps == 0) && tma_encode();
         if (tma) {
             T1Params tp;
             tp.q = q3;
-            tp.tpr = (uint32_t)(g.nbx / 8);
+            tp.tpr = (uint32_t)(g.nbx / kT1Warps);
+            tp.nst = q3.nchunks / kT1Warps;
             CUtensorMap map;
             cuuint64_t dims[3] = {g.nx, g.ny, g.nz};
             cuuint64_t strides[2] = {g.nx * 4, g.nx * g.ny * 4};
@@ -720,7 +721,7 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
             int per_sm = 0;
             LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantize3d8_tma, kT1Threads, tsm));
             if (per_sm < 1) per_sm = 1;
-            const uint64_t grid = umin64((uint64_t)device_sms() * per_sm, q3.ntiles);
+            const uint64_t grid = umin64((uint64_t)device_sms() * per_sm, tp.nst);
             tp.step_q = (uint32_t)((grid ? grid : 1) / tp.tpr);
             tp.step_rem = (uint32_t)((grid ? grid : 1) % tp.tpr);
             k_quantize3d8_tma<<<(unsigned)(grid ? grid : 1), kT1Threads, tsm, s>>>(tp, map);

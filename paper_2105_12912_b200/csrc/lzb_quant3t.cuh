@@ -3,7 +3,8 @@
 // reference (P/quantize.py:90-213, P/pipeline.py:102-105, P/codebook.py:23-27)
 // and to k_quantize3d8; see lzb_fast3d.cuh for the per-chunk register layout.
 //
-// A tile is 8 consecutive chunks along x = a 64x8x8 f32 box (16 KB).  Each
+// A super tile is 16 consecutive chunks along x = a 128x8x8 f32 box (32 KB,
+// 512-byte row segments; two outlier tiles of 8 chunks).  Each
 // persistent CTA owns tiles b, b + G, b + 2G, ... and streams them through a
 // ring of kT1Stages shared-memory stages with TMA (two 32x8x8 boxes per
 // tile, SWIZZLE_128B so the warps' row reads are bank-conflict free),
@@ -20,16 +21,17 @@
 
 namespace lzb {
 
-constexpr int kT1Warps = 8;        // one chunk of the tile per warp
+constexpr int kT1Warps = 16;       // one chunk of the super tile per warp
 constexpr int kT1Threads = kT1Warps * 32;
 constexpr int kT1Stages = 4;       // tiles in flight per CTA
 constexpr uint32_t kT1Box = 8192;  // bytes per 32x8x8 f32 box
-constexpr uint32_t kT1Tile = 2 * kT1Box;
+constexpr uint32_t kT1Tile = 4 * kT1Box;  // 16 chunks = 128x8x8 f32 (512-byte rows)
 
 struct T1Params {
     Q3Params q;
-    uint32_t tpr;               // tiles per chunk row (nbx / 8)
+    uint32_t tpr;               // super tiles (16 chunks) per chunk row (nbx / 16)
     uint32_t step_q, step_rem;  // divmod(gridDim.x, tpr)
+    uint64_t nst;               // super tiles (= 2 outlier tiles of kQ3TileChunks each)
 };
 
 __device__ __forceinline__ void t1_mbar_init(uint32_t a, uint32_t count) {
@@ -85,8 +87,9 @@ __device__ __forceinline__ void t1_step(const T1Params &P, T1Pos &o) {
 }
 __device__ __forceinline__ void t1_issue(const CUtensorMap *map, const T1Pos &o, uint32_t dst, uint32_t mbar) {
     t1_mbar_expect(mbar, kT1Tile);
-    t1_tma3(dst, map, (int)(o.tx * 64), (int)(o.by * 8), (int)(o.bz * 8), mbar);
-    t1_tma3(dst + kT1Box, map, (int)(o.tx * 64 + 32), (int)(o.by * 8), (int)(o.bz * 8), mbar);
+#pragma unroll
+    for (int b = 0; b < 4; b++)
+        t1_tma3(dst + b * kT1Box, map, (int)(o.tx * 128 + 32 * b), (int)(o.by * 8), (int)(o.bz * 8), mbar);
 }
 
 // select element j (0..7) of a register row without dynamic indexing
@@ -104,7 +107,7 @@ __device__ __forceinline__ void t1_put(T (&v)[8], uint32_t j, T x) {
         if (j == (uint32_t)k) v[k] = x;
 }
 
-__global__ void __launch_bounds__(kT1Threads, 2)
+__global__ void __launch_bounds__(kT1Threads, 1)
     k_quantize3d8_tma(const __grid_constant__ T1Params P, const __grid_constant__ CUtensorMap map) {
     const Q3Params &p = P.q;
     extern __shared__ __align__(1024) unsigned char t1_smem[];
@@ -132,7 +135,7 @@ __global__ void __launch_bounds__(kT1Threads, 2)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         T1Pos q = pos;
         for (int s = 0; s < kT1Stages; s++) {
-            if (blockIdx.x + s * G < p.ntiles) t1_issue(&map, q, tiles_s + s * kT1Tile, full_s + 8 * s);
+            if (blockIdx.x + s * G < P.nst) t1_issue(&map, q, tiles_s + s * kT1Tile, full_s + 8 * s);
             t1_step(P, q);
         }
     }
@@ -155,10 +158,10 @@ __global__ void __launch_bounds__(kT1Threads, 2)
     const uint32_t off11 = (warp >> 2) * kT1Box + R1 * 128 + (((j2 + 1) ^ sw) << 4);
     int flags = 0;
     uint32_t it = 0;
-    for (uint64_t t = blockIdx.x; t < p.ntiles; t += G, it++, t1_step(P, pos)) {
+    for (uint64_t t = blockIdx.x; t < P.nst; t += G, it++, t1_step(P, pos)) {
         const uint32_t st = it % kT1Stages;
-        const uint32_t bx = pos.tx * 8 + warp;
-        const bool fast = ((uint64_t)pos.tx * 64 + 64 <= p.g.nx) && ((uint64_t)pos.by * 8 + 8 <= p.g.ny) &&
+        const uint32_t bx = pos.tx * 16 + warp;
+        const bool fast = ((uint64_t)pos.tx * 128 + 128 <= p.g.nx) && ((uint64_t)pos.by * 8 + 8 <= p.g.ny) &&
                           ((uint64_t)pos.bz * 8 + 8 <= p.g.nz);
         const uint64_t gi0 = (uint64_t)bx * 8 + p.g.nx * ((uint64_t)pos.by * 8) + plane * ((uint64_t)pos.bz * 8) +
                              lane_off;
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(kT1Threads, 2)
         if (slow) {
             // generic path (global reads, exact where needed); the tile's
             // records are re-derived in order by k_q3_emit (over_list)
-            const uint64_t c = t * kQ3TileChunks + warp;
+            const uint64_t c = t * kT1Warps + warp;
             nout = 0;
             if (c < p.nchunks) {
                 const Q3Res rr = q3_chunk_slow<float, uint16_t>(&p, c, lane, s_codes, nullptr, (uint32_t)kQ3Stash,
@@ -307,17 +310,21 @@ __global__ void __launch_bounds__(kT1Threads, 2)
         last = __shfl_sync(f3::kFull, last, 0);
         if (last) {
             __syncwarp();  // order the lanes' reads after lane 0's acquire
+            // two outlier tiles of 8 chunks: lanes 0-7 and 8-15
             const uint32_t cl = lane < kT1Warps ? s_cnt[st][lane] : 0u;
             uint32_t inc = cl;
 #pragma unroll
-            for (int o = 1; o < kT1Warps; o <<= 1) {
+            for (int o = 1; o < 8; o <<= 1) {
                 const uint32_t v = __shfl_up_sync(f3::kFull, inc, o);
-                if (lane >= (uint32_t)o) inc += v;
+                if ((lane & 7) >= (uint32_t)o) inc += v;
             }
-            const uint32_t tot = __shfl_sync(f3::kFull, inc, kT1Warps - 1);
-            const bool over = s_slow[st] || __any_sync(f3::kFull, cl > (uint32_t)kT1Sub);
-            if (!over && lane < kT1Warps) {
-                uint64_t *tslot = p.slots + t * 2 * kQ3Slot + 2 * (inc - cl);
+            const uint32_t tot0 = __shfl_sync(f3::kFull, inc, 7), tot1 = __shfl_sync(f3::kFull, inc, 15);
+            const bool slow_st = s_slow[st] != 0;
+            const uint32_t big = __ballot_sync(f3::kFull, lane < kT1Warps && cl > (uint32_t)kT1Sub);
+            const bool over0 = slow_st || (big & 0xFFu), over1 = slow_st || (big & 0xFF00u);
+            const uint64_t tile = 2 * t + (lane >> 3);
+            if (lane < kT1Warps && !((lane >> 3) ? over1 : over0)) {
+                uint64_t *tslot = p.slots + tile * 2 * kQ3Slot + 2 * (inc - cl);
                 for (uint32_t k = 0; k < cl; k++) {
                     tslot[2 * k] = s_rec[st][lane][k][0];
                     tslot[2 * k + 1] = s_rec[st][lane][k][1];
@@ -325,12 +332,14 @@ __global__ void __launch_bounds__(kT1Threads, 2)
             }
             __syncwarp();  // every lane's reads of the stage bookkeeping are done
             if (lane == 0) {
-                p.tile_cnt[t] = tot;
-                if (over) p.over_list[atomicAdd(p.n_over, 1u)] = (uint32_t)t;
+                p.tile_cnt[2 * t] = tot0;
+                p.tile_cnt[2 * t + 1] = tot1;
+                if (over0) p.over_list[atomicAdd(p.n_over, 1u)] = (uint32_t)(2 * t);
+                if (over1) p.over_list[atomicAdd(p.n_over, 1u)] = (uint32_t)(2 * t + 1);
                 s_rel[st] = 0;
                 s_slow[st] = 0;
                 const uint64_t tn = t + kT1Stages * G;
-                if (tn < p.ntiles) {
+                if (tn < P.nst) {
                     T1Pos q = pos;
 #pragma unroll 1
                     for (int s = 0; s < kT1Stages; s++) t1_step(P, q);

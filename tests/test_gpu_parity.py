@@ -226,8 +226,8 @@ def test_corruption_raises(cuda):
 
 
 def test_tma_tile_path_3d(cuda):
-    """ChunkSpec(8,8,8) f32 grids whose chunk rows hold whole 8-chunk tiles
-    (nx a multiple of 64) take K1's TMA path: smooth, noisy (non-origin and
+    """ChunkSpec(8,8,8) f32 grids whose chunk rows hold whole 16-chunk super
+    tiles (nx a multiple of 128) take K1's TMA path (others the cp.async one): smooth, noisy (non-origin and
     > 4-per-chunk outliers), partial y/z chunk layers, values on exact rounding
     ties and values too large for the int32 fast path -- all byte-identical to
     the oracle."""
@@ -236,12 +236,13 @@ def test_tma_tile_path_3d(cuda):
     cases = []
     cases.append((smooth((24, 32, 128)), dict(eb=1e-4)))
     cases.append((smooth((21, 19, 64)), dict(eb=1e-3)))                        # partial y/z chunks
-    noisy = (rng.standard_normal((16, 16, 192)) * 50).astype(np.float32)
+    cases.append((smooth((21, 19, 256)), dict(eb=1e-3)))
+    noisy = (rng.standard_normal((16, 16, 256)) * 50).astype(np.float32)
     cases.append((noisy, dict(eb=1e-4, cap=64)))                               # many outliers
     cases.append((noisy, dict(eb=1e-2, cap=4)))
-    ties = (np.round(rng.uniform(-300, 300, (8, 8, 64))) + 0.5).astype(np.float32) * np.float32(0.5)
+    ties = (np.round(rng.uniform(-300, 300, (8, 8, 128))) + 0.5).astype(np.float32) * np.float32(0.5)
     cases.append((ties, dict(eb=0.25, eb_mode="abs")))                         # x / (2 eb) on a .5 tie
-    big = smooth((16, 8, 64)) * np.float32(1e4)
+    big = smooth((16, 8, 128)) * np.float32(1e4)
     cases.append((big, dict(eb=1e-9, eb_mode="abs", cap=1024)))                # |q| >= 2^22: exact path
     for vals, kw in cases:
         f = lzb.Field.from_array(vals)
