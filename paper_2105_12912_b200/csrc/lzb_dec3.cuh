@@ -584,3 +584,266 @@ __global__ void __launch_bounds__(kF7Warps * 32, 1) k_dec_final7(DecParams p) {
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
+
+// count-only decode with the byte LUT (irregular entries in final9)
+__device__ __forceinline__ bool d3_count8(const uint32_t *stg, uint32_t head, const uint64_t *s_lut,
+                                          const uint16_t *s_st, const uint8_t *s_l1, const DecCanon *tab,
+                                          uint32_t mstop, uint32_t &rel, uint32_t &cnt) {
+    cnt = 0;
+    if (rel >= mstop) return true;
+    SWin r;
+    r.init(stg, rel + head);
+    while (rel < mstop) {
+        const uint32_t pk = r.peek12();
+        const uint64_t en = s_lut[pk];
+        uint32_t n = (uint32_t)(en >> 48) & 7u, adv = (uint32_t)(en >> 51) & 15u;
+        if (n == 0) {
+            const uint32_t l1 = s_l1[pk];
+            adv = (l1 & 0x80u) ? dlen_long(tab, r.peek64(), l1 & 0x7Fu) : l1;
+            if (adv == 0) return false;
+            n = 1;
+        } else if (mstop - rel < (uint32_t)kLutBits) {
+            const uint32_t hs = (uint32_t)s_st[pk] & (0xFFFu << (mstop - rel));
+            n -= __popc(hs);
+            adv = hs ? (uint32_t)(__ffs(hs) - 1) : adv;
+        }
+        cnt += n;
+        rel += adv;
+        r.skip(adv);
+    }
+    return true;
+}
+
+// Final decode with a byte-wide stage (u16 books): symbols are staged as
+// bytes s - (cap/2 - 128) and widened in the copy-out, and the decode LUT
+// holds byte deltas (8-byte entries), so a warp needs half of k_dec_final7's
+// shared memory and twice as many warps fit on an SM (the single-chain
+// decode is latency-bound).  A symbol outside the byte range (rare: such
+// symbols have long code words) is staged as the escape byte 255 and its
+// value kept in a per-warp side list that patches the output after the
+// copy-out; a subsequence with more than kF9Esc of them is re-decoded with
+// u16 stores straight to global memory.
+constexpr int kF9Warps = 32;
+constexpr uint32_t kF9Stage = 4256;  // bytes per warp: <= 4096 + 7 (alignment) + overrun slack
+constexpr uint32_t kF9Esc = 16;      // escaped symbols per warp and subsequence
+
+__global__ void __launch_bounds__(kF9Warps * 32, 1) k_dec_final9(DecParams p, uint32_t cap) {
+    extern __shared__ __align__(16) unsigned char f9_smem[];
+    uint64_t *s_lut = reinterpret_cast<uint64_t *>(f9_smem);
+    uint16_t *s_st = reinterpret_cast<uint16_t *>(s_lut + kLutSize);
+    uint16_t *s_s1 = s_st + kLutSize;
+    uint8_t *s_l1 = reinterpret_cast<uint8_t *>(s_s1 + kLutSize);
+    uint8_t *s_out = s_l1 + kLutSize;                                               // kF9Warps * kF9Stage
+    uint32_t *s_str = reinterpret_cast<uint32_t *>(s_out + kF9Warps * kF9Stage);   // kF9Warps * 2 * kStgWords
+    __shared__ DecCanon s_can;
+    __shared__ uint32_t s_esc[kF9Warps][kF9Esc];  // stage index << 16 | symbol
+    __shared__ uint32_t s_nesc[kF9Warps];
+    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) {
+        s_lut[i] = p.tab->lut8[i];
+        s_st[i] = p.tab->lut8s[i];
+        s_s1[i] = p.tab->lut1s[i];
+        s_l1[i] = p.tab->lut1[i];
+    }
+    load_canon(s_can, p.tab);
+    __syncthreads();
+    if (p.st->code) return;  // corrupt stream: leave the output untouched
+    const DecCanon *tab = &s_can;
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    const int32_t base8 = (int32_t)(cap / 2) - 128;
+    const uint32_t b2 = ((uint32_t)base8 & 0xFFFFu) * 0x00010001u;  // per-halfword widening addend
+    uint8_t *wout = s_out + warp * kF9Stage;
+    const uint32_t out_s = (uint32_t)__cvta_generic_to_shared(wout);
+    uint32_t *wstr = s_str + warp * 2 * kStgWords;
+    const uint32_t str_s = (uint32_t)__cvta_generic_to_shared(wstr);
+    uint16_t *out = static_cast<uint16_t *>(p.out);
+    const uint64_t nw = (uint64_t)gridDim.x * kF9Warps;
+    uint64_t t = (uint64_t)blockIdx.x * kF9Warps + warp;
+    uint32_t sb = 0;
+    d3_stage(p, t, str_s, lane);
+    for (; t < p.T; t += nw, sb ^= 1) {
+        d3_stage(p, t + nw, str_s + (sb ^ 1) * kStgWords * 4, lane);
+        d3_stage_wait();
+        const uint32_t *stg = wstr + sb * kStgWords;
+        const uint32_t e = p.ent0[t];
+        if (e == kExitInvalid || e == kExitEnd) continue;
+        const uint64_t t0 = t * kS3;
+        const bool last = t == p.T - 1;
+        const uint32_t stop = last ? (uint32_t)(p.bit_len - t0) : kS3;
+        const uint32_t la = (stop + kMB - 1) / kMB - 1;
+        const uint64_t base = p.off0[t];
+        const uint64_t endo = last ? p.count : p.off0[t + 1];
+        const uint32_t total = (uint32_t)(endo - base);
+        const uint32_t b = lane * kMB;
+        const bool act = lane <= la;
+        const uint32_t mstop = act ? min(b + kMB, stop) : b;
+        const uint32_t cpv = act ? p.cp[t * 32 + lane] : 0u;
+        uint32_t cnt = act ? (cpv >> 8) : 0u;
+        uint32_t start = act ? b + (cpv & 0xFFu) : b;
+        if (lane == 0) start = e;
+        const bool irregular = e != 0 && ((p.irr[t] >> e) & 1ull);
+        if (irregular) {
+            // the true path joins the chain after microblock 0: re-resolve the
+            // lanes' starts and counts (count-only, lane by lane)
+            uint32_t x = __shfl_down_sync(kD3Full, start, 1);  // chain exit guess
+            bool need = lane == 0;
+            bool bad = false;
+            while (__any_sync(kD3Full, need)) {
+                bool changed = false;
+                if (need && act) {
+                    uint32_t rel = start, c;
+                    if (!d3_count8(stg, p.head, s_lut, s_st, s_l1, tab, mstop, rel, c)) bad = true;
+                    changed = rel != x;
+                    cnt = c;
+                    x = rel;
+                }
+                const uint32_t px = __shfl_up_sync(kD3Full, x, 1);
+                const bool pc = __shfl_up_sync(kD3Full, changed, 1);
+                need = lane > 0 && act && pc && px != start;
+                if (need) start = px;
+            }
+            if (__any_sync(kD3Full, bad)) {
+                if (lane == 0) set_status(p.st, LZB_E_CORRUPT);
+                continue;
+            }
+        } else {
+            const uint32_t rest = __reduce_add_sync(kD3Full, lane ? cnt : 0u);
+            if (lane == 0) cnt = total - rest;
+        }
+        uint32_t inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(kD3Full, inc, o);
+            if (lane >= (uint32_t)o) inc += v;
+        }
+        const uint32_t pre = inc - cnt;
+        const uint32_t sum = __shfl_sync(kD3Full, inc, 31);
+        // stage byte j <-> output element base - sh + j; out + base - sh is 16-byte aligned
+        const uint32_t sh = (uint32_t)(((reinterpret_cast<uintptr_t>(out) >> 1) + base) & 7u);
+        bool bad = sum != total || total > kS3 || (act && cnt > kMB);
+        bool wide = false;  // more escaped symbols than the side list holds
+        if (lane == 0) s_nesc[warp] = 0;
+        __syncwarp();
+        uint32_t rel = start;
+        const uint32_t a0 = out_s + sh + pre;  // the lane's first stage byte
+        uint32_t a = a0;
+        if (!__any_sync(kD3Full, bad) && act && rel < mstop) {
+            SWin r;
+            r.init(stg, rel + p.head);
+            while (rel < mstop) {
+                const uint32_t pk = r.peek12();
+                const uint64_t en = s_lut[pk];
+                uint32_t n = (uint32_t)(en >> 48) & 7u, adv = (uint32_t)(en >> 51) & 15u;
+                uint32_t lo = (uint32_t)en, hi = (uint32_t)(en >> 32);
+                if (n == 0) {  // long code word, out-of-byte symbol, or invalid prefix
+                    const uint32_t l1 = s_l1[pk];
+                    uint32_t sym = 0;
+                    if (l1 & 0x80u) adv = dsym_long(tab, p.syms, r.peek64(), l1 & 0x7Fu, sym);
+                    else if (l1) {
+                        adv = l1;
+                        sym = s_s1[pk];
+                    } else {
+                        adv = 0;
+                    }
+                    if (adv == 0) {
+                        bad = true;
+                        break;
+                    }
+                    const int32_t d = (int32_t)sym - base8;
+                    if (d < 0 || d > 254) {  // escape: the value goes to the side list
+                        const uint32_t k = atomicAdd(&s_nesc[warp], 1u);
+                        if (k < kF9Esc) s_esc[warp][k] = ((a - out_s) << 16) | sym;
+                        else wide = true;
+                        lo = 255u;
+                    } else {
+                        lo = (uint32_t)d;
+                    }
+                    n = 1;
+                } else if (mstop - rel < (uint32_t)kLutBits) {  // code words must start before mstop
+                    const uint32_t hs = (uint32_t)s_st[pk] & (0xFFFu << (mstop - rel));
+                    n -= __popc(hs);
+                    adv = hs ? (uint32_t)(__ffs(hs) - 1) : adv;
+                }
+                asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(lo));
+                if (n > 1) asm volatile("st.shared.u8 [%0+1], %1;" ::"r"(a), "r"(lo >> 8));
+                if (n > 2) asm volatile("st.shared.u8 [%0+2], %1;" ::"r"(a), "r"(lo >> 16));
+                if (n > 3) asm volatile("st.shared.u8 [%0+3], %1;" ::"r"(a), "r"(lo >> 24));
+                if (n > 4) asm volatile("st.shared.u8 [%0+4], %1;" ::"r"(a), "r"(hi));
+                if (n > 5) asm volatile("st.shared.u8 [%0+5], %1;" ::"r"(a), "r"(hi >> 8));
+                a += n;
+                rel += adv;
+                r.skip(adv);
+            }
+        }
+        if (__any_sync(kD3Full, wide) && !__any_sync(kD3Full, bad)) {
+            // u16 symbols straight to global memory (slow path)
+            rel = start;
+            uint64_t o = base + pre;
+            const uint64_t o0 = o;
+            if (act && rel < mstop) {
+                SWin r;
+                r.init(stg, rel + p.head);
+                while (rel < mstop) {
+                    const uint32_t pk = r.peek12();
+                    const uint32_t l1 = s_l1[pk];
+                    uint32_t sym = 0, L;
+                    if (l1 & 0x80u) L = dsym_long(tab, p.syms, r.peek64(), l1 & 0x7Fu, sym);
+                    else {
+                        L = l1;
+                        sym = s_s1[pk];
+                    }
+                    if (L == 0 || o - o0 >= cnt) {
+                        bad = true;
+                        break;
+                    }
+                    out[o++] = (uint16_t)sym;
+                    rel += L;
+                    r.skip(L);
+                }
+            }
+            if (act && o - o0 != cnt) bad = true;
+            const uint32_t nstart = __shfl_down_sync(kD3Full, start, 1);
+            if (act && lane < la && rel != nstart) bad = true;
+            if (__any_sync(kD3Full, bad) && lane == 0) set_status(p.st, LZB_E_CORRUPT);
+            continue;
+        }
+        if (act && (a - a0) != cnt) bad = true;
+        {
+            const uint32_t nstart = __shfl_down_sync(kD3Full, start, 1);
+            if (act && lane < la && rel != nstart) bad = true;
+        }
+        if (__any_sync(kD3Full, bad)) {
+            if (lane == 0) set_status(p.st, LZB_E_CORRUPT);
+            continue;
+        }
+        __syncwarp();
+        // copy-out: 8 staged bytes -> 8 u16 symbols (one 16-byte store)
+        const uint64_t g0 = base - sh;
+        const uint32_t q0 = sh ? 1u : 0u, q1 = (sh + total) >> 3;
+        const uint2 *wv = reinterpret_cast<const uint2 *>(wout);
+        for (uint32_t q = q0 + lane; q < q1; q += 32) {
+            const uint2 v = wv[q];
+            uint4 w;
+            w.x = __vadd2(__byte_perm(v.x, 0u, 0x4140), b2);
+            w.y = __vadd2(__byte_perm(v.x, 0u, 0x4342), b2);
+            w.z = __vadd2(__byte_perm(v.y, 0u, 0x4140), b2);
+            w.w = __vadd2(__byte_perm(v.y, 0u, 0x4342), b2);
+            *reinterpret_cast<uint4 *>(out + g0 + 8 * q) = w;
+        }
+        {  // the partial head / tail units, one element per lane
+            const uint32_t c = lane & 7;
+            const uint32_t j = (lane < 8 ? 0u : 8u * q1) + c;
+            const bool part = lane < 8 ? (sh != 0) : (lane < 16 && ((sh + total) & 7) != 0);
+            if (part && j >= sh && j < sh + total) out[g0 + j] = (uint16_t)((int32_t)wout[j] + base8);
+        }
+        __syncwarp();
+        {  // patch the escaped symbols over their widened escape bytes
+            const uint32_t ne = s_nesc[warp];
+            for (uint32_t k = lane; k < ne; k += 32) {
+                const uint32_t v = s_esc[warp][k];
+                out[g0 + (v >> 16)] = (uint16_t)(v & 0xFFFFu);
+            }
+        }
+        __syncwarp();
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}

@@ -624,6 +624,13 @@ struct DecTables {
     // decoded from the 12-bit window, up to six: s[0..5], then
     // n | used << 3 | starts << 8 (bit i of starts: a code word starts at i).
     uint4 lut6[kLutSize];
+    // Byte LUT for the final decode (u16 books, symbols near the radius):
+    // up to six code words whose symbols s satisfy 0 <= s - (cap/2 - 128) < 255,
+    // stored as those byte deltas; bits 48-50 count (0: first code word longer
+    // than 12 bits, invalid, or its symbol out of byte range), 51-54 bits used.
+    uint64_t lut8[kLutSize];
+    uint16_t lut8s[kLutSize];  // code-word start mask of lut8's code words
+    uint16_t lut1s[kLutSize];  // symbol of the first code word (when <= 12 bits)
     // Boundary LUT for the map pass: n | used << 4 | starts << 8, where bit i
     // of `starts` marks a code word starting at window offset i (up to 12
     // complete code words greedily decoded from the 12-bit window).
@@ -886,6 +893,28 @@ __global__ void __launch_bounds__(1024) k_dec_luts(DecTables *tab, const uint32_
         }
         tab->lut6[v] = make_uint4(s6[0] | (s6[1] << 16), s6[2] | (s6[3] << 16), s6[4] | (s6[5] << 16),
                                   m | (u << 3) | (sm << 8));
+    }
+    // lut8: byte deltas against cap/2 - 128, the prefix whose symbols fit a byte
+    {
+        const int32_t base = (int32_t)(cap / 2) - 128;
+        uint32_t m = wide_cap ? 0u : (n < 6 ? n : 6u);
+        for (uint32_t i = 0; i < m; i++) {
+            const int32_t d = (int32_t)sym[i] - base;
+            if (d < 0 || d > 254) {  // 255 is the final pass's escape byte
+                m = i;
+                break;
+            }
+        }
+        uint64_t e = 0;
+        uint32_t u = 0, sm = 0;
+        for (uint32_t i = 0; i < m; i++) {
+            e |= (uint64_t)(uint32_t)((int32_t)sym[i] - base) << (8 * i);
+            sm |= 1u << u;
+            u += len[i];
+        }
+        tab->lut8[v] = e | ((uint64_t)m << 48) | ((uint64_t)u << 51);
+        tab->lut8s[v] = (uint16_t)sm;
+        tab->lut1s[v] = (uint16_t)(n && !wide_cap ? sym[0] : 0u);
     }
     // lutb: all complete code words (count-only), their starts
     {
@@ -1356,11 +1385,11 @@ static int huff_decode_impl(const uint8_t *bits, uint32_t bit_phase, uint64_t bi
         const unsigned fg = (unsigned)umin64((L.T + kFThreads - 1) / kFThreads, (uint64_t)sms * 4);
         const size_t fsm = kLutSize * sizeof(uint64_t) + (size_t)(kFThreads / 32) * 32 * (kStage + 1) * sym_bytes;
         if (sym_bytes == 2 && cap <= 65536) {
-            const size_t f7 = (size_t)kLutSize * (sizeof(uint4) + 1) + (size_t)kF7Warps * kF7Slots * 2 +
-                              (size_t)kF7Warps * 2 * kStgWords * 4;
-            LZB_CUDA_TRY(cudaFuncSetAttribute(k_dec_final7, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f7));
-            const unsigned g7 = (unsigned)umin64((L.T + kF7Warps - 1) / kF7Warps, (uint64_t)sms);
-            k_dec_final7<<<g7, kF7Warps * 32, f7, s>>>(p);
+            const size_t f9 = (size_t)kLutSize * (8 + 2 + 2 + 1) + (size_t)kF9Warps * kF9Stage +
+                              (size_t)kF9Warps * 2 * kStgWords * 4;
+            LZB_CUDA_TRY(cudaFuncSetAttribute(k_dec_final9, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f9));
+            const unsigned g9 = (unsigned)umin64((L.T + kF9Warps - 1) / kF9Warps, (uint64_t)sms);
+            k_dec_final9<<<g9, kF9Warps * 32, f9, s>>>(p, cap);
         } else {
             auto kern = sym_bytes == 2 ? k_dec_final<uint16_t> : k_dec_final<uint32_t>;
             LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
