@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(kD3Warps * 32) k_dec_maps3(DecParams p) {
 
         // ---- C: entry phases 1..P-1 ----
         uint64_t irr = 0;
+        uint32_t emin = kExitInvalid, emax = 0;  // range of this lane's valid exit codes
         for (uint32_t ph = 1 + lane; ph < p.P; ph += 32) {
             uint32_t out = kExitInvalid;
             bool regular = false;
@@ -364,13 +365,27 @@ __global__ void __launch_bounds__(kD3Warps * 32) k_dec_maps3(DecParams p) {
                 }
             }
             if (!regular) irr |= 1ull << ph;
+            if (out != kExitInvalid) {
+                emin = min(emin, out & 0xFFu);
+                emax = max(emax, out & 0xFFu);
+            }
             p.maps[t * p.P + ph] = out;
         }
         irr = __reduce_or_sync(kD3Full, (uint32_t)irr) |
               ((uint64_t)__reduce_or_sync(kD3Full, (uint32_t)(irr >> 32)) << 32);
+        // do all valid entry phases exit at the same phase?  (fast composition)
+        const uint32_t m0 = (vl && xraw != kExitInvalid) ? xraw : kExitInvalid;
+        if (m0 != kExitInvalid) {
+            emin = min(emin, m0);
+            emax = max(emax, m0);
+        }
+        const uint32_t cmn = __reduce_min_sync(kD3Full, emin);
+        const bool nonuni = __reduce_max_sync(kD3Full, emax) != cmn && cmn != kExitInvalid;
         if (lane == 0) {
-            p.maps[t * p.P] = (vl && xraw != kExitInvalid) ? ((tot << 8) | xraw) : kExitInvalid;
+            p.maps[t * p.P] = m0 == kExitInvalid ? kExitInvalid : ((tot << 8) | xraw);
             p.irr[t] = irr;
+            p.uexit[t] = (uint8_t)cmn;
+            if (nonuni) atomicAdd(p.nonuni, 1u);
         }
         __syncwarp();
     }

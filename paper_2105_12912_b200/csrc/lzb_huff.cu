@@ -687,6 +687,10 @@ struct DecParams {
     uint64_t *off0;
     uint16_t *cp;      // v3: per microblock (count << 8) | chain entry offset
     uint64_t *irr;     // v3: per subsequence, entry phases that join the chain late
+    uint8_t *uexit;    // per subsequence: the exit shared by all valid entry phases (0xFF: none)
+    unsigned int *nonuni;  // count of subsequences whose valid entries exit differently
+    uint64_t *ulb;     // look-back words of the uniform scan
+    unsigned int *uticket;
 };
 
 __device__ __forceinline__ uint32_t bswap_load(const DecParams &p, uint64_t w) {
@@ -943,7 +947,8 @@ __global__ void __launch_bounds__(1024) k_dec_luts(DecTables *tab, const uint32_
 // (32-bit or 64-bit packed (count << 8) | exit).
 template <typename InT>
 __global__ void k_dec_compose(const InT *in, uint64_t n_in, uint32_t P, uint32_t G, uint64_t *out,
-                              uint64_t nout) {
+                              uint64_t nout, const unsigned int *nonuni) {
+    if (*nonuni == 0) return;  // the uniform scan resolves the entries
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nout * P;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t g = i / P;
@@ -984,7 +989,78 @@ __device__ __forceinline__ void walk_down(const InT *maps, uint32_t P, uint64_t 
     }
 }
 
+// Fast composition.  When every subsequence's valid entry phases all exit
+// at the same phase (they joined the chain -- the normal case for Huffman
+// codes), subsequence t's entry is t-1's common exit no matter where t-1 was
+// entered, so entries are direct and offsets one exclusive scan of the
+// entered maps' counts (single pass, decoupled look-back).  Otherwise the
+// hierarchical composition below runs instead.
+__global__ void __launch_bounds__(256) k_dec_scan_uniform(DecParams p) {
+    if (*p.nonuni != 0) return;
+    __shared__ uint64_t s_t, s_ex;
+    __shared__ uint64_t s_scan[33];
+    __shared__ int s_bad;
+    const uint64_t ntl = (p.T + 2047) / 2048;
+    while (true) {
+        if (threadIdx.x == 0) {
+            s_t = atomicAdd(p.uticket, 1u);
+            s_bad = 0;
+        }
+        __syncthreads();
+        const uint64_t tl = s_t;
+        if (tl >= ntl) break;
+        const uint64_t b0 = tl * 2048 + (uint64_t)threadIdx.x * 8;
+        uint64_t c[8], sum = 0;
+        uint32_t ent[8];
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint64_t t = b0 + k;
+            c[k] = 0;
+            ent[k] = 0;
+            if (t < p.T) {
+                const uint32_t e = t == 0 ? 0u : p.uexit[t - 1];
+                ent[k] = e;
+                if (e >= p.P || (t + 1 < p.T && p.uexit[t] == kExitEnd)) {
+                    bad = true;  // no valid entry, or END before the last subsequence
+                } else {
+                    const uint32_t v = p.maps[t * p.P + e];
+                    if ((v & 0xFF) == kExitInvalid) bad = true;
+                    c[k] = v >> 8;
+                }
+                sum += c[k];
+            }
+        }
+        if (bad) s_bad = 1;
+        uint64_t tot;
+        const uint64_t off = block_exclusive_scan<uint64_t>(sum, s_scan, &tot);
+        if ((threadIdx.x >> 5) == 0) {
+            const uint64_t ex = lookback_warp(p.ulb, tl, tot);
+            if (lane_id() == 0) s_ex = ex;
+        }
+        __syncthreads();
+        uint64_t run = s_ex + off;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint64_t t = b0 + k;
+            if (t < p.T) {
+                p.ent0[t] = (uint8_t)ent[k];
+                p.off0[t] = run;
+            }
+            run += c[k];
+        }
+        if (s_bad) set_status(p.st, LZB_E_CORRUPT);
+        if (tl == ntl - 1 && threadIdx.x == 0) {
+            const uint64_t total = s_ex + tot;
+            if (p.uexit[p.T - 1] != kExitEnd || total != p.count) set_status(p.st, LZB_E_CORRUPT);
+            p.st->u[0] = total;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void k_dec_top(DecParams p) {
+    if (*p.nonuni == 0) return;
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     uint32_t e = 0;
     uint64_t o = 0;
@@ -1004,6 +1080,7 @@ __global__ void k_dec_top(DecParams p) {
 }
 
 __global__ void k_dec_down2(DecParams p) {
+    if (*p.nonuni == 0) return;
     for (uint64_t h = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; h < p.ng2;
          h += (uint64_t)gridDim.x * blockDim.x)
         walk_down(p.g1, p.P, h * p.G, umin64(h * p.G + p.G, p.ng1), p.ent2[h], p.off2[h], p.ent1,
@@ -1011,6 +1088,7 @@ __global__ void k_dec_down2(DecParams p) {
 }
 
 __global__ void k_dec_down1(DecParams p) {
+    if (*p.nonuni == 0) return;
     for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < p.ng1;
          g += (uint64_t)gridDim.x * blockDim.x)
         walk_down(p.maps, p.P, g * p.G, umin64(g * p.G + p.G, p.T), p.ent1[g], p.off1[g], p.ent0,
@@ -1143,6 +1221,9 @@ static void dec_scratch(Sc &s, const DecLayout &L, uint32_t cap) {
     s.template take<uint64_t>(L.T);
     s.template take<uint16_t>(L.T * 32);
     s.template take<uint64_t>(L.T);
+    s.template take<uint8_t>(L.T);
+    s.template take<unsigned int>(4);
+    s.template take<uint64_t>(L.T / 2048 + 2);
 }
 
 static int dev_sms() {
@@ -1361,7 +1442,13 @@ static int huff_decode_impl(const uint8_t *bits, uint32_t bit_phase, uint64_t bi
     p.off0 = sc.take<uint64_t>(L.T);
     p.cp = sc.take<uint16_t>(L.T * 32);
     p.irr = sc.take<uint64_t>(L.T);
-    if (!p.irr) return LZB_E_ARG;
+    p.uexit = sc.take<uint8_t>(L.T);
+    p.nonuni = sc.take<unsigned int>(4);
+    p.uticket = p.nonuni + 1;
+    p.ulb = sc.take<uint64_t>(L.T / 2048 + 2);
+    if (!p.ulb) return LZB_E_ARG;
+    LZB_CUDA_TRY(cudaMemsetAsync(p.nonuni, 0, 4 * sizeof(unsigned int), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.ulb, 0, (L.T / 2048 + 2) * sizeof(uint64_t), s));
     p.st = st;
     p.out = sym;
     const int sms = dev_sms();
@@ -1369,11 +1456,13 @@ static int huff_decode_impl(const uint8_t *bits, uint32_t bit_phase, uint64_t bi
     // k_dec_tables flags a hint that disagrees with the lengths as corrupt).
     k_dec_maps3<<<(unsigned)umin64((L.T + kD3Warps - 1) / kD3Warps, (uint64_t)sms * 16), kD3Warps * 32, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
+    k_dec_scan_uniform<<<(unsigned)umin64((L.T + 2047) / 2048, (uint64_t)sms * 4), 256, 0, s>>>(p);
+    LZB_LAUNCH_CHECK();
     k_dec_compose<uint32_t><<<(unsigned)umin64((L.ng1 * L.P + 255) / 256, (uint64_t)sms * 32), 256, 0, s>>>(
-        p.maps, L.T, L.P, L.G, p.g1, L.ng1);
+        p.maps, L.T, L.P, L.G, p.g1, L.ng1, p.nonuni);
     LZB_LAUNCH_CHECK();
     k_dec_compose<uint64_t><<<(unsigned)umin64((L.ng2 * L.P + 255) / 256, (uint64_t)sms * 32), 256, 0, s>>>(
-        p.g1, L.ng1, L.P, L.G, p.g2, L.ng2);
+        p.g1, L.ng1, L.P, L.G, p.g2, L.ng2, p.nonuni);
     LZB_LAUNCH_CHECK();
     k_dec_top<<<1, 32, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
