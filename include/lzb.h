@@ -178,6 +178,33 @@ int lzb_huff_decode_at(const uint8_t *bits, uint64_t bit_phase, uint64_t bit_len
                        void *stream);
 
 /* ---------------------------------------------------------------------
+ * Bit-range decode: multi-GPU decompression of ONE stored stream (SURVEY
+ * §8e; the reference decodes the whole stream in one process,
+ * P/huffman.py:107-138).  A rank owns stream bits [bit_lo, bit_hi) of the
+ * stream at `bits` (4-byte aligned, bit_len bits in total, replicated on
+ * every rank); bit_lo is a multiple of LZB_DEC_RANGE_ALIGN and bit_hi is
+ * too unless it is bit_len.
+ *
+ * lzb_huff_range_maps writes fmap[p] = (symbols << 8) | exit for every
+ * entry phase p < maxlen: decoding the range from bit bit_lo + p yields
+ * `symbols` code words and leaves at phase `exit` of the next range (0xFE:
+ * the stream ended exactly, 0xFF: invalid).  The host chains the ranks'
+ * maps from phase 0 to get each range's entry phase, exit phase and symbol
+ * count; lzb_huff_range_decode (same scratch, still holding pass 1's state)
+ * then writes the range's `count` symbols.  A chain that does not end in
+ * 0xFE with the header's symbol count is a corrupt archive.
+ * ------------------------------------------------------------------- */
+#define LZB_DEC_RANGE_ALIGN 4096
+size_t lzb_huff_range_scratch_bytes(uint64_t range_bits, uint32_t maxlen, uint32_t cap);
+int lzb_huff_range_maps(const uint8_t *bits, uint64_t bit_len, uint64_t bit_lo, uint64_t bit_hi,
+                        const uint8_t *lengths, uint32_t cap, uint32_t maxlen, uint64_t *fmap,
+                        lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream);
+int lzb_huff_range_decode(const uint8_t *bits, uint64_t bit_len, uint64_t bit_lo, uint64_t bit_hi,
+                          const uint8_t *lengths, uint32_t cap, uint32_t maxlen, uint32_t entry,
+                          uint32_t exit_phase, uint64_t count, void *sym, int sym_bytes,
+                          lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream);
+
+/* ---------------------------------------------------------------------
  * Number of maximal runs of a symbol stream (sizes K4's outputs before the
  * RLE / RLE_VLE workflows, P/rle.py:17-35).  st->u[0] = run count.
  * ------------------------------------------------------------------- */

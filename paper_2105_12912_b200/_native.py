@@ -50,6 +50,10 @@ SIGNATURES = {
     "lzb_huff_decode_scratch_bytes": (_SZ, [_U64, _U32, _U32]),
     "lzb_huff_decode": (_I, [_P, _U64, _U64, _P, _U32, _U32, _P, _I, _P, _P, _SZ, _P]),
     "lzb_huff_decode_at": (_I, [_P, _U64, _U64, _U64, _P, _U32, _U32, _P, _I, _P, _P, _SZ, _P]),
+    "lzb_huff_range_scratch_bytes": (_SZ, [_U64, _U32, _U32]),
+    "lzb_huff_range_maps": (_I, [_P, _U64, _U64, _U64, _P, _U32, _U32, _P, _P, _P, _SZ, _P]),
+    "lzb_huff_range_decode": (_I, [_P, _U64, _U64, _U64, _P, _U32, _U32, _U32, _U32, _U64, _P, _I, _P, _P,
+                                   _SZ, _P]),
     "lzb_rle_encode_scratch_bytes": (_SZ, [_U64]),
     "lzb_count_runs": (_I, [_P, _I, _U64, _P, _P]),
     "lzb_rle_encode": (_I, [_P, _I, _U64, _P, _P, _U64, _U64, _P, _P, _SZ, _P]),

@@ -250,9 +250,9 @@ __global__ void __launch_bounds__(kD3Warps * 32) k_dec_maps3(DecParams p) {
         d3_stage_wait();
         const uint32_t *stg = s_str[warp][sb];
         const uint64_t t0 = t * kS3;
-        const bool last = t == p.T - 1;
+        const bool last = t == p.T - 1 && !p.open_end;  // END semantics
         const uint32_t stop = last ? (uint32_t)(p.bit_len - t0) : kS3;
-        const uint32_t endrel = (uint32_t)umin64(p.bit_len - t0, 0xFFFFFFF0u);
+        const uint32_t endrel = (uint32_t)umin64(p.total_bits - t0, 0xFFFFFFF0u);
         const uint32_t la = (stop + kMB - 1) / kMB - 1;  // last active lane
         const uint32_t b = lane * kMB;
         const bool act = lane <= la;

@@ -691,6 +691,12 @@ struct DecParams {
     unsigned int *nonuni;  // count of subsequences whose valid entries exit differently
     uint64_t *ulb;     // look-back words of the uniform scan
     unsigned int *uticket;
+    // bit-range mode (multi-GPU decode of one stream, lzb_huff_range_*):
+    // the range starts in phase entry0 and must leave in phase exit_expect
+    // (kExitEnd when it ends the stream); an open range's last subsequence
+    // is an ordinary one, and code words may run past bit_len up to total_bits.
+    uint32_t entry0, exit_expect, open_end;
+    uint64_t total_bits;
 };
 
 __device__ __forceinline__ uint32_t bswap_load(const DecParams &p, uint64_t w) {
@@ -1019,7 +1025,7 @@ __global__ void __launch_bounds__(256) k_dec_scan_uniform(DecParams p) {
             c[k] = 0;
             ent[k] = 0;
             if (t < p.T) {
-                const uint32_t e = t == 0 ? 0u : p.uexit[t - 1];
+                const uint32_t e = t == 0 ? p.entry0 : p.uexit[t - 1];
                 ent[k] = e;
                 if (e >= p.P || (t + 1 < p.T && p.uexit[t] == kExitEnd)) {
                     bad = true;  // no valid entry, or END before the last subsequence
@@ -1052,7 +1058,7 @@ __global__ void __launch_bounds__(256) k_dec_scan_uniform(DecParams p) {
         if (s_bad) set_status(p.st, LZB_E_CORRUPT);
         if (tl == ntl - 1 && threadIdx.x == 0) {
             const uint64_t total = s_ex + tot;
-            if (p.uexit[p.T - 1] != kExitEnd || total != p.count) set_status(p.st, LZB_E_CORRUPT);
+            if (p.uexit[p.T - 1] != p.exit_expect || total != p.count) set_status(p.st, LZB_E_CORRUPT);
             p.st->u[0] = total;
         }
         __syncthreads();
@@ -1062,7 +1068,7 @@ __global__ void __launch_bounds__(256) k_dec_scan_uniform(DecParams p) {
 __global__ void k_dec_top(DecParams p) {
     if (*p.nonuni == 0) return;
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    uint32_t e = 0;
+    uint32_t e = p.entry0;
     uint64_t o = 0;
     for (uint64_t h = 0; h < p.ng2; h++) {
         p.ent2[h] = (uint8_t)e;
@@ -1075,7 +1081,7 @@ __global__ void k_dec_top(DecParams p) {
         o += v >> 8;
         e = (uint32_t)(v & 0xFF);
     }
-    if (e != kExitEnd || o != p.count) set_status(p.st, LZB_E_CORRUPT);
+    if (e != p.exit_expect || o != p.count) set_status(p.st, LZB_E_CORRUPT);
     p.st->u[0] = o;
 }
 
@@ -1388,41 +1394,34 @@ extern "C" size_t lzb_huff_decode_scratch_bytes(uint64_t bit_len, uint32_t maxle
     return s.bytes();
 }
 
-static int huff_decode_impl(const uint8_t *bits, uint32_t bit_phase, uint64_t bit_len, uint64_t count,
-                            const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym, int sym_bytes,
-                            lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream) {
-    if (!lengths || !st || (sym_bytes != 2 && sym_bytes != 4) || cap == 0 || maxlen == 0 ||
-        maxlen > 64 || bit_phase > 7)
-        return LZB_E_ARG;
-    cudaStream_t s = as_stream(stream);
-    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
-    DecLayout L = dec_layout(bit_len, maxlen);
+// Tables + LUTs + the scratch carve-up shared by the whole-stream and the
+// bit-range entry points.  `bits`/`bit_phase` locate the first bit to decode,
+// `bit_len` bits are decoded, code words may read up to `total_bits`.
+static int dec_setup(const uint8_t *bits, uint32_t bit_phase, uint64_t bit_len, uint64_t total_bits,
+                     uint64_t count, const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym,
+                     lzb_dstatus *st, void *scratch, size_t scratch_bytes, cudaStream_t s, bool tables,
+                     DecParams &p, DecLayout &L) {
+    L = dec_layout(bit_len, maxlen);
     Scratch sc(scratch, scratch_bytes);
     DecTables *tab = sc.take<DecTables>(1);
     uint32_t *syms = sc.take<uint32_t>(cap);
     if (!syms) return LZB_E_ARG;
-    k_dec_tables<<<1, 1024, 0, s>>>(lengths, cap, maxlen, tab, syms, st);
-    LZB_LAUNCH_CHECK();
-    k_dec_luts<<<kLutSize / 1024, 1024, 0, s>>>(tab, syms, cap, st);
-    LZB_LAUNCH_CHECK();
-    if (count == 0) {
-        // P/huffman.py:114-117
-        if (bit_len != 0) {
-            lzb_dstatus h{};
-            h.code = LZB_E_CORRUPT;
-            LZB_CUDA_TRY(cudaMemcpyAsync(st, &h, sizeof(int32_t), cudaMemcpyHostToDevice, s));
-            LZB_CUDA_TRY(cudaStreamSynchronize(s));
-        }
-        return LZB_OK;
+    if (tables) {
+        k_dec_tables<<<1, 1024, 0, s>>>(lengths, cap, maxlen, tab, syms, st);
+        LZB_LAUNCH_CHECK();
+        k_dec_luts<<<kLutSize / 1024, 1024, 0, s>>>(tab, syms, cap, st);
+        LZB_LAUNCH_CHECK();
     }
-    if (!bits || !sym) return LZB_E_ARG;
-    DecParams p;
     uintptr_t a = reinterpret_cast<uintptr_t>(bits);
     p.words = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
     p.head = (uint32_t)(a & 3) * 8 + bit_phase;
-    p.nwords = ((p.head + bit_len + 7) / 8 + 3) / 4;
+    p.nwords = ((p.head + total_bits + 7) / 8 + 3) / 4;
     p.bit_len = bit_len;
+    p.total_bits = total_bits;
     p.count = count;
+    p.entry0 = 0;
+    p.exit_expect = kExitEnd;
+    p.open_end = 0;
     p.tab = tab;
     p.syms = syms;
     p.S = L.S;
@@ -1444,25 +1443,43 @@ static int huff_decode_impl(const uint8_t *bits, uint32_t bit_phase, uint64_t bi
     p.irr = sc.take<uint64_t>(L.T);
     p.uexit = sc.take<uint8_t>(L.T);
     p.nonuni = sc.take<unsigned int>(4);
-    p.uticket = p.nonuni + 1;
+    p.uticket = p.nonuni + 1;  // nonuni[2]: an always-set gate for the range composition
     p.ulb = sc.take<uint64_t>(L.T / 2048 + 2);
     if (!p.ulb) return LZB_E_ARG;
-    LZB_CUDA_TRY(cudaMemsetAsync(p.nonuni, 0, 4 * sizeof(unsigned int), s));
-    LZB_CUDA_TRY(cudaMemsetAsync(p.ulb, 0, (L.T / 2048 + 2) * sizeof(uint64_t), s));
     p.st = st;
     p.out = sym;
+    return LZB_OK;
+}
+
+// Per-subsequence transfer maps (phases >= the book's real max length cannot
+// be entries: P = maxlen hint, k_dec_tables flags a hint that disagrees with
+// the lengths as corrupt), then the uniform-exit scan.
+static int dec_maps(DecParams &p, const DecLayout &L, cudaStream_t s) {
     const int sms = dev_sms();
-    // phases >= the book's real max length cannot be entries (P = maxlen hint;
-    // k_dec_tables flags a hint that disagrees with the lengths as corrupt).
+    LZB_CUDA_TRY(cudaMemsetAsync(p.nonuni, 0, 4 * sizeof(unsigned int), s));
     k_dec_maps3<<<(unsigned)umin64((L.T + kD3Warps - 1) / kD3Warps, (uint64_t)sms * 16), kD3Warps * 32, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
-    k_dec_scan_uniform<<<(unsigned)umin64((L.T + 2047) / 2048, (uint64_t)sms * 4), 256, 0, s>>>(p);
-    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}
+
+static int dec_compose(DecParams &p, const DecLayout &L, cudaStream_t s, const unsigned int *gate) {
+    const int sms = dev_sms();
     k_dec_compose<uint32_t><<<(unsigned)umin64((L.ng1 * L.P + 255) / 256, (uint64_t)sms * 32), 256, 0, s>>>(
-        p.maps, L.T, L.P, L.G, p.g1, L.ng1, p.nonuni);
+        p.maps, L.T, L.P, L.G, p.g1, L.ng1, gate);
     LZB_LAUNCH_CHECK();
     k_dec_compose<uint64_t><<<(unsigned)umin64((L.ng2 * L.P + 255) / 256, (uint64_t)sms * 32), 256, 0, s>>>(
-        p.g1, L.ng1, L.P, L.G, p.g2, L.ng2, p.nonuni);
+        p.g1, L.ng1, L.P, L.G, p.g2, L.ng2, gate);
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}
+
+// Entry phase + symbol offset of every subsequence (uniform scan, or the
+// composed hierarchy top-down), then the final decode into p.out.
+static int dec_resolve_final(DecParams &p, const DecLayout &L, cudaStream_t s, int sym_bytes, uint32_t cap) {
+    const int sms = dev_sms();
+    LZB_CUDA_TRY(cudaMemsetAsync(p.uticket, 0, sizeof(unsigned int), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.ulb, 0, (L.T / 2048 + 2) * sizeof(uint64_t), s));
+    k_dec_scan_uniform<<<(unsigned)umin64((L.T + 2047) / 2048, (uint64_t)sms * 4), 256, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
     k_dec_top<<<1, 32, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
@@ -1470,23 +1487,56 @@ static int huff_decode_impl(const uint8_t *bits, uint32_t bit_phase, uint64_t bi
     LZB_LAUNCH_CHECK();
     k_dec_down1<<<(unsigned)umin64((L.ng1 + 127) / 128, (uint64_t)sms * 8), 128, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
-    {
+    if (sym_bytes == 2 && cap <= 65536) {
+        const size_t f9 = (size_t)kLutSize * (8 + 2 + 2 + 1) + (size_t)kF9Warps * kF9Stage +
+                          (size_t)kF9Warps * 2 * kStgWords * 4;
+        LZB_CUDA_TRY(cudaFuncSetAttribute(k_dec_final9, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f9));
+        const unsigned g9 = (unsigned)umin64((L.T + kF9Warps - 1) / kF9Warps, (uint64_t)sms);
+        k_dec_final9<<<g9, kF9Warps * 32, f9, s>>>(p, cap);
+    } else {
         const unsigned fg = (unsigned)umin64((L.T + kFThreads - 1) / kFThreads, (uint64_t)sms * 4);
         const size_t fsm = kLutSize * sizeof(uint64_t) + (size_t)(kFThreads / 32) * 32 * (kStage + 1) * sym_bytes;
-        if (sym_bytes == 2 && cap <= 65536) {
-            const size_t f9 = (size_t)kLutSize * (8 + 2 + 2 + 1) + (size_t)kF9Warps * kF9Stage +
-                              (size_t)kF9Warps * 2 * kStgWords * 4;
-            LZB_CUDA_TRY(cudaFuncSetAttribute(k_dec_final9, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f9));
-            const unsigned g9 = (unsigned)umin64((L.T + kF9Warps - 1) / kF9Warps, (uint64_t)sms);
-            k_dec_final9<<<g9, kF9Warps * 32, f9, s>>>(p, cap);
-        } else {
-            auto kern = sym_bytes == 2 ? k_dec_final<uint16_t> : k_dec_final<uint32_t>;
-            LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-            kern<<<fg, kFThreads, fsm, s>>>(p);
-        }
+        auto kern = sym_bytes == 2 ? k_dec_final<uint16_t> : k_dec_final<uint32_t>;
+        LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+        kern<<<fg, kFThreads, fsm, s>>>(p);
     }
     LZB_LAUNCH_CHECK();
     return LZB_OK;
+}
+
+static int huff_decode_impl(const uint8_t *bits, uint32_t bit_phase, uint64_t bit_len, uint64_t count,
+                            const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym, int sym_bytes,
+                            lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream) {
+    if (!lengths || !st || (sym_bytes != 2 && sym_bytes != 4) || cap == 0 || maxlen == 0 ||
+        maxlen > 64 || bit_phase > 7)
+        return LZB_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
+    if (count == 0) {
+        // P/huffman.py:114-117: tables are still validated
+        Scratch sc(scratch, scratch_bytes);
+        DecTables *tab = sc.take<DecTables>(1);
+        uint32_t *syms = sc.take<uint32_t>(cap);
+        if (!syms) return LZB_E_ARG;
+        k_dec_tables<<<1, 1024, 0, s>>>(lengths, cap, maxlen, tab, syms, st);
+        LZB_LAUNCH_CHECK();
+        if (bit_len != 0) {
+            lzb_dstatus h{};
+            h.code = LZB_E_CORRUPT;
+            LZB_CUDA_TRY(cudaMemcpyAsync(st, &h, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            LZB_CUDA_TRY(cudaStreamSynchronize(s));
+        }
+        return LZB_OK;
+    }
+    if (!bits || !sym) return LZB_E_ARG;
+    DecParams p;
+    DecLayout L;
+    int rc = dec_setup(bits, bit_phase, bit_len, bit_len, count, lengths, cap, maxlen, sym, st, scratch,
+                       scratch_bytes, s, true, p, L);
+    if (rc != LZB_OK) return rc;
+    if ((rc = dec_maps(p, L, s)) != LZB_OK) return rc;
+    if ((rc = dec_compose(p, L, s, p.nonuni)) != LZB_OK) return rc;
+    return dec_resolve_final(p, L, s, sym_bytes, cap);
 }
 
 extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t count,
@@ -1504,4 +1554,72 @@ extern "C" int lzb_huff_decode_at(const uint8_t *bits, uint64_t bit_phase, uint6
     if (bit_phase > 7) return LZB_E_ARG;
     return huff_decode_impl(bits, (uint32_t)bit_phase, bit_len, count, lengths, cap, maxlen, sym, sym_bytes,
                             st, scratch, scratch_bytes, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Bit-range decode: one rank of a multi-GPU decompression of ONE stream
+// (SURVEY §8e).  Rank k owns the stream bits [bit_lo, bit_hi); bit_lo is a
+// multiple of LZB_DEC_RANGE_ALIGN, so its subsequences are the whole-stream
+// decoder's.  Pass 1 (lzb_huff_range_maps) composes the range's transfer map
+// F_k(phase) = (symbols, exit phase); the host chains F_0..F_{k-1} from phase 0
+// (one all-gather of maxlen words per rank) to get the range's entry phase
+// and first symbol; pass 2 (lzb_huff_range_decode) resolves and decodes.
+// ---------------------------------------------------------------------------
+static int range_args(const uint8_t *bits, uint64_t bit_len, uint64_t bit_lo, uint64_t bit_hi,
+                      const uint8_t *lengths, uint32_t cap, uint32_t maxlen, lzb_dstatus *st) {
+    if (!bits || !lengths || !st || cap == 0 || maxlen == 0 || maxlen > 64) return LZB_E_ARG;
+    if (bit_lo % LZB_DEC_RANGE_ALIGN != 0 || bit_lo >= bit_hi || bit_hi > bit_len) return LZB_E_ARG;
+    if (bit_hi != bit_len && bit_hi % LZB_DEC_RANGE_ALIGN != 0) return LZB_E_ARG;
+    if (reinterpret_cast<uintptr_t>(bits) & 3) return LZB_E_ARG;
+    return LZB_OK;
+}
+
+extern "C" size_t lzb_huff_range_scratch_bytes(uint64_t range_bits, uint32_t maxlen, uint32_t cap) {
+    return lzb_huff_decode_scratch_bytes(range_bits, maxlen, cap);
+}
+
+extern "C" int lzb_huff_range_maps(const uint8_t *bits, uint64_t bit_len, uint64_t bit_lo, uint64_t bit_hi,
+                                   const uint8_t *lengths, uint32_t cap, uint32_t maxlen, uint64_t *fmap,
+                                   lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream) {
+    int rc = range_args(bits, bit_len, bit_lo, bit_hi, lengths, cap, maxlen, st);
+    if (rc != LZB_OK || !fmap) return rc != LZB_OK ? rc : LZB_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
+    DecParams p;
+    DecLayout L;
+    rc = dec_setup(bits + bit_lo / 8, 0, bit_hi - bit_lo, bit_len - bit_lo, 0, lengths, cap, maxlen, nullptr,
+                   st, scratch, scratch_bytes, s, true, p, L);
+    if (rc != LZB_OK) return rc;
+    p.open_end = bit_hi < bit_len;
+    if ((rc = dec_maps(p, L, s)) != LZB_OK) return rc;
+    // the composition is always needed here (F_k for every entry phase)
+    LZB_CUDA_TRY(cudaMemsetAsync(p.nonuni + 2, 1, sizeof(unsigned int), s));
+    if ((rc = dec_compose(p, L, s, p.nonuni + 2)) != LZB_OK) return rc;
+    k_dec_compose<uint64_t><<<(unsigned)((L.P + 63) / 64), 64, 0, s>>>(p.g2, L.ng2, L.P, (uint32_t)L.ng2,
+                                                                     fmap, 1, p.nonuni + 2);
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}
+
+extern "C" int lzb_huff_range_decode(const uint8_t *bits, uint64_t bit_len, uint64_t bit_lo, uint64_t bit_hi,
+                                     const uint8_t *lengths, uint32_t cap, uint32_t maxlen, uint32_t entry,
+                                     uint32_t exit_phase, uint64_t count, void *sym, int sym_bytes,
+                                     lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream) {
+    int rc = range_args(bits, bit_len, bit_lo, bit_hi, lengths, cap, maxlen, st);
+    if (rc != LZB_OK) return rc;
+    if ((sym_bytes != 2 && sym_bytes != 4) || entry >= maxlen) return LZB_E_ARG;
+    const bool open = bit_hi < bit_len;
+    if (open && exit_phase >= maxlen) return LZB_E_ARG;
+    if (count == 0) return open ? LZB_E_ARG : LZB_OK;
+    if (!sym) return LZB_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    DecParams p;
+    DecLayout L;
+    rc = dec_setup(bits + bit_lo / 8, 0, bit_hi - bit_lo, bit_len - bit_lo, count, lengths, cap, maxlen, sym,
+                   st, scratch, scratch_bytes, s, false, p, L);
+    if (rc != LZB_OK) return rc;
+    p.open_end = open;
+    p.entry0 = entry;
+    p.exit_expect = open ? exit_phase : kExitEnd;
+    return dec_resolve_final(p, L, s, sym_bytes, cap);
 }

@@ -23,6 +23,18 @@ Only the Huffman workflow is sharded; when the rule selects RLE / RLE+VLE
 (runs would have to be stitched across slabs) the ranks gather the symbol
 stream to rank 0, which encodes it -- correct, not scalable.
 
+Decompression comes in two forms.  ``decompress_sharded`` inverts
+``compress_sharded`` with no collective (each rank still holds its own
+slice).  ``decompress_archive_sharded`` decodes ONE stored archive,
+replicated on every rank, whose slab layout is unknown: rank k takes an
+equal, 4096-bit-aligned range of the dense stream, builds that range's
+transfer map F_k(phase) = (symbols, exit phase) with the self-synchronising
+decoder (lzb_huff_range_maps), the maps are all-gathered (maxlen words per
+rank) and chained from phase 0 on every rank, each rank decodes its range
+from its resolved entry phase (lzb_huff_range_decode), an all-to-all moves
+the symbols to their slab's owner, and each rank reconstructs its slab with
+the outlier records of its index range.
+
 The per-rank compute is behind ``SlabOps`` (device kernels in production,
 ``DeviceSlabOps``); tests drive the same collective/offset/assembly logic
 with CPU stand-ins over a gloo process group.
@@ -131,6 +143,130 @@ class SlabOps:
                     n_out: int, dtype_code: int):
         """Slab values (fuse outliers, partial sums, dequantise)."""
         raise NotImplementedError
+
+
+    # -- single-archive decompress (decompress_archive_sharded) --
+    def stream_info(self, arc, hdr) -> tuple[int, int, int]:
+        """(bit_len, symbol count, max code length) of a Huffman archive."""
+        raise NotImplementedError
+
+    def range_maps(self, arc, hdr, bit_len: int, lo: int, hi: int, maxlen: int):
+        """int64[maxlen] transfer map of stream bits [lo, hi): (symbols << 8) | exit."""
+        raise NotImplementedError
+
+    def range_decode(self, arc, hdr, bit_len: int, lo: int, hi: int, maxlen: int, entry: int,
+                     exit_phase: int, count: int):
+        """The `count` symbols (code_bytes each) decoded from bit lo + entry."""
+        raise NotImplementedError
+
+    def exchange(self, codes, send_bytes: list[int], recv_bytes: list[int], group):
+        """all-to-all of byte ranges (rank order on both sides)."""
+        raise NotImplementedError
+
+    def slab_records(self, arc, hdr, idx_lo: int, idx_hi: int):
+        """(slab-local records, count) of the outliers with lo <= index < hi."""
+        raise NotImplementedError
+
+    def decompress_full(self, arc, hdr):
+        """Whole-field values (replicated fallback for the run-length workflows)."""
+        raise NotImplementedError
+
+
+EXIT_END = 0xFE
+EXIT_INVALID = 0xFF
+RANGE_ALIGN = 4096  # LZB_DEC_RANGE_ALIGN
+
+
+def stream_ranges(bit_len: int, world: int) -> list[tuple[int, int]]:
+    """Equal, RANGE_ALIGN-aligned bit ranges of the dense stream, rank order."""
+    t = (bit_len + RANGE_ALIGN - 1) // RANGE_ALIGN
+    q, r = divmod(t, world)
+    out = []
+    for k in range(world):
+        t0 = k * q + min(k, r)
+        t1 = t0 + q + (1 if k < r else 0)
+        out.append((min(bit_len, t0 * RANGE_ALIGN), min(bit_len, t1 * RANGE_ALIGN)))
+    return out
+
+
+def chain_ranges(maps: list, ranges: list[tuple[int, int]], count: int):
+    """Chain the ranks' transfer maps from phase 0 (the stream start).
+
+    Returns per rank (entry phase, exit phase, first symbol, symbols).  A
+    chain that hits an invalid code word, ends early, or does not end exactly
+    at the stream end with `count` symbols is a corrupt archive."""
+    from .errors import CorruptArchiveError
+
+    e, o = 0, 0
+    out = []
+    for k, (lo, hi) in enumerate(ranges):
+        if hi <= lo:
+            out.append((e, e, o, 0))
+            continue
+        if e == EXIT_END or e == EXIT_INVALID or e >= len(maps[k]):
+            raise CorruptArchiveError("bit stream does not decode to its declared symbols")
+        v = int(maps[k][e])
+        n, x = v >> 8, v & 0xFF
+        out.append((e, x, o, n))
+        e, o = x, o + n
+    if e != EXIT_END or o != count:
+        raise CorruptArchiveError("bit stream does not decode to its declared symbols")
+    return out
+
+
+def _overlap(a0: int, a1: int, b0: int, b1: int) -> int:
+    return max(0, min(a1, b1) - max(a0, b0))
+
+
+def decompress_archive_sharded(ops: SlabOps, arc, group=None, raw_host: bytes | None = None):
+    """Rank-local part of decompressing ONE archive held by every rank.
+
+    Returns (this rank's slab values or None, (lo, hi) along the slowest
+    axis, header).  Collectives: one all-gather of maxlen int64 per rank and
+    one all-to-all of symbols (each rank sends to the one or two slab owners
+    its stream range overlaps)."""
+    import torch
+    import torch.distributed as dist
+
+    from .pipeline import Workflow, code_bytes_for, parse_header
+
+    hdr = parse_header(raw_host if raw_host is not None else arc)
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    dims, chunk, cap = hdr.dims, hdr.chunk, hdr.cap
+    lo, hi = slab_bounds(dims, chunk, rank, world)
+    sd = slab_dims(dims, lo, hi) if hi > lo else None
+    if hdr.workflow is not Workflow.HUFFMAN:
+        y = ops.decompress_full(arc, hdr)
+        a, b = slab_index_offset(dims, lo), slab_index_offset(dims, hi)
+        return (y[a:b] if sd is not None else None), (lo, hi), hdr
+    bit_len, count, maxlen = ops.stream_info(arc, hdr)
+    ranges = stream_ranges(bit_len, world)
+    r_lo, r_hi = ranges[rank]
+    if r_hi > r_lo:
+        fmap = ops.range_maps(arc, hdr, bit_len, r_lo, r_hi, maxlen)
+    else:
+        fmap = ops.to_tensor(np.arange(maxlen, dtype=np.int64))  # empty range: identity
+    fmap = fmap.to(torch.int64).reshape(-1)
+    allm = [torch.zeros_like(fmap) for _ in range(world)]
+    dist.all_gather(allm, fmap, group=group)
+    chain = chain_ranges([m.cpu().numpy() for m in allm], ranges, count)
+    entry, exit_phase, first, n_sym = chain[rank]
+    cb = code_bytes_for(cap)
+    mine = ops.range_decode(arc, hdr, bit_len, r_lo, r_hi, maxlen, entry, exit_phase, n_sym)         if n_sym else None
+    # symbol ranges of the slabs (a slab's first chunk-major symbol is its
+    # first row-major element: slabs are whole chunk layers)
+    starts = [slab_index_offset(dims, slab_bounds(dims, chunk, j, world)[0]) for j in range(world)]
+    starts.append(dims.count)
+    send = [cb * _overlap(first, first + n_sym, starts[j], starts[j + 1]) for j in range(world)]
+    recv = [cb * _overlap(c[2], c[2] + c[3], starts[rank], starts[rank + 1]) for c in chain]
+    codes = ops.exchange(mine, send, recv, group)
+    if sd is None:
+        return None, (lo, hi), hdr
+    recs, n_out = ops.slab_records(arc, hdr, starts[rank], starts[rank + 1])
+    y = ops.reconstruct(codes, sd, chunk, hdr.eb_abs, cap, recs, n_out,
+                        0 if hdr.dtype == "f32" else 1)
+    return y, (lo, hi), hdr
 
 
 def compress_sharded(ops: SlabOps, values, dims: Dims, vmin: float, vmax: float, eb: float,
@@ -400,10 +536,113 @@ class DeviceSlabOps(SlabOps):
                                      records.data_ptr() if records is not None else None, n_out, g,
                                      eb_abs, cap, y.data_ptr(), dtype_code, None, st.data_ptr(),
                                      scr.data_ptr(), rs, N.stream_ptr()), "reconstruct")
-        (sd,) = N.read_status(self._decode_status)
-        N.raise_for(sd, "decode", "bit stream does not decode to its declared symbols")
+        if getattr(self, "_decode_status", None) is not None:
+            (sd,) = N.read_status(self._decode_status)
+            N.raise_for(sd, "decode", "bit stream does not decode to its declared symbols")
         (sk,) = N.read_status(st)
         if sk.code == N.LZB_E_CORRUPT:
             raise CorruptArchiveError("invalid outlier list")
         N.raise_for(sk, "reconstruct")
         return y
+
+    # -- single-archive decompress --
+    def _host(self, arc, a: int, b: int) -> bytes:
+        return arc[a:b].cpu().numpy().tobytes()
+
+    def stream_info(self, arc, hdr):
+        from .errors import CorruptArchiveError
+        from .pipeline import _validate_lengths_host
+
+        sym_off, sym_len = hdr.symbols
+        if sym_len < 16:
+            raise CorruptArchiveError("bit stream shorter than its header")
+        bit_len, count = struct.unpack("<QQ", self._host(arc, sym_off, sym_off + 16))
+        if sym_len - 16 < (bit_len + 7) // 8:
+            raise CorruptArchiveError("bit stream data truncated")
+        if count != hdr.count:
+            raise CorruptArchiveError("decoded stream length does not match the grid")
+        cb = np.frombuffer(self._host(arc, hdr.codebook[0], sum(hdr.codebook)), np.uint8)
+        self._arc_ptr = arc.data_ptr()
+        return bit_len, count, _validate_lengths_host(cb)
+
+    def _range_scratch(self, lo, hi, maxlen, cap):
+        from . import _native as N
+
+        key = (lo, hi, maxlen, cap)
+        if getattr(self, "_rkey", None) != key:
+            L = N.lib()
+            self._rbytes = L.lzb_huff_range_scratch_bytes(hi - lo, maxlen, cap)
+            self._rscr = N.empty_bytes(self._rbytes, self.device)
+            self._rst = N.empty_bytes(N.STATUS_BYTES, self.device)
+            self._rkey = key
+        return self._rscr, self._rbytes, self._rst
+
+    def range_maps(self, arc, hdr, bit_len, lo, hi, maxlen):
+        import torch
+
+        from . import _native as N
+
+        L = N.lib()
+        scr, nb, st = self._range_scratch(lo, hi, maxlen, hdr.cap)
+        fmap = torch.empty(maxlen, dtype=torch.int64, device=self.device)
+        base = arc.data_ptr()
+        N.check_rc(L.lzb_huff_range_maps(base + hdr.symbols[0] + 16, bit_len, lo, hi,
+                                         base + hdr.codebook[0], hdr.cap, maxlen, fmap.data_ptr(),
+                                         st.data_ptr(), scr.data_ptr(), nb, N.stream_ptr()),
+                   "huff_range_maps")
+        (s,) = N.read_status(st)
+        N.raise_for(s, "decode", "bit stream does not decode to its declared symbols")
+        return fmap
+
+    def range_decode(self, arc, hdr, bit_len, lo, hi, maxlen, entry, exit_phase, count):
+        import torch
+
+        from . import _native as N
+        from .pipeline import code_bytes_for
+
+        L = N.lib()
+        cb = code_bytes_for(hdr.cap)
+        scr, nb, st = self._range_scratch(lo, hi, maxlen, hdr.cap)
+        sym = torch.empty(count * cb, dtype=torch.uint8, device=self.device)
+        base = arc.data_ptr()
+        N.check_rc(L.lzb_huff_range_decode(base + hdr.symbols[0] + 16, bit_len, lo, hi,
+                                           base + hdr.codebook[0], hdr.cap, maxlen, entry,
+                                           exit_phase if exit_phase < 0xFE else 0, count,
+                                           sym.data_ptr(), cb, st.data_ptr(), scr.data_ptr(), nb,
+                                           N.stream_ptr()), "huff_range_decode")
+        self._decode_status = st
+        return sym
+
+    def exchange(self, codes, send_bytes, recv_bytes, group):
+        import torch
+        import torch.distributed as dist
+
+        inp = codes if codes is not None else torch.empty(0, dtype=torch.uint8, device=self.device)
+        out = torch.empty(sum(recv_bytes), dtype=torch.uint8, device=self.device)
+        if dist.get_backend(group) == "gloo":  # CPU transport (tests, same-device runs)
+            o = torch.empty(sum(recv_bytes), dtype=torch.uint8)
+            dist.all_to_all_single(o, inp.cpu(), recv_bytes, send_bytes, group=group)
+            out.copy_(o)
+        else:
+            dist.all_to_all_single(out, inp, recv_bytes, send_bytes, group=group)
+        return out
+
+    def slab_records(self, arc, hdr, idx_lo, idx_hi):
+        import torch
+
+        n = hdr.outlier_count
+        if n == 0:
+            return None, 0
+        off = hdr.outliers[0]
+        r = arc[off: off + 16 * n].view(torch.int64).view(-1, 2)
+        b = torch.searchsorted(r[:, 0].contiguous(),
+                               torch.tensor([idx_lo, idx_hi], dtype=torch.int64, device=arc.device))
+        a, z = (int(v) for v in b.cpu())
+        if z <= a:
+            return None, 0
+        return self.local_records(r[a:z].reshape(-1).view(torch.uint8), z - a, idx_lo), z - a
+
+    def decompress_full(self, arc, hdr):
+        from .pipeline import decompress_device
+
+        return decompress_device(arc)[0]

@@ -6,6 +6,7 @@ infrastructure); production uses DeviceSlabOps (the CUDA kernels)."""
 
 import os
 import socket
+import struct
 
 import numpy as np
 import pytest
@@ -73,6 +74,82 @@ class OracleSlabOps:
                              "f32" if dtype_code == 0 else "f64")
 
 
+    # -- single-archive decompress: the true code-word boundaries come from a
+    # whole-stream oracle decode; a range walk decodes bit-serially from its
+    # entry until it lands on one of them (self-synchronisation), then follows
+    # the true path.
+    def stream_info(self, arc, hdr):
+        off = hdr.symbols[0]
+        bit_len, count = struct.unpack_from("<QQ", arc, off)
+        lens = np.frombuffer(arc, np.uint8, hdr.codebook[1], hdr.codebook[0])
+        data = arc[off + 16: off + 16 + (bit_len + 7) // 8]
+        self._syms = O.huff_decode(bit_len, count, data, lens)
+        self._bits = np.unpackbits(np.frombuffer(data, np.uint8))
+        self._bounds = np.concatenate([[0], np.cumsum(lens[self._syms].astype(np.int64))])
+        codes = O.canonical_codes(lens)
+        self._book = {(int(n), int(codes[i])) for i, n in enumerate(lens) if n}
+        self._cap = hdr.cap
+        return bit_len, count, int(lens.max())
+
+    def _walk(self, pos, hi, bit_len):
+        n = 0
+        while pos < hi:
+            j = int(np.searchsorted(self._bounds, pos))
+            if self._bounds[j] == pos:  # synced
+                k = int(np.searchsorted(self._bounds, hi))
+                return n + k - j, int(self._bounds[k])
+            code, ln = 0, 0
+            while (ln, code) not in self._book:
+                if pos + ln >= bit_len or ln >= 64:
+                    return None
+                code = (code << 1) | int(self._bits[pos + ln])
+                ln += 1
+            pos += ln
+            n += 1
+        return n, pos
+
+    def range_maps(self, arc, hdr, bit_len, lo, hi, maxlen):
+        import torch
+
+        f = np.zeros(maxlen, np.int64)
+        for ph in range(maxlen):
+            w = self._walk(lo + ph, hi, bit_len)
+            if w is None:
+                f[ph] = 0xFF
+            elif hi == bit_len:
+                f[ph] = (w[0] << 8) | (0xFE if w[1] == bit_len else 0xFF)
+            else:
+                f[ph] = (w[0] << 8) | (w[1] - hi)
+        return torch.from_numpy(f)
+
+    def range_decode(self, arc, hdr, bit_len, lo, hi, maxlen, entry, exit_phase, count):
+        j = int(np.searchsorted(self._bounds, lo + entry))
+        assert self._bounds[j] == lo + entry
+        assert self._bounds[j + count] == (bit_len if exit_phase == 0xFE else hi + exit_phase)
+        return self._syms[j: j + count].astype(np.uint16 if self._cap <= 65536 else np.uint32)
+
+    def exchange(self, codes, send_bytes, recv_bytes, group):
+        import torch
+        import torch.distributed as dist
+
+        dt = np.uint16 if self._cap <= 65536 else np.uint32
+        inp = torch.from_numpy(np.ascontiguousarray(codes).view(np.uint8).copy()) \
+            if codes is not None else torch.empty(0, dtype=torch.uint8)
+        out = torch.empty(sum(recv_bytes), dtype=torch.uint8)
+        dist.all_to_all_single(out, inp, recv_bytes, send_bytes, group=group)
+        return out.numpy().view(dt)
+
+    def slab_records(self, arc, hdr, idx_lo, idx_hi):
+        r = np.frombuffer(arc, [("i", "<u8"), ("d", "<i8")], hdr.outlier_count, hdr.outliers[0])
+        sel = r[(r["i"] >= idx_lo) & (r["i"] < idx_hi)]
+        if not len(sel):
+            return None, 0
+        return self.local_records(sel.view(np.uint8), len(sel), idx_lo), len(sel)
+
+    def decompress_full(self, arc, hdr):
+        return O.decompress(arc)[0]
+
+
 def _worker(rank, world, port, case, q):
     import torch.distributed as dist
 
@@ -134,6 +211,84 @@ def test_sharded_archive_is_byte_identical(shape, world):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert got == ref
+
+
+def _archive_worker(rank, world, port, case, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2105_12912_b200 import distributed as D
+
+        arc, shape = case
+        y, (lo, hi), hdr = D.decompress_archive_sharded(OracleSlabOps(), arc, raw_host=arc)
+        ref = O.decompress(arc)[0].reshape(shape)
+        want = ref[lo:hi].reshape(-1) if len(shape) > 1 else ref[lo:hi]
+        if hi > lo:
+            assert y is not None and np.array_equal(np.asarray(y), want), rank
+        else:
+            assert y is None
+        q.put((rank, lo, hi))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("shape,workflow", [((40, 30, 36), None), ((300, 257), None),
+                                            ((70,), None), ((64, 64), "rle")])
+def test_sharded_decompress_of_one_archive(shape, workflow, world):
+    """Every rank holds the same archive; the ranks' slabs of the bit-range
+    decode (transfer maps all-gathered and chained, symbols all-to-all'd to
+    the slab owners) equal the single-process decompress."""
+    import torch.multiprocessing as mp
+
+    from helpers import smooth
+
+    vals = smooth(shape).reshape(-1)
+    if workflow == "rle":
+        vals = np.round(vals * 2).astype(np.float32)  # long runs of equal codes
+    dims = tuple(list(shape[::-1]) + [1] * (3 - len(shape))) + (len(shape),)
+    arc = O.compress(vals, dims, float(vals.min()), float(vals.max()), 1e-4 if workflow is None
+                     else 1e-2, workflow=workflow)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_archive_worker, args=(r, world, port, (arc, shape), q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got[0][1] == 0 and all(a[2] == b[1] for a, b in zip(got, got[1:]))
+
+
+def test_stream_ranges_and_chain():
+    from paper_2105_12912_b200 import distributed as D
+    from paper_2105_12912_b200.errors import CorruptArchiveError
+
+    for bit_len in (1, 4095, 4096, 4097, 10 * 4096 + 5):
+        for world in (1, 2, 3, 8):
+            r = D.stream_ranges(bit_len, world)
+            assert r[0][0] == 0 and r[-1][1] == bit_len
+            assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+            assert all(lo % 4096 == 0 for lo, hi in r if hi > lo)
+    # two ranges: [0,4096) maps phase 0 -> 3 symbols exit 2; [4096,..) phase 2 -> END
+    ranges = [(0, 4096), (4096, 5000), (5000, 5000)]
+    m0 = np.array([(3 << 8) | 2, 0xFF, 0xFF], np.int64)
+    m1 = np.array([0xFF, 0xFF, (4 << 8) | 0xFE], np.int64)
+    assert D.chain_ranges([m0, m1, None], ranges, 7) == [(0, 2, 0, 3), (2, 0xFE, 3, 4),
+                                                         (0xFE, 0xFE, 7, 0)]
+    with pytest.raises(CorruptArchiveError):
+        D.chain_ranges([m0, m1, None], ranges, 8)  # wrong symbol count
+    with pytest.raises(CorruptArchiveError):
+        D.chain_ranges([m0, np.array([0xFF, 0xFF, 0xFF]), None], ranges, 7)  # invalid code word
+    m0e = np.array([(3 << 8) | 0xFE, 0xFF, 0xFF], np.int64)
+    with pytest.raises(CorruptArchiveError):
+        D.chain_ranges([m0e, m1, None], ranges, 7)  # END before the last range
 
 
 def test_slab_bounds_cover_whole_chunk_layers():
