@@ -440,6 +440,7 @@ def run_sharded(args, cfg, rank, world, dev, local_rank):
                "ms_per_step": round(v * 1e3, 2), "steps": args.e2e_steps,
                "note": "per rank: its slab H2D, sharded compress + slab decompress, slab D2H; max over ranks"}
         del xh, yh, xd
+    arch = archive_decompress_sharded(args, cfg, dims, ops, x, lo, hi, eb, vmin, vmax, dev, nbytes)
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": round(nbytes / t_step / 1e9, 3), "unit": "GB/s",
@@ -461,8 +462,55 @@ def run_sharded(args, cfg, rank, world, dev, local_rank):
             "gpu_launches": (LAUNCHES["lzb_quantize"] + LAUNCHES["lzb_codebook"] + LAUNCHES["lzb_huff_encode"]
                              + LAUNCHES["lzb_huff_decode"] + LAUNCHES["lzb_reconstruct_with_outliers"])
                             * args.steps * world,
-            "clocks": clk, "e2e": e2e, "cpu_baseline": None,
+            "clocks": clk, "e2e": e2e, "cpu_baseline": None, "archive_decompress": arch,
         }), flush=True)
+
+
+def archive_decompress_sharded(args, cfg, dims, ops, x, lo, hi, eb, vmin, vmax, dev, nbytes):
+    """Side measurement (not the headline): decompress ONE stored archive,
+    replicated on every rank, on N GPUs -- per-rank bit-range transfer maps,
+    their all-gather, range decode, all-to-all of symbols to the slab owners,
+    slab reconstruct (distributed.decompress_archive_sharded).  Time = max
+    over ranks (CUDA events)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2105_12912_b200 as lzb
+    from paper_2105_12912_b200 import distributed as D
+
+    try:
+        xf = gen_field_device(cfg, dev)
+        fa = lzb.compress_device(lzb.Field.from_array(xf.reshape(cfg["shape"])), eb)
+        arc = fa.data[: fa.nbytes].clone()
+        del xf, fa
+        ta = []
+        ya = None
+        for k in range(args.warmup + args.steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            a0, a1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            a0.record()
+            ya, (alo, ahi), _ = D.decompress_archive_sharded(ops, arc)
+            a1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([a0.elapsed_time(a1) / 1e3], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            if k >= args.warmup:
+                ta.append(float(t))
+        assert (alo, ahi) == (lo, hi)
+        slack = float(np.spacing(np.float32(max(abs(vmin), abs(vmax))))) / 2
+        ok = ya is None or (ya.double() - x.double()).abs().max().item() <= \
+            eb * (vmax - vmin) * (1 + 1e-12) + slack
+        okt = torch.tensor([1 if ok else 0], device=dev, dtype=torch.int64)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        v = statistics.mean(ta)
+        return {"decompress_gbs": round(nbytes / v / 1e9, 3), "ms_per_step": round(v * 1e3, 3),
+                "steps": args.steps, "bound_ok": bool(int(okt.item())),
+                "note": "one stored archive on every rank -> each rank's slab: range maps, "
+                        "all-gather, range decode, all-to-all, reconstruct; max over ranks"}
+    except Exception as exc:  # reported, never fatal for the headline line
+        return {"error": repr(exc)[:300]}
 
 
 def run_gpu(args, cfg, rank, world, local_rank):
