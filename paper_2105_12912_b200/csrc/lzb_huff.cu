@@ -447,25 +447,23 @@ __device__ __forceinline__ void enc_pack_lane(const uint4 (&v)[4], uint32_t nv, 
     last_n = n;
 }
 
-__global__ void __launch_bounds__(kWWarps * 32, 2) k_huff_encode_w(const __grid_constant__ EncWParams p) {
+__global__ void __launch_bounds__(kWWarps * 32, 4) k_huff_encode_w(const __grid_constant__ EncWParams p) {
     extern __shared__ __align__(16) unsigned char ew_smem[];
-    // [table: cap x u64 (left-aligned code | len << 32)][lens: cap x u8]
-    // [stage: warps x 2 x 2 KB][words: warps x wwords u32]
+    // [table: cap x u64 (left-aligned code | len << 32)][stage: warps x 2 KB]
+    // [words: warps x wwords u32]
     uint64_t *s_tab = reinterpret_cast<uint64_t *>(ew_smem);
-    uint8_t *s_len = reinterpret_cast<uint8_t *>(s_tab + p.cap);
-    unsigned char *stage_all = ew_smem + (((size_t)p.cap * 9 + 15) & ~(size_t)15);
-    uint32_t *words_all = reinterpret_cast<uint32_t *>(stage_all + kWWarps * 2 * kWTile * 2);
+    unsigned char *stage_all = ew_smem + (((size_t)p.cap * 8 + 15) & ~(size_t)15);
+    uint32_t *words_all = reinterpret_cast<uint32_t *>(stage_all + kWWarps * kWTile * 2);
     for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) {
         const uint32_t L = p.lengths[i];
         const uint32_t cal = (L && L <= 32) ? (uint32_t)(p.codes[i] << (32 - L)) : 0u;
         s_tab[i] = (uint64_t)cal | ((uint64_t)L << 32);
-        s_len[i] = (uint8_t)L;
     }
     __syncthreads();
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     const uint64_t NW = (uint64_t)gridDim.x * kWWarps;
     uint64_t t = (uint64_t)blockIdx.x * kWWarps + warp;
-    unsigned char *stage = stage_all + warp * 2 * kWTile * 2;
+    unsigned char *stage = stage_all + warp * kWTile * 2;
     const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
     uint32_t *words = words_all + warp * p.wwords;
     const uint32_t words_s = (uint32_t)__cvta_generic_to_shared(words);
@@ -474,19 +472,18 @@ __global__ void __launch_bounds__(kWWarps * 32, 2) k_huff_encode_w(const __grid_
     const bool aligned_in = (reinterpret_cast<uintptr_t>(p.sym) & 15) == 0;
 
     auto is_full = [&](uint64_t tt) { return aligned_in && (tt + 1) * kWTile <= p.n; };
-    auto prefetch = [&](uint64_t tt, uint32_t buf) {
+    auto prefetch = [&](uint64_t tt) {
         const unsigned char *src = reinterpret_cast<const unsigned char *>(p.sym + tt * kWTile);
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             const uint32_t q = j * 32 + lane;  // coalesced global pieces
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(stage_s + buf * kWTile * 2 + wswz(q) * 16),
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(stage_s + wswz(q) * 16),
                          "l"(src + q * 16)
                          : "memory");
         }
     };
-    if (t < p.ntiles && is_full(t)) prefetch(t, 0);
+    if (t < p.ntiles && is_full(t)) prefetch(t);
     asm volatile("cp.async.commit_group;" ::: "memory");
-    uint32_t sb = 0;
     // the lane count and tile offset are loaded one tile ahead (latency)
     uint32_t nb_nx = t < p.ntiles ? p.lcnt[t * 32 + lane] : 0u;
     uint64_t ex_nx = t < p.ntiles ? p.toff[t] : 0ull;
@@ -497,20 +494,18 @@ __global__ void __launch_bounds__(kWWarps * 32, 2) k_huff_encode_w(const __grid_
         if (tn < p.ntiles) {
             nb_nx = p.lcnt[tn * 32 + lane];
             ex_nx = p.toff[tn];
-            if (is_full(tn)) prefetch(tn, sb ^ 1);
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncwarp();  // lanes read pieces other lanes copied
         const bool full = is_full(t);
         const uint64_t b0 = t * kWTile + (uint64_t)lane * kWSyms;
-        // ---- the lane's 32 symbols ----
+        // ---- the lane's 32 symbols (into registers; the stage is then free) ----
         uint4 v[4];
         uint32_t nv = kWSyms;
         if (full) {
 #pragma unroll
             for (int k = 0; k < 4; k++)
-                v[k] = *reinterpret_cast<const uint4 *>(stage + sb * kWTile * 2 + wswz(4 * lane + k) * 16);
+                v[k] = *reinterpret_cast<const uint4 *>(stage + wswz(4 * lane + k) * 16);
         } else {
             nv = b0 >= p.n ? 0u : (uint32_t)umin64(kWSyms, p.n - b0);
 #pragma unroll
@@ -526,6 +521,9 @@ __global__ void __launch_bounds__(kWWarps * 32, 2) k_huff_encode_w(const __grid_
                 v[k] = make_uint4(w[0], w[1], w[2], w[3]);
             }
         }
+        __syncwarp();  // every lane holds its pieces: refill the stage with the next tile
+        if (tn < p.ntiles && is_full(tn)) prefetch(tn);
+        asm volatile("cp.async.commit_group;" ::: "memory");
         // ---- lane bit offsets from the count pass ----
         uint32_t inc = nb;
 #pragma unroll
@@ -568,7 +566,6 @@ __global__ void __launch_bounds__(kWWarps * 32, 2) k_huff_encode_w(const __grid_
             }
         }
         __syncwarp();
-        sb ^= 1;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
@@ -1288,7 +1285,7 @@ static int huff_encode_w(const void *sym, uint64_t n, const uint8_t *lengths, co
     p.st = st;
     p.ntiles = ntw;
     p.wwords = (32 * maxlen + 2 + 3) & ~3u;
-    const size_t smem = (((size_t)cap * 9 + 15) & ~(size_t)15) + (size_t)kWWarps * 2 * kWTile * 2 +
+    const size_t smem = (((size_t)cap * 8 + 15) & ~(size_t)15) + (size_t)kWWarps * kWTile * 2 +
                         (size_t)kWWarps * p.wwords * 4;
     LZB_CUDA_TRY(cudaFuncSetAttribute(k_huff_encode_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
