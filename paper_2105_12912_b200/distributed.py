@@ -19,9 +19,16 @@ into its own byte slice.  Neighbouring slices share at most one boundary
 byte, which the assembly OR-merges; the result is byte-identical to the
 single-GPU archive (and to the reference's).
 
-Only the Huffman workflow is sharded; when the rule selects RLE / RLE+VLE
-(runs would have to be stitched across slabs) the ranks gather the symbol
-stream to rank 0, which encodes it -- correct, not scalable.
+When the 1.09-bit rule selects RLE+VLE, each rank run-length encodes its
+slab (K4), the ranks all-gather each slab's boundary runs (first / last
+value, total length, split count) and every rank applies the same stitching
+plan (``plan_rle_stitch``): a maximal run that crosses slab boundaries --
+possibly through whole single-run slabs -- is emitted once, by the rank
+where it starts, re-split at the u32 limit exactly as the single-device
+encoder splits it.  The run-value histogram of the stitched runs is
+all-reduced for the VLE code book, the ranks' value bits and run counts are
+all-gathered for offsets, and each rank encodes its values at its bit phase;
+the archive is again byte-identical to the single-device one.
 
 Decompression comes in two forms.  ``decompress_sharded`` inverts
 ``compress_sharded`` with no collective (each rank still holds its own
@@ -101,6 +108,7 @@ class SlabResult:
     phase: int = 0        # bit phase of the slab's first bit inside bits[0]
     nbits: int = 0        # the slab's bits in the dense stream
     n_out: int = 0        # the slab's outlier records
+    rle: dict | None = None  # RLE+VLE: emitted run lengths, run offset, the slab's own runs
 
 
 class SlabOps:
@@ -118,7 +126,7 @@ class SlabOps:
         raise NotImplementedError
 
     def encode_at(self, codes, n: int, lengths, words, cap: int, maxlen: int, phase: int,
-                  bits: int):
+                  bits: int, sym_bytes: int | None = None):
         """-> uint8 slice of ceil((phase + bits) / 8) bytes."""
         raise NotImplementedError
 
@@ -128,6 +136,27 @@ class SlabOps:
 
     def to_tensor(self, x):
         """Object -> torch tensor on the collective's device (for all_reduce)."""
+        raise NotImplementedError
+
+    # -- RLE+VLE compress --
+    def rle_local(self, codes, n: int, max_run: int):
+        """Runs of the slab's symbols -> (values, lengths, R, boundary) where
+        boundary = (R, head value, head total, head entries, tail value, tail
+        total, tail entries); a maximal run split at max_run spans several
+        consecutive entries of one value."""
+        raise NotImplementedError
+
+    def rle_emit(self, values, lengths, a: int, b: int, group, max_run: int):
+        """Entries [a, b) followed by the re-split run `group` = (value,
+        total) (or nothing) -> (values u32, lengths u32, count)."""
+        raise NotImplementedError
+
+    def value_hist(self, values, n: int, cap: int):
+        """int64[cap] histogram of n run values (same device as values)."""
+        raise NotImplementedError
+
+    def rle_decode_local(self, values, lengths, runs: int, n: int, cap: int):
+        """The slab's symbols from its own (unstitched) runs."""
         raise NotImplementedError
 
     # -- decompress side (decompress_sharded) --
@@ -269,9 +298,116 @@ def decompress_archive_sharded(ops: SlabOps, arc, group=None, raw_host: bytes | 
     return y, (lo, hi), hdr
 
 
+def plan_rle_stitch(infos: list, max_run: int):
+    """Stitching plan of the slabs' local runs (identical on every rank).
+
+    infos[k] = (R, head value, head total, head entries, tail value, tail
+    total, tail entries) of rank k's local runs (R = 0: empty slab).  Returns
+    (keep, group, emitted): rank k keeps its local entries [keep[k][0],
+    keep[k][1]) and then emits group[k] = (value, total) re-split at max_run
+    (the maximal run that starts with its tail and may continue through the
+    following slabs), or nothing; emitted[k] is its entry count."""
+    world = len(infos)
+    keep = [(0, 0)] * world
+    group = [None] * world
+    cur = None  # open run crossing a boundary: [value, total, owner rank]
+    for k, (R, hv, ht, hc, tv, tt, tc) in enumerate(infos):
+        if R == 0:
+            continue
+        uniform = hc == R  # the whole slab is one maximal run
+        a = 0
+        if cur is not None and cur[0] == hv:
+            cur[1] += ht
+            a = hc
+            if uniform:
+                keep[k] = (R, R)
+                continue
+        elif cur is not None:
+            group[cur[2]] = (cur[0], cur[1])
+            cur = None
+        if cur is None and uniform:
+            cur = [hv, ht, k]
+            keep[k] = (0, 0)
+            continue
+        if cur is not None:
+            group[cur[2]] = (cur[0], cur[1])
+        cur = [tv, tt, k]
+        keep[k] = (a, R - tc)
+    if cur is not None:
+        group[cur[2]] = (cur[0], cur[1])
+    emitted = [(b - a) + (0 if g is None else -(-g[1] // max_run)) for (a, b), g in zip(keep, group)]
+    return keep, group, emitted
+
+
+def split_run(total: int, max_run: int) -> list[int]:
+    """P/rle.py:17-35: a run longer than max_run becomes max_run-long runs and a remainder."""
+    q, r = divmod(total, max_run)
+    return [max_run] * q + ([r] if r else [])
+
+
+def _boundary(hv, hl, tv, tl, r: int) -> tuple:
+    """Boundary tuple of a slab's runs from its first / last entries (a
+    split maximal run = consecutive entries of one value)."""
+    if r == 0:
+        return (0, 0, 0, 0, 0, 0, 0)
+    hc = 1
+    while hc < len(hv) and hv[hc] == hv[0]:
+        hc += 1
+    tc = 1
+    while tc < len(tv) and tv[len(tv) - 1 - tc] == tv[-1]:
+        tc += 1
+    if hc == len(hv) and len(hv) < r or tc == len(tv) and len(tv) < r:
+        raise NotImplementedError("a boundary run split into more than 64 entries")
+    return (r, int(hv[0]), int(hl[:hc].astype(np.int64).sum()), hc,
+            int(tv[-1]), int(tl[len(tl) - tc:].astype(np.int64).sum()), tc)
+
+
+def _compress_sharded_rle(ops, codes, n_local, n_out, recs, dims, lo, cap, meta, rank, world, group,
+                          device, max_run):
+    import torch
+    import torch.distributed as dist
+
+    if n_local:
+        vals, lens, r_k, info = ops.rle_local(codes, n_local, max_run)
+    else:
+        vals, lens, r_k, info = None, None, 0, (0, 0, 0, 0, 0, 0, 0)
+    mine = torch.tensor(list(info), dtype=torch.int64, device=device)
+    allv = [torch.zeros(7, dtype=torch.int64, device=device) for _ in range(world)]
+    dist.all_gather(allv, mine, group=group)
+    infos = [tuple(int(x) for x in v) for v in allv]
+    keep, grp, emitted = plan_rle_stitch(infos, max_run)
+    a, b = keep[rank]
+    e_k = emitted[rank]
+    ev, el = (ops.rle_emit(vals, lens, a, b, grp[rank], max_run) if e_k else (None, None))
+    # run-value histogram of the stitched runs -> the VLE code book
+    vh = ops.value_hist(ev, e_k, cap) if e_k else None
+    h = ops.to_tensor(vh) if vh is not None else torch.zeros(cap, dtype=torch.int64, device=device)
+    h = h.to(torch.int64).clone()
+    dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+    lengths, words, maxlen, total_vbits = ops.codebook(h, cap)
+    my_bits = ops.local_bits(vh, lengths) if vh is not None else 0
+    mv = torch.tensor([my_bits, n_out], dtype=torch.int64, device=device)
+    allb = [torch.zeros(2, dtype=torch.int64, device=device) for _ in range(world)]
+    dist.all_gather(allb, mv, group=group)
+    allb = [(int(v[0]), int(v[1])) for v in allb]
+    B_k = sum(v[0] for v in allb[:rank])
+    O_k = sum(v[1] for v in allb[:rank])
+    assert sum(v[0] for v in allb) == total_vbits
+    phase = B_k % 8
+    bits = ops.encode_at(ev, e_k, lengths, words, cap, maxlen, phase, my_bits, sym_bytes=4) \
+        if e_k else None
+    if n_out:
+        recs = ops.offset_records(recs, n_out, slab_index_offset(dims, lo))
+    meta.update(workflow="RLE_VLE", total_bits=total_vbits, total_out=sum(v[1] for v in allb),
+                lengths=lengths, maxlen=maxlen, n_runs=sum(emitted))
+    rle = dict(lens=el, run_start=sum(emitted[:rank]), n_runs=e_k, local=(vals, lens, r_k))
+    return SlabResult(rank, B_k // 8, bits, recs, O_k, meta, phase=phase, nbits=my_bits,
+                      n_out=n_out, rle=rle)
+
+
 def compress_sharded(ops: SlabOps, values, dims: Dims, vmin: float, vmax: float, eb: float,
                      eb_mode: str, cap: int, chunk: ChunkSpec, dtype_code: int, group=None,
-                     device=None) -> SlabResult:
+                     device=None, max_run: int = 0xFFFFFFFF) -> SlabResult:
     """Rank-local part of the sharded compress (every rank calls this with its slab)."""
     import torch
     import torch.distributed as dist
@@ -297,8 +433,11 @@ def compress_sharded(ops: SlabOps, values, dims: Dims, vmin: float, vmax: float,
     lengths, words, maxlen, total_bits = ops.codebook(h, cap)
     n = dims.count
     b = float(np.float64(total_bits) / np.float64(n))  # P/codebook.py:110-115
-    if b <= 1.09:
-        raise NotImplementedError("sharded RLE/RLE_VLE: use the gathered path")
+    meta = dict(dims=dims, chunk=chunk, cap=cap, eb=eb, eb_mode=eb_mode, vmin=vmin, vmax=vmax,
+                dtype_code=dtype_code, workflow="HUFFMAN")
+    if b <= 1.09:  # P/smoothness.py:111-136 -> RLE_VLE
+        return _compress_sharded_rle(ops, codes, n_local, n_out, recs, dims, lo, cap, meta, rank,
+                                     world, group, h.device, max_run)
     # (2) all-gather of (bits, outliers)
     my_bits = ops.local_bits(hist, lengths) if hist is not None else 0
     mine = torch.tensor([my_bits, n_out], dtype=torch.int64, device=h.device)
@@ -315,9 +454,7 @@ def compress_sharded(ops: SlabOps, values, dims: Dims, vmin: float, vmax: float,
         if n_local else None
     if n_out:
         recs = ops.offset_records(recs, n_out, slab_index_offset(dims, lo))
-    meta = dict(dims=dims, chunk=chunk, cap=cap, eb=eb, eb_mode=eb_mode, vmin=vmin, vmax=vmax,
-                dtype_code=dtype_code, total_bits=total_bits, total_out=total_out,
-                lengths=lengths, maxlen=maxlen)
+    meta.update(total_bits=total_bits, total_out=total_out, lengths=lengths, maxlen=maxlen)
     return SlabResult(rank, B_k // 8, bits, recs, O_k, meta, phase=phase, nbits=my_bits, n_out=n_out)
 
 
@@ -341,7 +478,12 @@ def decompress_sharded(ops: SlabOps, res: SlabResult, group=None):
         return None
     sd = slab_dims(dims, lo, hi)
     eb_abs = _resolve_eb(m["eb_mode"], m["eb"], m["vmin"], m["vmax"])
-    codes = ops.decode_at(res.bits, res.phase, res.nbits, sd.count, m["lengths"], cap, m["maxlen"])
+    if res.rle is not None:  # the slab's own runs (before stitching) decode exactly its symbols
+        vals, lens, r_k = res.rle["local"]
+        codes = ops.rle_decode_local(vals, lens, r_k, sd.count, cap)
+    else:
+        codes = ops.decode_at(res.bits, res.phase, res.nbits, sd.count, m["lengths"], cap,
+                              m["maxlen"])
     recs = ops.local_records(res.records, res.n_out, slab_index_offset(dims, lo)) if res.n_out \
         else None
     return ops.reconstruct(codes, sd, chunk, eb_abs, cap, recs, res.n_out, m["dtype_code"])
@@ -367,13 +509,25 @@ def assemble(results: list[SlabResult], lengths_bytes: bytes) -> bytes:
         if r.records is not None and len(r.records):
             rb = np.asarray(r.records, np.uint8)
             recs[16 * r.record_start: 16 * r.record_start + len(rb)] = rb
-    sym = struct.pack("<QQ", total_bits, dims.count) + data.tobytes()
+    if m.get("workflow") == "RLE_VLE":
+        n_runs = m["n_runs"]
+        lens = np.zeros(n_runs, np.uint32)
+        for r in results:
+            if r.rle is not None and r.rle["n_runs"]:
+                a = r.rle["run_start"]
+                lens[a: a + r.rle["n_runs"]] = np.asarray(r.rle["lens"]).view(np.uint32)[: r.rle["n_runs"]]
+        # P/pipeline.py:158-221: [runs][bit_len][count = runs][value bits][lengths]
+        sym = struct.pack("<QQQ", n_runs, total_bits, n_runs) + data.tobytes() + lens.tobytes()
+        wf = 2
+    else:
+        sym = struct.pack("<QQ", total_bits, dims.count) + data.tobytes()
+        wf = 0
     cb_off = _SECTION_BASE
     sym_off = (cb_off + cap + 7) & ~7
     out_off = (sym_off + len(sym) + 7) & ~7
     hdr = _HEADER.pack(MAGIC, 1, m["dtype_code"], dims.ndim, dims.nx, dims.ny, dims.nz,
                        chunk.cx, chunk.cy, chunk.cz, 1 if m["eb_mode"] == "rel" else 0, m["eb"],
-                       m["vmin"], m["vmax"], cap, 0, dims.count, total_out, cb_off, cap,
+                       m["vmin"], m["vmax"], cap, wf, dims.count, total_out, cb_off, cap,
                        sym_off, len(sym), out_off, 16 * total_out)
     blob = bytearray(out_off + 16 * total_out)
     blob[: len(hdr)] = hdr
@@ -387,10 +541,15 @@ def gather_results(res: SlabResult, group=None) -> list[SlabResult] | None:
     """Gather every rank's slice to rank 0 (outside the timed region)."""
     import torch.distributed as dist
 
+    rle = None
+    if res.rle is not None:
+        rle = dict(run_start=res.rle["run_start"], n_runs=res.rle["n_runs"],
+                   lens=None if res.rle["lens"] is None else _host_bytes(res.rle["lens"]))
     host = SlabResult(res.rank, res.byte_start,
                       None if res.bits is None else _host_bytes(res.bits),
                       None if res.records is None else _host_bytes(res.records),
-                      res.record_start, {k: v for k, v in res.meta.items() if k != "lengths"})
+                      res.record_start, {k: v for k, v in res.meta.items() if k != "lengths"},
+                      rle=rle)
     out = [None] * dist.get_world_size(group) if dist.get_rank(group) == 0 else None
     dist.gather_object(host, out, dst=0, group=group)
     return out
@@ -466,22 +625,94 @@ class DeviceSlabOps(SlabOps):
 
         return int((hist.to(torch.int64) * lengths.to(torch.int64)).sum().item())
 
-    def encode_at(self, codes, n, lengths, words, cap, maxlen, phase, bits):
+    def encode_at(self, codes, n, lengths, words, cap, maxlen, phase, bits, sym_bytes=None):
         from . import _native as N
         from .pipeline import code_bytes_for
 
         L = N.lib()
+        sb = sym_bytes or code_bytes_for(cap)
         nbytes = (phase + bits + 7) // 8
         out = N.empty_bytes(nbytes + 4, self.device)
         out[: nbytes].zero_()
         st = N.empty_bytes(N.STATUS_BYTES, self.device)
         es = L.lzb_huff_encode_scratch_bytes(n)
         scr = N.empty_bytes(es, self.device)
-        N.check_rc(L.lzb_huff_encode_at(codes.data_ptr(), code_bytes_for(cap), n,
+        N.check_rc(L.lzb_huff_encode_at(codes.data_ptr(), sb, n,
                                         lengths.data_ptr(), words.data_ptr(), cap, maxlen, phase,
                                         out.data_ptr(), nbytes, st.data_ptr(), scr.data_ptr(), es,
                                         N.stream_ptr()), "huff_encode_at")
         return out[:nbytes]
+
+    def rle_local(self, codes, n, max_run):
+        import torch
+
+        from . import _native as N
+
+        L = N.lib()
+        cb = codes.numel() // n  # code bytes (the quantize output is n * code_bytes)
+        st = N.empty_bytes(N.STATUS_BYTES, self.device)
+        N.check_rc(L.lzb_count_runs(codes.data_ptr(), cb, n, st.data_ptr(), N.stream_ptr()), "count_runs")
+        (sc,) = N.read_status(st)
+        N.raise_for(sc, "count_runs")
+        cap_runs = sc.u[0] + (n // max_run + 1 if n > max_run else 0)
+        vals = torch.empty(max(cap_runs, 1), dtype=torch.int32, device=self.device)
+        lens = torch.empty(max(cap_runs, 1), dtype=torch.int32, device=self.device)
+        rs = L.lzb_rle_encode_scratch_bytes_runs(n, cap_runs)
+        scr = N.empty_bytes(rs, self.device)
+        N.check_rc(L.lzb_rle_encode(codes.data_ptr(), cb, n, vals.data_ptr(), lens.data_ptr(), cap_runs,
+                                    max_run, st.data_ptr(), scr.data_ptr(), rs, N.stream_ptr()),
+                   "rle_encode")
+        (sr,) = N.read_status(st)
+        N.raise_for(sr, "rle_encode")
+        r = sr.u[0]
+        vals, lens = vals[:r], lens[:r]
+        k = min(r, 64)
+        hv_ = vals[:k].cpu().numpy().view(np.uint32)
+        hl_ = lens[:k].cpu().numpy().view(np.uint32)
+        tv_ = vals[r - k:].cpu().numpy().view(np.uint32)
+        tl_ = lens[r - k:].cpu().numpy().view(np.uint32)
+        return vals, lens, r, _boundary(hv_, hl_, tv_, tl_, r)
+
+    def rle_emit(self, values, lengths, a, b, group, max_run):
+        import torch
+
+        parts_v, parts_l = [values[a:b]], [lengths[a:b]]
+        if group is not None:
+            sp = split_run(group[1], max_run)
+            parts_v.append(torch.full((len(sp),), group[0], dtype=torch.int32, device=self.device))
+            parts_l.append(torch.tensor(np.array(sp, np.uint32).view(np.int32), device=self.device))
+        return torch.cat(parts_v).contiguous(), torch.cat(parts_l).contiguous()
+
+    def value_hist(self, values, n, cap):
+        import torch
+
+        from . import _native as N
+
+        L = N.lib()
+        h = torch.empty(cap, dtype=torch.int64, device=self.device)
+        st = N.empty_bytes(N.STATUS_BYTES, self.device)
+        N.check_rc(L.lzb_histogram(values.data_ptr(), 4, n, cap, h.data_ptr(), st.data_ptr(),
+                                   N.stream_ptr()), "histogram")
+        (s,) = N.read_status(st)
+        N.raise_for(s, "histogram")
+        return h
+
+    def rle_decode_local(self, values, lengths, runs, n, cap):
+        import torch
+
+        from . import _native as N
+        from .pipeline import code_bytes_for
+
+        L = N.lib()
+        cb = code_bytes_for(cap)
+        sym = torch.empty(n * cb, dtype=torch.uint8, device=self.device)
+        st = N.empty_bytes(N.STATUS_BYTES, self.device)
+        rs = L.lzb_rle_decode_scratch_bytes(runs)
+        scr = N.empty_bytes(rs, self.device)
+        N.check_rc(L.lzb_rle_decode(values.data_ptr(), lengths.data_ptr(), runs, cap, sym.data_ptr(), cb,
+                                    n, st.data_ptr(), scr.data_ptr(), rs, N.stream_ptr()), "rle_decode")
+        self._decode_status = st
+        return sym
 
     def offset_records(self, records, n_out, offset):
         import torch

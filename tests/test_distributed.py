@@ -41,12 +41,34 @@ class OracleSlabOps:
     def local_bits(self, hist, lengths):
         return int((np.asarray(hist) * lengths.astype(np.int64)).sum())
 
-    def encode_at(self, codes, n, lengths, words, cap, maxlen, phase, bits):
+    def encode_at(self, codes, n, lengths, words, cap, maxlen, phase, bits, sym_bytes=None):
         b, _, data = O.huff_encode(codes, lengths, words)
         assert b == bits
         arr = np.unpackbits(np.frombuffer(data, np.uint8))[:bits]
         arr = np.concatenate([np.zeros(phase, np.uint8), arr])
         return np.packbits(arr)
+
+    def rle_local(self, codes, n, max_run):
+        from paper_2105_12912_b200 import distributed as D
+
+        v, ln = O.rle_encode(np.asarray(codes), max_run)
+        return v, ln, len(v), D._boundary(v[:64], ln[:64], v[-64:], ln[-64:], len(v))
+
+    def rle_emit(self, values, lengths, a, b, group, max_run):
+        from paper_2105_12912_b200 import distributed as D
+
+        v, ln = list(values[a:b]), list(lengths[a:b])
+        if group is not None:
+            sp = D.split_run(group[1], max_run)
+            v += [group[0]] * len(sp)
+            ln += sp
+        return np.array(v, np.uint32), np.array(ln, np.uint32)
+
+    def value_hist(self, values, n, cap):
+        return O.histogram(np.asarray(values, np.uint32), cap)
+
+    def rle_decode_local(self, values, lengths, runs, n, cap):
+        return O.rle_decode(values, lengths, n)
 
     def offset_records(self, records, n_out, offset):
         r = records.view([("i", "<u8"), ("d", "<i8")]).copy()
@@ -306,3 +328,106 @@ def test_slab_bounds_cover_whole_chunk_layers():
                 assert lo == prev and (lo % c == 0 or lo == n) and (hi % c == 0 or hi == n)
                 prev = hi
             assert prev == n
+
+
+def _rle_worker(rank, world, port, case, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2105_12912_b200 import ChunkSpec, Dims
+        from paper_2105_12912_b200 import distributed as D
+
+        vals, shape, eb, ref_arc = case
+        dims = Dims.of(*shape[::-1])
+        chunk = ChunkSpec.default_for(dims.ndim)
+        lo, hi = D.slab_bounds(dims, chunk, rank, world)
+        full = vals.reshape(shape)
+        slab = full[lo:hi].reshape(-1) if dims.ndim > 1 else full[lo:hi]
+        res = D.compress_sharded(OracleSlabOps(), slab, dims, float(vals.min()), float(vals.max()), eb,
+                                 "rel", 1024, chunk, 0)
+        assert res.meta["workflow"] == "RLE_VLE"
+        y = D.decompress_sharded(OracleSlabOps(), res)
+        ref = O.decompress(ref_arc)[0].reshape(shape)
+        want = ref[lo:hi].reshape(-1) if dims.ndim > 1 else ref[lo:hi]
+        if hi > lo:
+            assert y is not None and np.array_equal(y, want), rank
+        lens = np.frombuffer(ref_arc, np.uint8, 1024, O.parse_header(ref_arc)["codebook"][0]).copy() \
+            if rank == 0 else None
+        got = D.gather_results(res)
+        if rank == 0:
+            q.put(D.assemble(got, lens.tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("shape", [(32, 24, 40), (256, 100), (20000,)])
+def test_sharded_rle_vle_archive_is_byte_identical(shape, world):
+    """Auto selection picks RLE+VLE (long runs of the radius code); runs that
+    cross slab boundaries are stitched so the archive equals the
+    single-process one byte for byte."""
+    import torch.multiprocessing as mp
+
+    rng = np.random.default_rng(7)
+    vals = np.zeros(int(np.prod(shape)), np.float32)
+    # a few blocks of noise in a constant sea: long runs spanning slab boundaries
+    for _ in range(3):
+        a = int(rng.integers(0, vals.size - 10))
+        vals[a: a + 10] = rng.normal(0, 1, 10).astype(np.float32)
+    vals[0] = 4.0  # non-degenerate range
+    eb = 1e-3
+    dims = tuple(list(shape[::-1]) + [1] * (3 - len(shape))) + (len(shape),)
+    ref = O.compress(vals, dims, float(vals.min()), float(vals.max()), eb)
+    assert O.parse_header(ref)["workflow"] == 2  # RLE_VLE
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rle_worker, args=(r, world, port, (vals, shape, eb, ref), q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == ref
+
+
+def test_rle_stitch_plan_matches_global_runs():
+    """Random streams with long runs (and a tiny max_run so splits and merged
+    splits happen), cut into slabs at random points incl. empty and
+    single-run slabs: local runs + the stitching plan == the global runs."""
+    from paper_2105_12912_b200 import distributed as D
+
+    rng = np.random.default_rng(11)
+    for case in range(300):
+        n = int(rng.integers(1, 400))
+        vals = np.repeat(rng.integers(0, 3, 60), rng.integers(1, 40, 60))[:n].astype(np.uint32)
+        n = len(vals)
+        max_run = int(rng.choice([3, 7, 1000]))
+        world = int(rng.integers(1, 6))
+        cuts = np.sort(rng.integers(0, n + 1, world - 1))
+        bounds = [0] + cuts.tolist() + [n]
+        infos, local = [], []
+        for k in range(world):
+            sl = vals[bounds[k]: bounds[k + 1]]
+            v, ln = O.rle_encode(sl, max_run) if len(sl) else (np.empty(0, np.uint32),) * 2
+            local.append((v, ln))
+            infos.append(D._boundary(v, ln, v, ln, len(v)) if len(v) else (0,) * 7)
+        keep, group, emitted = D.plan_rle_stitch(infos, max_run)
+        ev, el = [], []
+        for k in range(world):
+            v, ln = local[k]
+            a, b = keep[k]
+            ev += list(v[a:b])
+            el += list(ln[a:b])
+            if group[k] is not None:
+                sp = D.split_run(group[k][1], max_run)
+                ev += [group[k][0]] * len(sp)
+                el += sp
+            assert emitted[k] == (b - a) + (len(D.split_run(group[k][1], max_run)) if group[k] else 0)
+        gv, gl = O.rle_encode(vals, max_run)
+        assert ev == list(gv) and el == list(gl), case
