@@ -196,8 +196,9 @@ class SlabOps:
         """(slab-local records, count) of the outliers with lo <= index < hi."""
         raise NotImplementedError
 
-    def decompress_full(self, arc, hdr):
-        """Whole-field values (replicated fallback for the run-length workflows)."""
+    def rle_slab_codes(self, arc, hdr, s_lo: int, s_hi: int):
+        """Symbols [s_lo, s_hi) of a run-length archive (RLE / RLE+VLE): the
+        run section is validated whole, only the overlapping runs expanded."""
         raise NotImplementedError
 
 
@@ -266,9 +267,16 @@ def decompress_archive_sharded(ops: SlabOps, arc, group=None, raw_host: bytes | 
     lo, hi = slab_bounds(dims, chunk, rank, world)
     sd = slab_dims(dims, lo, hi) if hi > lo else None
     if hdr.workflow is not Workflow.HUFFMAN:
-        y = ops.decompress_full(arc, hdr)
+        # the run section is small and read by every rank; each rank expands
+        # only the runs that overlap its slab's symbols (no exchange)
+        if sd is None:
+            return None, (lo, hi), hdr
         a, b = slab_index_offset(dims, lo), slab_index_offset(dims, hi)
-        return (y[a:b] if sd is not None else None), (lo, hi), hdr
+        codes = ops.rle_slab_codes(arc, hdr, a, b)
+        recs, n_out = ops.slab_records(arc, hdr, a, b)
+        y = ops.reconstruct(codes, sd, chunk, hdr.eb_abs, cap, recs, n_out,
+                            0 if hdr.dtype == "f32" else 1)
+        return y, (lo, hi), hdr
     bit_len, count, maxlen = ops.stream_info(arc, hdr)
     ranges = stream_ranges(bit_len, world)
     r_lo, r_hi = ranges[rank]
@@ -873,7 +881,67 @@ class DeviceSlabOps(SlabOps):
             return None, 0
         return self.local_records(r[a:z].reshape(-1).view(torch.uint8), z - a, idx_lo), z - a
 
-    def decompress_full(self, arc, hdr):
-        from .pipeline import decompress_device
+    def rle_slab_codes(self, arc, hdr, s_lo, s_hi):
+        import torch
 
-        return decompress_device(arc)[0]
+        from . import _native as N
+        from .errors import CorruptArchiveError
+        from .pipeline import Workflow, _validate_lengths_host, code_bytes_for
+
+        L = N.lib()
+        cap, n = hdr.cap, hdr.count
+        sym_off, sym_len = hdr.symbols
+        if sym_len < 8:
+            raise CorruptArchiveError("run section shorter than its count")
+        (R,) = struct.unpack("<Q", self._host(arc, sym_off, sym_off + 8))
+        base = arc.data_ptr()
+        st = N.empty_bytes(N.STATUS_BYTES, self.device)
+        if hdr.workflow is Workflow.RLE:
+            if sym_len != 8 + 8 * R:
+                raise CorruptArchiveError("run section size mismatch")
+            vals = arc[sym_off + 8: sym_off + 8 + 4 * R].view(torch.int32)
+            lo_len = sym_off + 8 + 4 * R
+        else:
+            if sym_len < 24:
+                raise CorruptArchiveError("bit stream shorter than its header")
+            bit_len, count = struct.unpack("<QQ", self._host(arc, sym_off + 8, sym_off + 24))
+            nbytes = (bit_len + 7) // 8
+            if sym_len - 24 < nbytes:
+                raise CorruptArchiveError("bit stream data truncated")
+            if count != R or sym_len != 8 + 16 + nbytes + 4 * R:
+                raise CorruptArchiveError("run section size mismatch")
+            cb = np.frombuffer(self._host(arc, hdr.codebook[0], sum(hdr.codebook)), np.uint8)
+            maxlen = _validate_lengths_host(cb)
+            vals = torch.empty(max(R, 1), dtype=torch.int32, device=self.device)
+            ds = L.lzb_huff_decode_scratch_bytes(bit_len, maxlen, cap)
+            scr = N.empty_bytes(ds, self.device)
+            N.check_rc(L.lzb_huff_decode(base + sym_off + 24, bit_len, R, base + hdr.codebook[0], cap,
+                                         maxlen, vals.data_ptr(), 4, st.data_ptr(), scr.data_ptr(), ds,
+                                         N.stream_ptr()), "huff_decode")
+            (sd,) = N.read_status(st)
+            N.raise_for(sd, "decode", "bit stream does not decode to its declared symbols")
+            lo_len = sym_off + 24 + nbytes
+        if R == 0:
+            raise CorruptArchiveError("run section does not decode to the grid")
+        lens = arc[lo_len: lo_len + 4 * R].clone().view(torch.int32)  # unaligned in RLE+VLE
+        l64 = lens.to(torch.int64) & 0xFFFFFFFF
+        cum = torch.cumsum(l64, 0)
+        bad = torch.stack([(l64 == 0).any().to(torch.int64), cum[-1]]).cpu()
+        if int(bad[0]) or int(bad[1]) != n:  # P/rle.py:38-44
+            raise CorruptArchiveError("run section does not decode to the grid")
+        q = torch.tensor([s_lo, s_hi - 1], dtype=torch.int64, device=self.device)
+        ra, rb = (int(v) for v in torch.searchsorted(cum, q, right=True).cpu())
+        sub_v = vals[ra: rb + 1].contiguous()
+        sub_l = lens[ra: rb + 1].clone()
+        edges = torch.stack([cum[ra] - l64[ra], cum[rb]]).cpu()
+        first_start, last_end = int(edges[0]), int(edges[1])
+        def as_i32(v: int) -> int:  # u32 run length in the int32 tensor's bit pattern
+            return int(np.uint32(v).view(np.int32))
+
+        cum_ra = int(edges[0]) + int(l64[ra])
+        if ra == rb:
+            sub_l[0] = as_i32(s_hi - s_lo)
+        else:
+            sub_l[0] = as_i32(cum_ra - s_lo)
+            sub_l[-1] = as_i32(int(l64[rb]) - (last_end - s_hi))
+        return self.rle_decode_local(sub_v, sub_l, rb - ra + 1, s_hi - s_lo, cap)

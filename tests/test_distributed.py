@@ -168,8 +168,8 @@ class OracleSlabOps:
             return None, 0
         return self.local_records(sel.view(np.uint8), len(sel), idx_lo), len(sel)
 
-    def decompress_full(self, arc, hdr):
-        return O.decompress(arc)[0]
+    def rle_slab_codes(self, arc, hdr, s_lo, s_hi):
+        return O.decode_symbols(arc, O.parse_header(arc))[s_lo:s_hi]
 
 
 def _worker(rank, world, port, case, q):

@@ -132,14 +132,19 @@ def _worker(rank, world, port, arc_bytes, q):
         dist.destroy_process_group()
 
 
-def test_sharded_decompress_of_one_archive_same_device(cuda):
+@pytest.mark.parametrize("workflow", [None, "rle", "rlevle"])
+def test_sharded_decompress_of_one_archive_same_device(cuda, workflow):
     import torch.multiprocessing as mp
 
     from helpers import smooth
 
     shape = (48, 40, 64)
     vals = smooth(shape).reshape(-1).astype(np.float32)
-    arc = O.compress(vals, (64, 40, 48, 3), float(vals.min()), float(vals.max()), 1e-4)
+    if workflow is not None:
+        vals = np.round(vals / 8).astype(np.float32)  # long runs
+    arc = O.compress(vals, (64, 40, 48, 3), float(vals.min()), float(vals.max()),
+                     1e-4 if workflow is None else 1e-2, workflow=workflow)
+    assert O.parse_header(arc)["workflow"] == {None: 0, "rle": 1, "rlevle": 2}[workflow]
     ref = O.decompress(arc)[0].reshape(shape)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
