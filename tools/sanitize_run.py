@@ -21,3 +21,11 @@ for vals, eb, kw in cases:
     h = lzb.parse_header(blob)
     err = np.abs(out.values.astype(np.float64) - vals.reshape(-1).astype(np.float64)).max()
     print(vals.shape, h.workflow.name, len(blob), "ok" if err <= h.eb_abs * 1.0001 + 1e-3 else "BOUND!")
+# bit-range decode (multi-GPU single-archive decompress), 3 ranges
+from test_gpu_range_decode import _range_decode_all  # noqa: E402
+
+stream = rng.choice(64, size=40_000, p=np.r_[np.full(8, 0.1), np.full(56, 0.2 / 56)]).astype(np.uint32)
+book = lzb.Codebook.from_counts(np.bincount(stream, minlength=64))
+bs = lzb.encode(stream, book)
+got, _ = _range_decode_all(bs, book, 64, 3)
+print("range decode", "ok" if np.array_equal(got, stream) else "MISMATCH")
