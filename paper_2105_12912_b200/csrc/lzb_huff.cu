@@ -253,22 +253,21 @@ __global__ void k_huff_fixup(EncParams p) {
 }
 
 // ----------------------------------------------------------------------------
-// K3 fast path (u16 symbols, code words <= 32 bits, table in shared memory):
-// warp-independent tiles, no CTA barriers, few shared atomics.  A warp tile
-// is 1024 symbols; lane l owns the 32 consecutive symbols [32 l, 32 l + 32),
-// i.e. the four 16-byte pieces 4l..4l+3 of the cp.async stage (stored
-// XOR-swizzled so the lane reads are conflict-free).  Tiles are statically
-// assigned (tile t to warp t mod NW of a persistent grid), so the next tile
-// is prefetched while the current one is packed.  Per tile:
-//   pass 1: bit count per lane (length table) -> warp scan -> the tile's
-//           aggregate is published for the look-back right away;
-//   pass 2: each lane packs its code words into a 32-bit accumulator and
-//           stores every completed word; only its first word (shared with
-//           the previous lane when it starts mid-word) and its last partial
-//           word go through red.shared.or;
-//   resolve the tile's global bit offset (decoupled look-back, usually ready),
-//   store the full words with the bit phase applied and keep the <= 2 partial
-//   boundary words (head / tail) for k_huff_fixup_w.
+// K3 fast path (u16 symbols, code words <= 32 bits, table in shared memory).
+// A warp tile is 1024 symbols; lane l owns the 32 consecutive symbols
+// [32 l, 32 l + 32), i.e. the four 16-byte pieces 4l..4l+3.  Three kernels:
+//   k_huff_count_w: bit count of every tile and of every lane's 32 symbols
+//                   (order-independent coalesced loads; the DataError checks);
+//   k_huff_scan_w:  single-pass look-back scan -> u64 bit offset per tile;
+//   k_huff_encode_w: persistent warps (tile t to warp t mod NW, 4 CTAs/SM),
+//                   the next tile prefetched by cp.async into the warp's one
+//                   XOR-swizzled stage as soon as the lanes hold the current
+//                   one in registers; each lane packs its code words into a
+//                   32-bit accumulator and stores every word it completes
+//                   (its partial first / last word via red.shared.or), then
+//                   the warp stores the tile's words big-endian with the
+//                   tile's bit phase applied and keeps the <= 2 partial
+//                   boundary words (head / tail) for k_huff_fixup_w.
 // ----------------------------------------------------------------------------
 constexpr int kWSyms = 32;                 // symbols per lane
 constexpr int kWTile = 32 * kWSyms;        // 1024 symbols per warp tile

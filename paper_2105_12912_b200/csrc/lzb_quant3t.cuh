@@ -4,17 +4,21 @@
 // and to k_quantize3d8; see lzb_fast3d.cuh for the per-chunk register layout.
 //
 // A super tile is 16 consecutive chunks along x = a 128x8x8 f32 box (32 KB,
-// 512-byte row segments; two outlier tiles of 8 chunks).  Each
-// persistent CTA owns tiles b, b + G, b + 2G, ... and streams them through a
-// ring of kT1Stages shared-memory stages with TMA (two 32x8x8 boxes per
-// tile, SWIZZLE_128B so the warps' row reads are bank-conflict free),
-// completion tracked by one mbarrier per stage.  The 8 warps of the CTA each
-// take one chunk of the tile: prequant (f32 double-single fast path, exact
-// f64 division only for the rare element near a rounding tie), Lorenzo
-// deltas in registers/shuffles, codes stored as 16-byte rows straight into
-// the chunk-major stream, histogram into per-lane shared columns.  Outlier
-// ranks across the tile's chunks come from a per-tile count exchange; the
-// CTA barrier that exchanges them also frees the stage for the next TMA.
+// 512-byte row segments; two outlier tiles of 8 chunks).  Each persistent
+// CTA (16 warps, one per SM) owns super tiles b, b + G, b + 2G, ... and
+// streams them through a ring of kT1Stages shared-memory stages with TMA
+// (four 32x8x8 boxes per tile, SWIZZLE_128B so the warps' 16-byte row reads
+// are bank-conflict free), completion tracked by one mbarrier per stage.
+// Each warp takes one chunk of the tile: prequant (f32 double-single fast
+// path, exact f64 division only for the rare element near a rounding tie),
+// Lorenzo deltas in registers/shuffles, codes stored as 16-byte rows straight
+// into the chunk-major stream, histogram into per-lane shared columns.  No
+// CTA barrier per tile: warps publish their outlier counts / first records
+// in the stage's slots and bump a per-stage counter; the last warp to
+// release a stage publishes the two outlier tiles and issues its TMA refill.
+// (Measured alternatives that were slower on C5q: 2 or 4 stages, 8-chunk
+// tiles with 2 CTAs/SM, releasing the stage right after the shared-memory
+// reads -- more TMA traffic in flight costs more than it hides.)
 #pragma once
 
 #include <cudaTypedefs.h>
