@@ -159,3 +159,41 @@ def test_sharded_decompress_of_one_archive_same_device(cuda, workflow):
         assert p.exitcode == 0
     for rank, lo, hi, y in got:
         assert np.array_equal(y, ref[lo:hi].reshape(-1)), rank
+
+
+def test_range_decode_agrees_with_whole_stream_decode_on_damaged_streams(cuda):
+    """Flipped bits, a shortened bit length and a wrong symbol count: the
+    chained ranges either fail (CorruptArchiveError / a non-zero status)
+    exactly when the whole-stream decoder fails, or return its symbols."""
+    import paper_2105_12912_b200 as lzb
+    from paper_2105_12912_b200.errors import CorruptArchiveError
+    from paper_2105_12912_b200.huffman import BitStream
+
+    rng = np.random.default_rng(99)
+    g = np.array([int(1e6 * 0.6 ** abs(i - 20)) + 1 for i in range(40)], np.int64)
+    stream = rng.choice(40, size=120_000, p=g / g.sum()).astype(np.uint32)
+    book = lzb.Codebook.from_counts(np.bincount(stream, minlength=64))
+    bs = lzb.encode(stream, book)
+    cases = []
+    for _ in range(6):
+        d = np.asarray(bs.data, np.uint8).copy()
+        k = int(rng.integers(0, bs.bit_len))
+        d[k // 8] ^= np.uint8(0x80 >> (k % 8))
+        cases.append(BitStream(bs.bit_len, bs.count, d))
+    cases.append(BitStream(bs.bit_len - 3, bs.count, np.asarray(bs.data, np.uint8)))
+    cases.append(BitStream(bs.bit_len, bs.count + 1, np.asarray(bs.data, np.uint8)))
+    cases.append(BitStream(bs.bit_len, bs.count - 1, np.asarray(bs.data, np.uint8)))
+    for i, c in enumerate(cases):
+        try:
+            want = lzb.decode(c, book)
+        except CorruptArchiveError:
+            want = None
+        for world in (2, 5):
+            try:
+                got, _ = _range_decode_all(c, book, 64, world)
+            except (CorruptArchiveError, AssertionError):
+                got = None
+            if want is None:
+                assert got is None, (i, world)
+            else:
+                assert got is not None and np.array_equal(got, want), (i, world)
