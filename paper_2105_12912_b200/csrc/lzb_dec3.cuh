@@ -192,25 +192,58 @@ __device__ __forceinline__ bool d3_bulk(const uint32_t *stg, uint32_t head, cons
     return true;
 }
 
-// Single code words from pos until pos >= mstop (returns 0) or pos is a start
-// recorded in (bm0, bm1) relative to b (returns 1), or an invalid / truncated
-// code word (returns 2).  cnt counts the code words walked.
-__device__ __forceinline__ int d3_walk(const uint32_t *stg, uint32_t head, const uint8_t *s_l1,
-                                       const DecCanon *tab, uint32_t &pos, uint32_t b, uint32_t mstop,
-                                       uint32_t endrel, uint64_t bm0, uint64_t bm1, uint32_t &cnt) {
+// bits q .. q+31 of the 128-bit start map (zero past bit 127)
+__device__ __forceinline__ uint32_t bm2_win(uint64_t b0, uint64_t b1, uint32_t q) {
+    uint64_t v;
+    if (q < 64) v = (b0 >> q) | (q ? (b1 << (64 - q)) : 0ull);
+    else if (q < 128) v = b1 >> (q - 64);
+    else v = 0;
+    return (uint32_t)v;
+}
+
+// Walk code words from pos until a code-word boundary is at / after mstop
+// (returns 0) or is a start recorded in (bm0, bm1) relative to b (returns
+// 1), or an invalid / truncated code word (returns 2); cnt counts the code
+// words walked.  Up to 12 code words per boundary-LUT lookup; single code
+// words for code words longer than the LUT and near the stream end.
+__device__ __forceinline__ int d3_walk_lut(const uint32_t *stg, uint32_t head, const uint32_t *s_b,
+                                           const uint8_t *s_l1, const DecCanon *tab, uint32_t &pos,
+                                           uint32_t b, uint32_t mstop, uint32_t endrel, uint64_t bm0,
+                                           uint64_t bm1, uint32_t &cnt) {
     if (pos >= mstop) return 0;
     if (bm2_test(bm0, bm1, pos - b)) return 1;
     SWin r;
     r.init(stg, pos + head);
     while (true) {
-        const uint32_t L = d3_len(s_l1, tab, r);
-        if (L == 0 || pos + L > endrel) return 2;
-        pos += L;
-        cnt++;
-        if (pos >= mstop) return 0;
-        if (bm2_test(bm0, bm1, pos - b)) return 1;
-        r.skip(L);
+        const uint32_t e = s_b[r.peek12()];
+        const uint32_t n = e & 15u, used = (e >> 4) & 15u;
+        if (n == 0 || pos + (uint32_t)kLutBits > endrel) {
+            const uint32_t L = d3_len(s_l1, tab, r);
+            if (L == 0 || pos + L > endrel) return 2;
+            pos += L;
+            cnt++;
+            if (pos >= mstop) return 0;
+            if (bm2_test(bm0, bm1, pos - b)) return 1;
+            r.skip(L);
+            continue;
+        }
+        // boundary at pos + j  <->  bit j - 1 (1 <= j <= used)
+        const uint32_t ends = ((e >> 8) >> 1) | (1u << (used - 1));
+        uint32_t hit = ends & bm2_win(bm0, bm1, pos + 1 - b);
+        const uint32_t dm = mstop - pos;  // >= 1
+        if (dm <= used) hit |= ends & ~((1u << (dm - 1)) - 1u);
+        if (hit) {
+            const uint32_t j = __ffs(hit);
+            cnt += __popc(ends & ((1u << j) - 1u));
+            pos += j;
+            return pos >= mstop ? 0 : 1;
+        }
+        pos += used;
+        cnt += n;
+        r.skip(used);
     }
+}
+
 }
 
 // per-microblock data shared by the lanes of a warp in phase C
@@ -276,7 +309,7 @@ __global__ void __launch_bounds__(kD3Warps * 32) k_dec_maps3(DecParams p) {
             if (need) {
                 uint32_t pos = px, k = 0, nx, nc;
                 bool lk;
-                const int w = d3_walk(stg, p.head, s_l1, tab, pos, b, mstop, endrel, bm0, bm1, k);
+                const int w = d3_walk_lut(stg, p.head, s_b, s_l1, tab, pos, b, mstop, endrel, bm0, bm1, k);
                 if (w == 2) {
                     lk = false;
                     nx = pos;
@@ -355,7 +388,7 @@ __global__ void __launch_bounds__(kD3Warps * 32) k_dec_maps3(DecParams p) {
                         break;
                     }
                     const uint32_t bk = k * kMB, ms = min(bk + kMB, stop);
-                    const int w = d3_walk(stg, p.head, s_l1, tab, pos, bk, ms, endrel, m.bm0, m.bm1, c);
+                    const int w = d3_walk_lut(stg, p.head, s_b, s_l1, tab, pos, bk, ms, endrel, m.bm0, m.bm1, c);
                     if (w == 2) break;
                     if (w == 1) {  // joined microblock k's phase-0 path
                         if (!m.ok0) break;
