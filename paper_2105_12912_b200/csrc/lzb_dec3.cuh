@@ -244,8 +244,6 @@ __device__ __forceinline__ int d3_walk_lut(const uint32_t *stg, uint32_t head, c
     }
 }
 
-}
-
 // per-microblock data shared by the lanes of a warp in phase C
 struct MbInfo {
     uint64_t bm0, bm1;  // phase-0 code-word starts (offsets from the microblock start)
