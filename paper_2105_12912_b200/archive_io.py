@@ -1,0 +1,203 @@
+"""Archive files: device archive <-> file through pinned host staging, and
+the parallel per-rank write of a sharded archive (the
+on-disk format is the reference's, P/pipeline.py:26-39, 184-221).
+
+* ``save(arc, path)`` / ``load(path)``: the archive moves in 64 MB pieces
+  through two pinned host buffers, so the device<->host copy of one piece
+  overlaps the file write / read of the other.
+* ``write_sharded(res, path, lengths)``: every rank of a sharded compress
+  (``distributed.compress_sharded``) writes its own byte ranges of the
+  archive file with ``pwrite`` -- its slice of the dense bit stream, its
+  outlier records, its run lengths (RLE+VLE) -- and rank 0 the header,
+  the code book and the section prefixes.  Slices of neighbouring ranks
+  share at most a boundary byte; one all-gather of each rank's first and
+  last byte lets the lowest sharing rank write their OR.  The file is
+  byte-identical to the single-device archive.
+"""
+
+from __future__ import annotations
+
+import os
+import struct
+
+import numpy as np
+
+from .distributed import _HEADER, _SECTION_BASE, MAGIC
+
+_PIECE = 64 << 20
+
+
+def _a8(v: int) -> int:
+    return (v + 7) & ~7
+
+
+def _host_u8(x) -> np.ndarray:
+    try:
+        import torch
+
+        if isinstance(x, torch.Tensor):
+            return x.detach().cpu().numpy().view(np.uint8).reshape(-1)
+    except ImportError:  # pragma: no cover
+        pass
+    return np.asarray(x).view(np.uint8).reshape(-1)
+
+
+def save(arc, path: str) -> int:
+    """Write an archive (DeviceArchive, CUDA/CPU uint8 tensor or bytes) to
+    `path`; returns the byte count."""
+    import torch
+
+    data = getattr(arc, "data", arc)
+    n = getattr(arc, "nbytes", None)
+    if isinstance(data, (bytes, bytearray, memoryview)):
+        with open(path, "wb") as fh:
+            fh.write(data)
+        return len(data)
+    n = data.numel() if n is None else n
+    fd = os.open(path, os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644)
+    try:
+        if not data.is_cuda:
+            os.pwrite(fd, data[:n].numpy().tobytes(), 0)
+            return n
+        bufs = [torch.empty(min(_PIECE, max(n, 1)), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        events = [None, None]
+        pending = None  # (buf index, file offset, length) copied but not yet written
+        for k, off in enumerate(range(0, n, _PIECE)):
+            ln = min(_PIECE, n - off)
+            b = k & 1
+            if events[b] is not None:
+                events[b].synchronize()
+            bufs[b][:ln].copy_(data[off: off + ln], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            events[b] = ev
+            if pending is not None:  # write the previous piece while this one copies
+                pb, poff, pln = pending
+                events[pb].synchronize()
+                os.pwrite(fd, bufs[pb][:pln].numpy().tobytes(), poff)
+            pending = (b, off, ln)
+        if pending is not None:
+            pb, poff, pln = pending
+            events[pb].synchronize()
+            os.pwrite(fd, bufs[pb][:pln].numpy().tobytes(), poff)
+        return n
+    finally:
+        os.close(fd)
+
+
+def load(path: str, device="cuda"):
+    """Read an archive file into a device uint8 tensor (pinned, overlapped)."""
+    import torch
+
+    n = os.path.getsize(path)
+    out = torch.empty(n, dtype=torch.uint8, device=device)
+    bufs = [torch.empty(min(_PIECE, max(n, 1)), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    events = [None, None]
+    with open(path, "rb", buffering=0) as fh:
+        for k, off in enumerate(range(0, n, _PIECE)):
+            ln = min(_PIECE, n - off)
+            b = k & 1
+            if events[b] is not None:
+                events[b].synchronize()  # the buffer's previous upload is done
+            got = fh.readinto(memoryview(bufs[b].numpy())[:ln])
+            if got != ln:
+                raise OSError(f"{path}: short read")
+            out[off: off + ln].copy_(bufs[b][:ln], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            events[b] = ev
+    torch.cuda.synchronize()
+    return out
+
+
+def layout(meta: dict) -> dict:
+    """Section offsets of a sharded compress's archive (P/pipeline.py:184-221)."""
+    cap, total_bits, total_out = meta["cap"], meta["total_bits"], meta["total_out"]
+    nbytes = (total_bits + 7) // 8
+    vle = meta.get("workflow") == "RLE_VLE"
+    prefix = 24 if vle else 16
+    sym_len = prefix + nbytes + (4 * meta["n_runs"] if vle else 0)
+    cb_off = _SECTION_BASE
+    sym_off = _a8(cb_off + cap)
+    out_off = _a8(sym_off + sym_len)
+    return dict(cb_off=cb_off, sym_off=sym_off, sym_len=sym_len, out_off=out_off,
+                data_off=sym_off + prefix, lens_off=sym_off + prefix + nbytes, nbytes=nbytes,
+                total=out_off + 16 * total_out, vle=vle)
+
+
+def _header(meta: dict, lay: dict) -> bytes:
+    dims, chunk, cap = meta["dims"], meta["chunk"], meta["cap"]
+    return _HEADER.pack(MAGIC, 1, meta["dtype_code"], dims.ndim, dims.nx, dims.ny, dims.nz,
+                        chunk.cx, chunk.cy, chunk.cz, 1 if meta["eb_mode"] == "rel" else 0,
+                        meta["eb"], meta["vmin"], meta["vmax"], cap, 2 if lay["vle"] else 0,
+                        dims.count, meta["total_out"], lay["cb_off"], cap, lay["sym_off"],
+                        lay["sym_len"], lay["out_off"], 16 * meta["total_out"])
+
+
+def write_sharded(res, path: str, lengths_bytes: bytes | None = None, group=None) -> int:
+    """Every rank writes its parts of the archive file; returns its size.
+    `lengths_bytes` (the cap code lengths) is only needed on rank 0 and
+    defaults to res.meta["lengths"]."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    m = res.meta
+    lay = layout(m)
+    sl = _host_u8(res.bits) if res.bits is not None else np.zeros(0, np.uint8)
+    first = res.byte_start
+    last = res.byte_start + len(sl) - 1
+    mine = torch.tensor([len(sl), first, last, int(sl[0]) if len(sl) else 0,
+                         int(sl[-1]) if len(sl) else 0], dtype=torch.int64)
+    allv = [torch.zeros(5, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allv, mine, group=group)
+    info = [tuple(int(x) for x in v) for v in allv]
+    # boundary bytes: OR of every rank's contribution, written by the lowest contributor
+    merged: dict[int, list] = {}
+    for k, (ln, f, l, fv, lv) in enumerate(info):
+        if not ln:
+            continue
+        for idx, val in ((f, fv), (l, lv)) if l != f else ((f, fv),):
+            e = merged.setdefault(idx, [0, k])
+            e[0] |= val
+            e[1] = min(e[1], k)
+    if rank == 0:
+        fd = os.open(path, os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644)
+        os.ftruncate(fd, lay["total"])  # zero padding between sections
+        lens = lengths_bytes if lengths_bytes is not None else _host_u8(m["lengths"]).tobytes()
+        os.pwrite(fd, _header(m, lay), 0)
+        os.pwrite(fd, bytes(lens[: m["cap"]]), lay["cb_off"])
+        if lay["vle"]:
+            os.pwrite(fd, struct.pack("<QQQ", m["n_runs"], m["total_bits"], m["n_runs"]),
+                      lay["sym_off"])
+        else:
+            os.pwrite(fd, struct.pack("<QQ", m["total_bits"], m["dims"].count), lay["sym_off"])
+        os.close(fd)
+    dist.barrier(group=group)
+    fd = os.open(path, os.O_WRONLY)
+    try:
+        if len(sl):
+            lo, hi = 0, len(sl)
+            if first in merged:
+                val, owner = merged[first]
+                if owner == rank:
+                    os.pwrite(fd, bytes([val]), lay["data_off"] + first)
+                lo = 1
+            if last in merged and hi > lo:
+                val, owner = merged[last]
+                if owner == rank:
+                    os.pwrite(fd, bytes([val]), lay["data_off"] + last)
+                hi -= 1
+            if hi > lo:
+                os.pwrite(fd, sl[lo:hi].tobytes(), lay["data_off"] + first + lo)
+        if res.records is not None and res.n_out:
+            os.pwrite(fd, _host_u8(res.records)[: 16 * res.n_out].tobytes(),
+                      lay["out_off"] + 16 * res.record_start)
+        if lay["vle"] and res.rle is not None and res.rle["n_runs"]:
+            ln = _host_u8(res.rle["lens"])[: 4 * res.rle["n_runs"]]
+            os.pwrite(fd, ln.tobytes(), lay["lens_off"] + 4 * res.rle["run_start"])
+    finally:
+        os.close(fd)
+    dist.barrier(group=group)
+    return lay["total"]

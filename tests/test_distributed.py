@@ -182,7 +182,7 @@ def _worker(rank, world, port, case, q):
         from paper_2105_12912_b200 import ChunkSpec, Dims
         from paper_2105_12912_b200 import distributed as D
 
-        vals, shape, eb = case
+        vals, shape, eb, path = case
         dims = Dims.of(*shape[::-1])
         chunk = ChunkSpec.default_for(dims.ndim)
         lo, hi = D.slab_bounds(dims, chunk, rank, world)
@@ -190,6 +190,9 @@ def _worker(rank, world, port, case, q):
         slab = full[lo:hi].reshape(-1) if dims.ndim > 1 else full[lo:hi]
         res = D.compress_sharded(OracleSlabOps(), slab, dims, float(vals.min()),
                                  float(vals.max()), eb, "rel", 1024, chunk, 0)
+        from paper_2105_12912_b200 import archive_io
+
+        archive_io.write_sharded(res, path)  # parallel pwrite of every rank's parts
         # slab-local decompress of the rank's own slice == that slab of the
         # single-device decompress
         y = D.decompress_sharded(OracleSlabOps(), res)
@@ -211,7 +214,7 @@ def _worker(rank, world, port, case, q):
 
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("shape", [(40, 30, 36), (300, 257), (70001,)])
-def test_sharded_archive_is_byte_identical(shape, world):
+def test_sharded_archive_is_byte_identical(shape, world, tmp_path):
     import torch.multiprocessing as mp
 
     from helpers import smooth
@@ -224,7 +227,8 @@ def test_sharded_archive_is_byte_identical(shape, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, (vals, shape, eb), q))
+    path = str(tmp_path / "sharded.lzb")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, (vals, shape, eb, path), q))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -233,6 +237,8 @@ def test_sharded_archive_is_byte_identical(shape, world):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert got == ref
+    with open(path, "rb") as fh:
+        assert fh.read() == ref  # the ranks' parallel file write
 
 
 def _archive_worker(rank, world, port, case, q):
@@ -340,7 +346,7 @@ def _rle_worker(rank, world, port, case, q):
         from paper_2105_12912_b200 import ChunkSpec, Dims
         from paper_2105_12912_b200 import distributed as D
 
-        vals, shape, eb, ref_arc = case
+        vals, shape, eb, ref_arc, path = case
         dims = Dims.of(*shape[::-1])
         chunk = ChunkSpec.default_for(dims.ndim)
         lo, hi = D.slab_bounds(dims, chunk, rank, world)
@@ -356,6 +362,9 @@ def _rle_worker(rank, world, port, case, q):
             assert y is not None and np.array_equal(y, want), rank
         lens = np.frombuffer(ref_arc, np.uint8, 1024, O.parse_header(ref_arc)["codebook"][0]).copy() \
             if rank == 0 else None
+        from paper_2105_12912_b200 import archive_io
+
+        archive_io.write_sharded(res, path, lens.tobytes() if rank == 0 else None)
         got = D.gather_results(res)
         if rank == 0:
             q.put(D.assemble(got, lens.tobytes()))
@@ -365,7 +374,7 @@ def _rle_worker(rank, world, port, case, q):
 
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("shape", [(32, 24, 40), (256, 100), (20000,)])
-def test_sharded_rle_vle_archive_is_byte_identical(shape, world):
+def test_sharded_rle_vle_archive_is_byte_identical(shape, world, tmp_path):
     """Auto selection picks RLE+VLE (long runs of the radius code); runs that
     cross slab boundaries are stitched so the archive equals the
     single-process one byte for byte."""
@@ -385,7 +394,8 @@ def test_sharded_rle_vle_archive_is_byte_identical(shape, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rle_worker, args=(r, world, port, (vals, shape, eb, ref), q))
+    path = str(tmp_path / "sharded_rle.lzb")
+    procs = [ctx.Process(target=_rle_worker, args=(r, world, port, (vals, shape, eb, ref, path), q))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -394,6 +404,8 @@ def test_sharded_rle_vle_archive_is_byte_identical(shape, world):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert got == ref
+    with open(path, "rb") as fh:
+        assert fh.read() == ref
 
 
 def test_rle_stitch_plan_matches_global_runs():

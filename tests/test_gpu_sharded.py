@@ -31,7 +31,7 @@ def _worker(rank, world, port, case, q):
         from paper_2105_12912_b200 import ChunkSpec, Dims
         from paper_2105_12912_b200 import distributed as D
 
-        vals, shape, eb = case
+        vals, shape, eb, path = case
         dims = Dims.of(*shape[::-1])
         chunk = ChunkSpec.default_for(dims.ndim)
         lo, hi = D.slab_bounds(dims, chunk, rank, world)
@@ -41,6 +41,9 @@ def _worker(rank, world, port, case, q):
         res = D.compress_sharded(ops, slab, dims, float(vals.min()), float(vals.max()), eb, "rel",
                                  1024, chunk, 0, device=torch.device("cuda"))
         y = D.decompress_sharded(ops, res)
+        from paper_2105_12912_b200 import archive_io
+
+        archive_io.write_sharded(res, path)  # each rank pwrites its parts
         lens = res.meta["lengths"].cpu().numpy().tobytes()
         wf = res.meta["workflow"]
         got = D.gather_results(res)
@@ -65,7 +68,7 @@ def _fields():
 
 
 @pytest.mark.parametrize("name,vals,shape,eb", list(_fields()), ids=[f[0] for f in _fields()])
-def test_sharded_compress_on_device(cuda, name, vals, shape, eb):
+def test_sharded_compress_on_device(cuda, name, vals, shape, eb, tmp_path):
     import torch.multiprocessing as mp
 
     import paper_2105_12912_b200 as lzb
@@ -77,7 +80,8 @@ def test_sharded_compress_on_device(cuda, name, vals, shape, eb):
     q = ctx.Queue()
     world = 2
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, (vals, shape, eb), q))
+    path = str(tmp_path / "sharded.lzb")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, (vals, shape, eb, path), q))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -88,5 +92,29 @@ def test_sharded_compress_on_device(cuda, name, vals, shape, eb):
     arc = [m for m in msgs if len(m) == 2][0]
     assert arc[1] == ("HUFFMAN" if name == "huffman" else "RLE_VLE")
     assert arc[0] == ref
+    with open(path, "rb") as fh:
+        assert fh.read() == ref
     for rank, lo, hi, y in [m for m in msgs if len(m) == 4]:
         assert np.array_equal(y, ref_y[lo:hi].reshape(-1)), rank
+
+
+def test_save_load_round_trip(cuda, tmp_path, monkeypatch):
+    """Device archive -> file -> device through the pinned double buffers
+    (small pieces so several are in flight)."""
+    import torch
+
+    import paper_2105_12912_b200 as lzb
+    from paper_2105_12912_b200 import archive_io
+    from helpers import smooth
+
+    monkeypatch.setattr(archive_io, "_PIECE", 1 << 14)
+    vals = smooth((40, 48, 64)).astype(np.float32)
+    field = lzb.Field.from_array(vals)
+    arc = lzb.compress_device(field, 1e-4)
+    path = str(tmp_path / "a.lzb")
+    n = archive_io.save(arc, path)
+    assert n == arc.nbytes and open(path, "rb").read() == lzb.compress(field, 1e-4)
+    back = archive_io.load(path)
+    assert torch.equal(back, arc.data[: arc.nbytes])
+    y = lzb.decompress(back)
+    assert np.array_equal(y.values.cpu().numpy(), lzb.decompress(lzb.compress(field, 1e-4)).values)
