@@ -326,15 +326,17 @@ __global__ void __launch_bounds__(kR3Threads, TMA ? 2 : 3)
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
             asm volatile("cp.async.wait_group 1;" ::: "memory");
-            const bool wide = reg_out ? ((wide_mask >> k) & 1u) != 0
-                                      : (r1 > r0 && r3_needs_wide(p, r0, r1, k));
+            // warp-uniform by construction; the vote tells the compiler so,
+            // which keeps the chunk's shuffles free of divergence handling
+            const bool wide = __any_sync(f3::kFull, reg_out ? ((wide_mask >> k) & 1u) != 0
+                                                            : (r1 > r0 && r3_needs_wide(p, r0, r1, k)));
             if (wide) {
                 OutT mmv[2] = {vmin, vmax};
                 r3_chunk_wide<SymT, OutT>(&p, c, k, r0, r1, lane, mmv, &overflow);
                 vmin = mmv[0];
                 vmax = mmv[1];
             } else {
-                const bool tma = TMA && cur.full;
+                const bool tma = TMA && __any_sync(f3::kFull, cur.full);
                 uint32_t yb = 0;
                 if (tma) {
                     yb = ybase_s + (nb & 1u) * 2048;
