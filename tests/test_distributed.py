@@ -266,9 +266,10 @@ def _archive_worker(rank, world, port, case, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("shape,workflow", [((40, 30, 36), None), ((300, 257), None),
-                                            ((70,), None), ((64, 64), "rle")])
+@pytest.mark.parametrize("shape,workflow,world",
+                         [(s, wf, w) for s, wf in [((40, 30, 36), None), ((300, 257), None),
+                                                  ((70,), None), ((64, 64), "rle")]
+                          for w in (2, 3)] + [((40, 30, 36), None, 8)])
 def test_sharded_decompress_of_one_archive(shape, workflow, world):
     """Every rank holds the same archive; the ranks' slabs of the bit-range
     decode (transfer maps all-gathered and chained, symbols all-to-all'd to
