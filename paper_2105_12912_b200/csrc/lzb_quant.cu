@@ -39,6 +39,7 @@ struct QuantParams {
     Geom g;
     double two_eb;
     double slack;  // eb_abs * (1 + 1e-12)  (P/quantize.py:108-111)
+    float inv_hi, inv_lo;  // 1 / two_eb as a float pair (f32 fast prequant)
     int64_t radius;
     uint32_t cap;
     void *codes;
@@ -80,6 +81,14 @@ template <typename InT>
 __device__ __forceinline__ int64_t load_pre(const QuantParams &p, uint64_t i, int &flags) {
     if constexpr (std::is_same<InT, int64_t>::value) {
         return static_cast<const int64_t *>(p.x)[i];
+    } else if constexpr (std::is_same<InT, float>::value) {
+        // f32: the double-single fast path of K1's 3D kernels (same proof,
+        // DESIGN.md K1); exact f64 division only near a rounding tie / 2^22
+        const float xv = static_cast<const float *>(p.x)[i];
+        bool ok = true;
+        const int32_t d = f3::pq_fast_f32(xv, p.inv_hi, p.inv_lo, ok);
+        if (ok) return d;
+        return prequant((double)xv, p.two_eb, p.slack, flags);
     } else {
         return prequant(load_in<InT>(p.x, i), p.two_eb, p.slack, flags);
     }
@@ -218,6 +227,8 @@ __global__ void __launch_bounds__(kQThreads) k_quantize(QuantParams p) {
     const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const int64_t r = p.radius;
     int flags = 0;
+    const bool line = p.g.ny == 1 && p.g.nz == 1;  // 1D geometry: no index divisions
+    const bool cx_pow2 = (p.g.cx & (p.g.cx - 1)) == 0;
 
     while (true) {
         if (tid == 0) s_tile = atomicAdd(p.ticket, 1u);
@@ -234,10 +245,14 @@ __global__ void __launch_bounds__(kQThreads) k_quantize(QuantParams p) {
             n = b.n;
             // ---- load + prequantize the box (coalesced along x) ----
             const uint32_t bxy = b.BX * b.EY;
-            for (uint32_t i = tid; i < n; i += kQThreads) {
-                uint32_t z = i / bxy, rem = i - z * bxy, y = rem / b.BX, xx = rem - y * b.BX;
-                uint64_t gi = (b.X0 + xx) + p.g.nx * ((b.Y0 + y) + p.g.ny * (b.Z0 + z));
-                s_pre[i] = load_pre<InT>(p, gi, flags);
+            if (line) {  // 1D: the box is a contiguous range of the field
+                for (uint32_t i = tid; i < n; i += kQThreads) s_pre[i] = load_pre<InT>(p, b.X0 + i, flags);
+            } else {
+                for (uint32_t i = tid; i < n; i += kQThreads) {
+                    uint32_t z = i / bxy, rem = i - z * bxy, y = rem / b.BX, xx = rem - y * b.BX;
+                    uint64_t gi = (b.X0 + xx) + p.g.nx * ((b.Y0 + y) + p.g.ny * (b.Z0 + z));
+                    s_pre[i] = load_pre<InT>(p, gi, flags);
+                }
             }
             __syncthreads();
         } else {
@@ -252,7 +267,10 @@ __global__ void __launch_bounds__(kQThreads) k_quantize(QuantParams p) {
             bool outl = false;
             if (pos < n) {
                 int64_t d;
-                if (BOX) {
+                if (BOX && line) {  // 1D: first difference inside the chunk
+                    const uint32_t lx = cx_pow2 ? (pos & (b.cx - 1)) : pos % b.cx;
+                    d = s_pre[pos] - (lx ? s_pre[pos - 1] : 0);
+                } else if (BOX) {
                     uint32_t bxl, ly, lz, lx;
                     box_pos(b, pos, bxl, ly, lz, lx);
                     d = box_delta(s_pre, b, bxl, ly, lz, lx);
@@ -656,6 +674,11 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
     qp.g = g;
     qp.two_eb = 2.0 * eb_abs;
     qp.slack = eb_abs * (1.0 + 1e-12);
+    {
+        const double inv = 1.0 / (2.0 * eb_abs);
+        qp.inv_hi = (float)inv;
+        qp.inv_lo = (float)(inv - (double)qp.inv_hi);
+    }
     qp.radius = cap / 2;
     qp.cap = cap;
     qp.codes = codes;

@@ -112,13 +112,15 @@ __global__ void __launch_bounds__(kRcThreads) k_reconstruct(RcParams p) {
     double vmin = INFINITY, vmax = -INFINITY;
     unsigned long long bad = ~0ull;
     bool overflow = false;
+    const bool line = p.g.ny == 1 && p.g.nz == 1;  // 1D geometry: no index divisions
+    const bool cx_pow2 = (p.g.cx & (p.g.cx - 1)) == 0;
     for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
         const RTile b = rtile(p.g, p.K, p.tiles_per_row, t);
         const SymT *cs = static_cast<const SymT *>(p.codes) + b.base;
         if (tid == 0) s_big = 0;
         // ---- codes -> q' (box layout) ----
         for (uint32_t i = tid; i < b.n; i += kRcThreads)
-            s_q[rt_box_index(b, i)] = (int64_t)cs[i] - p.radius;
+            s_q[line ? i : rt_box_index(b, i)] = (int64_t)cs[i] - p.radius;
         __syncthreads();
         // ---- fuse this tile's outliers (unique positions: plain adds) ----
         const uint64_t r0 = p.tile_start[t], r1 = p.tile_start[t + 1];
@@ -157,13 +159,20 @@ __global__ void __launch_bounds__(kRcThreads) k_reconstruct(RcParams p) {
             int64_t v[kRcItems];
             uint32_t flags = 0;
             int64_t run = 0;
+            // 1D: position inside the chunk, advanced without divisions
+            uint32_t mx = line ? (cx_pow2 ? (i0 & (b.cx - 1)) : i0 % b.cx) : 0u;
 #pragma unroll
             for (int k = 0; k < kRcItems; k++) {
                 uint32_t i = i0 + k;
                 bool head = false;
                 if (i < b.n) {
-                    uint32_t bxl = i % b.BX;
-                    head = (bxl % b.cx) == 0;
+                    if (line) {
+                        head = mx == 0;
+                        mx = mx + 1 == b.cx ? 0u : mx + 1;
+                    } else {
+                        uint32_t bxl = i % b.BX;
+                        head = (bxl % b.cx) == 0;
+                    }
                     int64_t q = s_q[i];
                     run = head ? q : run + q;
                     v[k] = run;
@@ -262,8 +271,13 @@ __global__ void __launch_bounds__(kRcThreads) k_reconstruct(RcParams p) {
         const uint32_t bxy = b.BX * b.EY;
         OutT *yo = static_cast<OutT *>(p.y);
         for (uint32_t i = tid; i < b.n; i += kRcThreads) {
-            uint32_t z = i / bxy, rem = i - z * bxy, yy = rem / b.BX, x = rem - yy * b.BX;
-            uint64_t gi = (b.X0 + x) + p.g.nx * ((b.Y0 + yy) + p.g.ny * (b.Z0 + z));
+            uint64_t gi;
+            if (line) {
+                gi = b.X0 + i;
+            } else {
+                uint32_t z = i / bxy, rem = i - z * bxy, yy = rem / b.BX, x = rem - yy * b.BX;
+                gi = (b.X0 + x) + p.g.nx * ((b.Y0 + yy) + p.g.ny * (b.Z0 + z));
+            }
             int64_t q = s_q[i];
             double d = __dmul_rn((double)q, p.two_eb);
             OutT o = (OutT)d;
