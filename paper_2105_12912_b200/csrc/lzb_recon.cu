@@ -102,7 +102,7 @@ __device__ __forceinline__ uint32_t rt_box_index(const RTile &b, uint32_t p) {
 }
 
 template <typename SymT, typename OutT>
-__global__ void __launch_bounds__(kRcThreads) k_reconstruct(RcParams p) {
+__global__ void __launch_bounds__(kRcThreads, 4) k_reconstruct(RcParams p) {
     __shared__ int64_t s_q[kRcTile];
     __shared__ int64_t s_cv[32];
     __shared__ uint32_t s_cf[32];
