@@ -88,16 +88,15 @@ __device__ int canonical_from_lengths(const uint8_t *lengths, uint32_t cap, uint
     for (uint32_t i = threadIdx.x; i < 65; i += blockDim.x) s_cnt[i] = 0;
     if (threadIdx.x < 4) s_misc[threadIdx.x] = 0;
     __syncthreads();
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
-        uint32_t L = lengths[s];
-        if (L > 64) {
-            atomicOr(&s_misc[0], 1u);
-            continue;
-        }
-        if (L) {
-            atomicAdd(&s_cnt[L], 1u);
-            atomicMax(&s_misc[1], L);
-        }
+    for (uint32_t s0 = 0; s0 < cap; s0 += blockDim.x) {  // warp-aggregated length counts
+        const uint32_t s = s0 + threadIdx.x;
+        const uint32_t L = s < cap ? lengths[s] : 0u;
+        if (L > 64) atomicOr(&s_misc[0], 1u);
+        const uint32_t Lc = L > 64 ? 0u : L;
+        const uint32_t peers = __match_any_sync(0xffffffffu, Lc);
+        if (Lc && (threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&s_cnt[Lc], (uint32_t)__popc(peers));
+        const uint32_t wmax = __reduce_max_sync(0xffffffffu, Lc);
+        if ((threadIdx.x & 31) == 0 && wmax) atomicMax(&s_misc[1], wmax);
     }
     __syncthreads();
     __shared__ int s_rc;
@@ -179,14 +178,16 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
     // compact nonzero symbols into sortable keys
     for (uint32_t s = threadIdx.x; s < npow2; s += blockDim.x) sc.key[s] = ~0ull;
     __syncthreads();
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
-        uint64_t f = hist[s];
-        lengths[s] = 0;
-        if (f) {
-            if (f >= (1ull << 44)) s_err = 1;
-            uint32_t k = atomicAdd(&s_n, 1u);
-            sc.key[k] = (f << 20) | s;
-        }
+    for (uint32_t s0 = 0; s0 < cap; s0 += blockDim.x) {  // warp-aggregated compaction
+        const uint32_t s = s0 + threadIdx.x;
+        const uint64_t f = s < cap ? hist[s] : 0ull;
+        if (s < cap) lengths[s] = 0;
+        if (f >= (1ull << 44)) s_err = 1;
+        const uint32_t m = __ballot_sync(0xffffffffu, f != 0);
+        uint32_t k0 = 0;
+        if ((threadIdx.x & 31) == 0 && m) k0 = atomicAdd(&s_n, (uint32_t)__popc(m));
+        k0 = __shfl_sync(0xffffffffu, k0, 0);
+        if (f) sc.key[k0 + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = (f << 20) | s;
     }
     __syncthreads();
     const uint32_t n = s_n;
@@ -299,8 +300,15 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
         sum += f * lengths[s];
         tot += f;
     }
-    atomicAdd(&s_sum, sum);
-    atomicAdd(&s_tot, tot);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {  // warp sums first: 32 shared atomics, not 1024
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&s_sum, sum);
+        atomicAdd(&s_tot, tot);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         st->u[0] = s_sum;
