@@ -541,8 +541,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
     def step(prof=None, out=None):
         arc = lzb.compress_device(field, eb, prof=prof)
-        pre = arc.data[: arc.header.symbols[0] + 32].cpu().numpy().tobytes()
-        y, hdr, _, _ = lzb.decompress_device(arc.data, raw_host=pre, prof=prof, out=out)
+        y, hdr, _, _ = lzb.decompress_device(arc, prof=prof, out=out)
         return arc, y
 
     ybuf = torch.empty(n, dtype=x.dtype, device=dev)

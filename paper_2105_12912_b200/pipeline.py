@@ -187,6 +187,9 @@ class DeviceArchive:
     data: object  # torch.uint8 CUDA tensor, exactly `nbytes` long view
     header: ArchiveHeader
     nbytes: int
+    # Huffman stream facts known at compress time (bit length, symbols, max
+    # code length): decompress_device(DeviceArchive) then needs no host reads
+    stream: tuple | None = None
 
     def to_bytes(self) -> bytes:
         return self.data[: self.nbytes].cpu().numpy().tobytes()
@@ -371,7 +374,8 @@ def compress_device(field: Field, eb: float, eb_mode: str = "rel", cap: int = 10
         N.raise_for(final[k], "encode")
     header = ArchiveHeader(dt, dims, chunk, eb_mode, eb, field.vmin, field.vmax, cap, chosen, n,
                            n_out, (cb_off, cb_len), (sym_off, sym_len), (out_off, 16 * n_out))
-    return DeviceArchive(arc[:total], header, total)
+    stream = (bits, n, int(sb.u[2])) if chosen is Workflow.HUFFMAN else None
+    return DeviceArchive(arc[:total], header, total, stream)
 
 
 def _new_archive(total: int, dev):
@@ -465,11 +469,17 @@ def decompress_device(arc, raw_host: bytes | None = None, prof=None, out=None):
 
     ``raw_host`` (optional) is the same archive on the host, used for the
     small header-level reads; without it ~100 bytes + the code book are read
-    back from the device.
+    back from the device.  ``arc`` may also be the DeviceArchive returned by
+    compress_device: its header and Huffman stream facts are already on the
+    host, so nothing is read back before the decode.
     """
     import torch
 
-    hdr = parse_header(raw_host if raw_host is not None else arc, total=arc.numel())
+    known = None
+    if isinstance(arc, DeviceArchive):  # header (and stream facts) already on the host
+        hdr, known, arc = arc.header, arc.stream, arc.data[: arc.nbytes]
+    else:
+        hdr = parse_header(raw_host if raw_host is not None else arc, total=arc.numel())
 
     def host_bytes(a: int, b: int) -> bytes:
         if raw_host is not None and b <= len(raw_host):
@@ -489,12 +499,15 @@ def decompress_device(arc, raw_host: bytes | None = None, prof=None, out=None):
     base = _dev(arc)
     sym_off, sym_len = hdr.symbols
     if hdr.workflow is Workflow.HUFFMAN:
-        cbytes = np.frombuffer(host_bytes(hdr.codebook[0], sum(hdr.codebook)), np.uint8)
-        maxlen = _validate_lengths_host(cbytes)
-        head = host_bytes(sym_off, sym_off + min(16, sym_len))
-        if len(head) < 16:
-            raise CorruptArchiveError("bit stream shorter than its header")
-        bit_len, count = struct.unpack_from("<QQ", head)
+        if known is not None:  # written by compress_device: no host round trip
+            bit_len, count, maxlen = known
+        else:
+            cbytes = np.frombuffer(host_bytes(hdr.codebook[0], sum(hdr.codebook)), np.uint8)
+            maxlen = _validate_lengths_host(cbytes)
+            head = host_bytes(sym_off, sym_off + min(16, sym_len))
+            if len(head) < 16:
+                raise CorruptArchiveError("bit stream shorter than its header")
+            bit_len, count = struct.unpack_from("<QQ", head)
         if sym_len - 16 < (bit_len + 7) // 8:
             raise CorruptArchiveError("bit stream data truncated")
         if count != n:

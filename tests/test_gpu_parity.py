@@ -68,6 +68,9 @@ def test_device_resident_field_matches(golden, cuda):
         y, hdr, vmin, vmax = lzb.decompress_device(da.data)
         want = O.decompress(arc)[0]
         assert np.array_equal(y.cpu().numpy(), want), c["name"]
+        # the DeviceArchive itself (header + stream facts already on the host)
+        y2, hdr2, vmin2, vmax2 = lzb.decompress_device(da)
+        assert np.array_equal(y2.cpu().numpy(), want) and (vmin2, vmax2) == (vmin, vmax), c["name"]
 
 
 @pytest.mark.parametrize("ndim", [1, 2, 3])
