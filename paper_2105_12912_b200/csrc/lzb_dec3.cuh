@@ -26,13 +26,12 @@
 //   Output: the transfer map of every entry phase (composed by the
 //   hierarchical passes into each subsequence's true entry and symbol
 //   offset), and per microblock the chain's entry offset and code-word count.
-// k_dec_final7 (per subsequence, u16 symbols): every lane decodes its
+// k_dec_final9 (per subsequence, u16 symbols): every lane decodes its
 //   microblock from its chain entry (lane 0 from the subsequence's true
-//   entry) with the six-symbol LUT straight into a per-warp stage laid out
-//   like the output range (predicated u16 stores), then the warp copies the
-//   stage out with coalesced 16-byte stores.
-//   Irregular entries first re-resolve the lanes' starts and counts by a
-//   count-only fixpoint.
+//   entry) with the byte LUT into a per-warp stage laid out like the output
+//   range, then the warp widens and copies the stage out with coalesced
+//   16-byte stores.  Irregular entries first re-resolve the lanes' starts
+//   and counts by a count-only fixpoint.
 #pragma once
 // (included inside namespace lzb)
 
@@ -41,8 +40,6 @@ constexpr uint32_t kMB = 128;       // bits per lane (microblock)
 constexpr uint32_t kS3 = 32 * kMB;  // bits per subsequence (warp)
 constexpr uint32_t kStgWords = 136; // staged stream words per subsequence (128 + tail)
 constexpr int kD3Warps = 8;         // k_dec_maps3 CTA
-constexpr int kF7Warps = 16;        // k_dec_final7 CTA
-constexpr uint32_t kF7Slots = 4256; // u16 stage slots per warp: <= 4096 + 7 (alignment) + overrun slack
 
 __device__ __forceinline__ bool bm2_test(uint64_t b0, uint64_t b1, uint32_t q) {  // q < 128
     const uint64_t w = q < 64 ? b0 : b1;
@@ -423,213 +420,6 @@ __global__ void __launch_bounds__(kD3Warps * 32) k_dec_maps3(DecParams p) {
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-// count-only decode with the six-symbol LUT (irregular entries in final7)
-__device__ __forceinline__ bool d3_count6(const uint32_t *stg, uint32_t head, const uint4 *s_lut,
-                                          const uint8_t *s_l1, const DecCanon *tab, uint32_t mstop,
-                                          uint32_t &rel, uint32_t &cnt) {
-    cnt = 0;
-    if (rel >= mstop) return true;
-    SWin r;
-    r.init(stg, rel + head);
-    while (rel < mstop) {
-        const uint32_t pk = r.peek12();
-        const uint32_t w = s_lut[pk].w;
-        uint32_t n = w & 7u, adv = (w >> 3) & 15u;
-        if (n == 0) {
-            const uint32_t l1 = s_l1[pk];
-            adv = (l1 & 0x80u) ? dlen_long(tab, r.peek64(), l1 & 0x7Fu) : 0u;
-            if (adv == 0) return false;
-            n = 1;
-        } else {
-            const uint32_t d = mstop - rel;
-            if (d < (uint32_t)kLutBits) {
-                const uint32_t hi = (w >> 8) & (0xFFFu << d);
-                n -= __popc(hi);
-                adv = hi ? (uint32_t)(__ffs(hi) - 1) : adv;
-            }
-        }
-        cnt += n;
-        rel += adv;
-        r.skip(adv);
-    }
-    return true;
-}
-
-__global__ void __launch_bounds__(kF7Warps * 32, 1) k_dec_final7(DecParams p) {
-    extern __shared__ __align__(16) unsigned char f7_smem[];
-    uint4 *s_lut = reinterpret_cast<uint4 *>(f7_smem);
-    uint16_t *s_out = reinterpret_cast<uint16_t *>(s_lut + kLutSize);           // kF7Warps * kF7Slots
-    uint32_t *s_str = reinterpret_cast<uint32_t *>(s_out + kF7Warps * kF7Slots);  // kF7Warps * 2 * kStgWords
-    uint8_t *s_l1 = reinterpret_cast<uint8_t *>(s_str + kF7Warps * 2 * kStgWords);
-    __shared__ DecCanon s_can;
-    for (uint32_t i = threadIdx.x; i < kLutSize; i += blockDim.x) {
-        s_lut[i] = p.tab->lut6[i];
-        s_l1[i] = p.tab->lut1[i];
-    }
-    load_canon(s_can, p.tab);
-    __syncthreads();
-    if (p.st->code) return;  // corrupt stream: leave the output untouched
-    const DecCanon *tab = &s_can;
-    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    uint16_t *wout = s_out + warp * kF7Slots;
-    const uint32_t out_s = (uint32_t)__cvta_generic_to_shared(wout);
-    uint32_t *wstr = s_str + warp * 2 * kStgWords;
-    const uint32_t str_s = (uint32_t)__cvta_generic_to_shared(wstr);
-    uint16_t *out = static_cast<uint16_t *>(p.out);
-    const uint64_t nw = (uint64_t)gridDim.x * kF7Warps;
-    uint64_t t = (uint64_t)blockIdx.x * kF7Warps + warp;
-    uint32_t sb = 0;
-    d3_stage(p, t, str_s, lane);
-    for (; t < p.T; t += nw, sb ^= 1) {
-        d3_stage(p, t + nw, str_s + (sb ^ 1) * kStgWords * 4, lane);
-        d3_stage_wait();
-        const uint32_t *stg = wstr + sb * kStgWords;
-        const uint32_t e = p.ent0[t];
-        if (e == kExitInvalid || e == kExitEnd) continue;
-        const uint64_t t0 = t * kS3;
-        const bool last = t == p.T - 1;
-        const uint32_t stop = last ? (uint32_t)(p.bit_len - t0) : kS3;
-        const uint32_t la = (stop + kMB - 1) / kMB - 1;
-        const uint64_t base = p.off0[t];
-        const uint64_t endo = last ? p.count : p.off0[t + 1];
-        const uint32_t total = (uint32_t)(endo - base);
-        const uint32_t b = lane * kMB;
-        const bool act = lane <= la;
-        const uint32_t mstop = act ? min(b + kMB, stop) : b;
-        const uint32_t cpv = p.cp[t * 32 + lane];
-        uint32_t cnt = act ? (cpv >> 8) : 0u;
-        uint32_t start = act ? b + (cpv & 0xFFu) : b;
-        if (lane == 0) start = e;
-        const bool irregular = e != 0 && ((p.irr[t] >> e) & 1ull);
-        if (irregular) {
-            // the true path joins the chain after microblock 0: re-resolve the
-            // lanes' starts and counts (count-only, lane by lane)
-            uint32_t x = __shfl_down_sync(kD3Full, start, 1);  // chain exit guess
-            bool need = lane == 0;
-            bool bad = false;
-            while (__any_sync(kD3Full, need)) {
-                bool changed = false;
-                if (need && act) {
-                    uint32_t rel = start, c;
-                    if (!d3_count6(stg, p.head, s_lut, s_l1, tab, mstop, rel, c)) bad = true;
-                    changed = rel != x;
-                    cnt = c;
-                    x = rel;
-                }
-                const uint32_t px = __shfl_up_sync(kD3Full, x, 1);
-                const bool pc = __shfl_up_sync(kD3Full, changed, 1);
-                need = lane > 0 && act && pc && px != start;
-                if (need) start = px;
-            }
-            if (__any_sync(kD3Full, bad)) {
-                if (lane == 0) set_status(p.st, LZB_E_CORRUPT);
-                continue;
-            }
-        } else {
-            const uint32_t rest = __reduce_add_sync(kD3Full, lane ? cnt : 0u);
-            if (lane == 0) cnt = total - rest;
-        }
-        uint32_t inc = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(kD3Full, inc, o);
-            if (lane >= (uint32_t)o) inc += v;
-        }
-        const uint32_t pre = inc - cnt;
-        const uint32_t sum = __shfl_sync(kD3Full, inc, 31);
-        // stage slot j <-> output element base - sh + j; out + base - sh is 16-byte aligned
-        const uint32_t sh = (uint32_t)(((reinterpret_cast<uintptr_t>(out) >> 1) + base) & 7u);
-        bool bad = sum != total || total > kS3 || (act && cnt > kMB);
-        uint32_t rel = start;
-        const uint32_t a0 = out_s + 2 * (sh + pre);  // the lane's first slot
-        uint32_t a = a0;
-        if (!__any_sync(kD3Full, bad) && act && rel < mstop) {
-            SWin r;
-            r.init(stg, rel + p.head);
-            // bulk: the 12-bit window stays inside the microblock
-            while (rel + kLutBits <= mstop) {
-                const uint32_t pk = r.peek12();
-                const uint4 en = s_lut[pk];
-                uint32_t n = en.w & 7u, adv = (en.w >> 3) & 15u;
-                uint32_t x = en.x;
-                if (n == 0) {  // code word longer than 12 bits (or invalid)
-                    const uint32_t l1 = s_l1[pk];
-                    adv = (l1 & 0x80u) ? dsym_long(tab, p.syms, r.peek64(), l1 & 0x7Fu, x) : 0u;
-                    if (adv == 0) {
-                        bad = true;
-                        break;
-                    }
-                    n = 1;
-                }
-                asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)x));
-                if (n > 1) asm volatile("st.shared.u16 [%0+2], %1;" ::"r"(a), "h"((unsigned short)(x >> 16)));
-                if (n > 2) asm volatile("st.shared.u16 [%0+4], %1;" ::"r"(a), "h"((unsigned short)en.y));
-                if (n > 3) asm volatile("st.shared.u16 [%0+6], %1;" ::"r"(a), "h"((unsigned short)(en.y >> 16)));
-                if (n > 4) asm volatile("st.shared.u16 [%0+8], %1;" ::"r"(a), "h"((unsigned short)en.z));
-                if (n > 5) asm volatile("st.shared.u16 [%0+10], %1;" ::"r"(a), "h"((unsigned short)(en.z >> 16)));
-                a += 2 * n;
-                rel += adv;
-                r.skip(adv);
-            }
-            // tail: code words must start before mstop
-            while (!bad && rel < mstop) {
-                const uint32_t pk = r.peek12();
-                const uint4 en = s_lut[pk];
-                uint32_t n = en.w & 7u, adv = (en.w >> 3) & 15u;
-                uint32_t x = en.x;
-                if (n == 0) {
-                    const uint32_t l1 = s_l1[pk];
-                    adv = (l1 & 0x80u) ? dsym_long(tab, p.syms, r.peek64(), l1 & 0x7Fu, x) : 0u;
-                    if (adv == 0) {
-                        bad = true;
-                        break;
-                    }
-                    n = 1;
-                } else {
-                    const uint32_t hi = (en.w >> 8) & (0xFFFu << (mstop - rel));
-                    n -= __popc(hi);
-                    adv = hi ? (uint32_t)(__ffs(hi) - 1) : adv;
-                }
-                asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)x));
-                if (n > 1) asm volatile("st.shared.u16 [%0+2], %1;" ::"r"(a), "h"((unsigned short)(x >> 16)));
-                if (n > 2) asm volatile("st.shared.u16 [%0+4], %1;" ::"r"(a), "h"((unsigned short)en.y));
-                if (n > 3) asm volatile("st.shared.u16 [%0+6], %1;" ::"r"(a), "h"((unsigned short)(en.y >> 16)));
-                if (n > 4) asm volatile("st.shared.u16 [%0+8], %1;" ::"r"(a), "h"((unsigned short)en.z));
-                if (n > 5) asm volatile("st.shared.u16 [%0+10], %1;" ::"r"(a), "h"((unsigned short)(en.z >> 16)));
-                a += 2 * n;
-                rel += adv;
-                r.skip(adv);
-            }
-        }
-        if (act && (a - a0) != 2 * cnt) bad = true;
-        {
-            const uint32_t nstart = __shfl_down_sync(kD3Full, start, 1);
-            if (act && lane < la && rel != nstart) bad = true;
-        }
-        if (__any_sync(kD3Full, bad)) {
-            if (lane == 0) set_status(p.st, LZB_E_CORRUPT);
-            continue;
-        }
-        __syncwarp();
-        // coalesced copy-out: unit q <-> output elements g0 + 8q .. g0 + 8q + 7
-        const uint64_t g0 = base - sh;
-        const uint4 *wv = reinterpret_cast<const uint4 *>(wout);
-        // whole 16-byte units: unit 0 is partial when sh > 0, the last when
-        // the range does not end on a unit boundary
-        const uint32_t q0 = sh ? 1u : 0u, q1 = (sh + total) >> 3;
-        for (uint32_t q = q0 + lane; q < q1; q += 32)
-            *reinterpret_cast<uint4 *>(out + g0 + 8 * q) = wv[q];
-        // the partial head / tail units, one element per lane
-        {
-            const uint32_t c = lane & 7;
-            const uint32_t j = (lane < 8 ? 0u : 8u * q1) + c;
-            const bool part = lane < 8 ? (sh != 0) : (lane < 16 && ((sh + total) & 7) != 0);
-            if (part && j >= sh && j < sh + total) out[g0 + j] = wout[j];
-        }
-        __syncwarp();
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-}
 
 // count-only decode with the byte LUT (irregular entries in final9)
 __device__ __forceinline__ bool d3_count8(const uint32_t *stg, uint32_t head, const uint64_t *s_lut,
@@ -662,8 +452,8 @@ __device__ __forceinline__ bool d3_count8(const uint32_t *stg, uint32_t head, co
 
 // Final decode with a byte-wide stage (u16 books): symbols are staged as
 // bytes s - (cap/2 - 128) and widened in the copy-out, and the decode LUT
-// holds byte deltas (8-byte entries), so a warp needs half of k_dec_final7's
-// shared memory and twice as many warps fit on an SM (the single-chain
+// holds byte deltas (8-byte entries), so a warp needs half the shared memory
+// of a u16 stage (the earlier k_dec_final7) and twice as many warps fit on an SM (the single-chain
 // decode is latency-bound).  A symbol outside the byte range (rare: such
 // symbols have long code words) is staged as the escape byte 255 and its
 // value kept in a per-warp side list that patches the output after the

@@ -616,10 +616,6 @@ struct DecTables {
     // 16-31/32-47/48-63 their symbols (books with cap > 65536 use count 0).
     uint64_t lutm[kLutSize];
     uint8_t lut1[kLutSize];  // first code word: len <= 12, or 0x80 | shortest long len, 0 invalid
-    // Six-symbol LUT for the final decode (u16 books): the code words greedily
-    // decoded from the 12-bit window, up to six: s[0..5], then
-    // n | used << 3 | starts << 8 (bit i of starts: a code word starts at i).
-    uint4 lut6[kLutSize];
     // Byte LUT for the final decode (u16 books, symbols near the radius):
     // up to six code words whose symbols s satisfy 0 <= s - (cap/2 - 128) < 255,
     // stored as those byte deltas; bits 48-50 count (0: first code word longer
@@ -887,18 +883,6 @@ __global__ void __launch_bounds__(1024) k_dec_luts(DecTables *tab, const uint32_
             e |= (uint64_t)sym[i] << (16 + 16 * i);
         }
         tab->lutm[v] = e;
-    }
-    // lut6: up to six code words, their starts
-    {
-        const uint32_t m = wide_cap ? 0u : (n < 6 ? n : 6u);
-        uint32_t s6[6] = {0, 0, 0, 0, 0, 0}, u = 0, sm = 0;
-        for (uint32_t i = 0; i < m; i++) {
-            s6[i] = sym[i];
-            sm |= 1u << u;
-            u += len[i];
-        }
-        tab->lut6[v] = make_uint4(s6[0] | (s6[1] << 16), s6[2] | (s6[3] << 16), s6[4] | (s6[5] << 16),
-                                  m | (u << 3) | (sm << 8));
     }
     // lut8: byte deltas against cap/2 - 128, the prefix whose symbols fit a byte
     {
