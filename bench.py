@@ -494,11 +494,19 @@ def archive_decompress_sharded(args, cfg, dims, ops, x, lo, hi, eb, vmin, vmax, 
     import paper_2105_12912_b200 as lzb
     from paper_2105_12912_b200 import distributed as D
 
-    try:
+    arc, err = None, None
+    try:  # every rank builds the stored archive; all must succeed before any collective
         xf = gen_field_device(cfg, dev)
         fa = lzb.compress_device(lzb.Field.from_array(xf.reshape(cfg["shape"])), eb)
         arc = fa.data[: fa.nbytes].clone()
         del xf, fa
+    except Exception as exc:  # pragma: no cover - box dependent
+        err = repr(exc)[:300]
+    oka = torch.tensor([1 if arc is not None else 0], device=dev, dtype=torch.int64)
+    dist.all_reduce(oka, op=dist.ReduceOp.MIN)
+    if int(oka.item()) != 1:
+        return {"error": err or "another rank could not build the archive"}
+    try:
         ta = []
         ya = None
         for k in range(args.warmup + args.steps):
