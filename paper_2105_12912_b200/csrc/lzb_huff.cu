@@ -393,8 +393,8 @@ __global__ void __launch_bounds__(256) k_huff_scan_w(const __grid_constant__ Enc
 __device__ __forceinline__ uint32_t wswz(uint32_t q) { return q ^ ((q >> 3) & 7u); }
 
 // Pack one lane's 32 code words at tile-relative bit `off` with a 32-bit
-// accumulator, two symbols per step when their code words fit 32 bits
-// together.  Every word the lane COMPLETES is stored plainly (only the lane
+// accumulator, four (or two) symbols per step when their code words fit 32
+// bits together.  Every word the lane COMPLETES is stored plainly (only the lane
 // holding a word's last bit completes it; bits of earlier lanes in that word
 // are zero here and are OR-ed in afterwards); the lane's final partial word is
 // returned for a red.shared.or after a __syncwarp.
@@ -418,27 +418,48 @@ __device__ __forceinline__ void enc_pack_lane(const uint4 (&v)[4], uint32_t nv, 
         waddr += f << 2;
         n = nn - (f << 5);
     };
-    // symbols in pairs: two code words that fit 32 bits together take one step
+    // symbols in quads: four code words that fit 32 bits together take one
+    // step; otherwise pairs, otherwise single code words.  (cap is a power of
+    // two: masking keeps an invalid symbol's lookup in range; the count pass
+    // has already flagged it as a DataError.)
 #pragma unroll
-    for (int i = 0; i < kWSyms / 2; i++) {
-        const uint4 &q = v[i >> 2];
-        const uint32_t w = (i & 3) == 0 ? q.x : (i & 3) == 1 ? q.y : (i & 3) == 2 ? q.z : q.w;
-        const uint32_t s0 = min(w & 0xFFFFu, capm1), s1 = min(w >> 16, capm1);
-        const uint64_t e0 = s_tab[s0], e1 = s_tab[s1];
+    for (int i = 0; i < kWSyms / 4; i++) {
+        const uint4 &q = v[i >> 1];
+        const uint32_t wa = (i & 1) ? q.z : q.x, wb = (i & 1) ? q.w : q.y;
+        const uint64_t e0 = s_tab[wa & capm1], e1 = s_tab[(wa >> 16) & capm1];
+        const uint64_t e2 = s_tab[wb & capm1], e3 = s_tab[(wb >> 16) & capm1];
         uint32_t L0 = (uint32_t)(e0 >> 32), L1 = (uint32_t)(e1 >> 32);
-        uint32_t c0 = (uint32_t)e0, c1 = (uint32_t)e1;  // left-aligned; 0 when L == 0
+        uint32_t L2 = (uint32_t)(e2 >> 32), L3 = (uint32_t)(e3 >> 32);
+        uint32_t c0 = (uint32_t)e0, c1 = (uint32_t)e1, c2 = (uint32_t)e2, c3 = (uint32_t)e3;
         if (!FULL) {
-            L0 = (uint32_t)(2 * i) < nv ? L0 : 0u;
+            const uint32_t b = 4 * i;
+            L0 = b < nv ? L0 : 0u;
             c0 = L0 ? c0 : 0u;
-            L1 = (uint32_t)(2 * i + 1) < nv ? L1 : 0u;
+            L1 = b + 1 < nv ? L1 : 0u;
             c1 = L1 ? c1 : 0u;
+            L2 = b + 2 < nv ? L2 : 0u;
+            c2 = L2 ? c2 : 0u;
+            L3 = b + 3 < nv ? L3 : 0u;
+            c3 = L3 ? c3 : 0u;
         }
-        const uint32_t L = L0 + L1;
-        if (L <= 32) {
-            step(c0 | __funnelshift_rc(c1, 0u, L0), L);  // c1 >> L0 (0 for L0 == 32)
+        const uint32_t La = L0 + L1, Lb = L2 + L3;
+        if (La + Lb <= 32) {
+            const uint32_t ca = c0 | __funnelshift_rc(c1, 0u, L0);  // c1 >> L0 (0 for L0 == 32)
+            const uint32_t cb = c2 | __funnelshift_rc(c3, 0u, L2);
+            step(ca | __funnelshift_rc(cb, 0u, La), La + Lb);
         } else {
-            step(c0, L0);
-            step(c1, L1);
+            if (La <= 32) {
+                step(c0 | __funnelshift_rc(c1, 0u, L0), La);
+            } else {
+                step(c0, L0);
+                step(c1, L1);
+            }
+            if (Lb <= 32) {
+                step(c2 | __funnelshift_rc(c3, 0u, L2), Lb);
+            } else {
+                step(c2, L2);
+                step(c3, L3);
+            }
         }
     }
     last_addr = waddr;
