@@ -801,7 +801,6 @@ class DeviceSlabOps(SlabOps):
         if count != hdr.count:
             raise CorruptArchiveError("decoded stream length does not match the grid")
         cb = np.frombuffer(self._host(arc, hdr.codebook[0], sum(hdr.codebook)), np.uint8)
-        self._arc_ptr = arc.data_ptr()
         return bit_len, count, _validate_lengths_host(cb)
 
     def _range_scratch(self, lo, hi, maxlen, cap):
@@ -886,7 +885,7 @@ class DeviceSlabOps(SlabOps):
 
         from . import _native as N
         from .errors import CorruptArchiveError
-        from .pipeline import Workflow, _validate_lengths_host, code_bytes_for
+        from .pipeline import Workflow, _validate_lengths_host
 
         L = N.lib()
         cap, n = hdr.cap, hdr.count

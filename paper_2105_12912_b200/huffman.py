@@ -48,8 +48,6 @@ def _sym_tensor(codes):
 
 def encode(codes, book: Codebook) -> BitStream:
     """Concatenate code words MSB first (P/huffman.py:46-61) -- K3 on the GPU."""
-    import torch
-
     n = len(codes)
     if n == 0:
         return BitStream(0, 0, np.empty(0, np.uint8))
