@@ -64,6 +64,12 @@ typedef struct lzb_dstatus {
 const char *lzb_version(void);
 const char *lzb_strerror(int code);
 
+/* Byte copy executed by SMs rather than a copy engine (host utility, not a
+ * reference stage): with unified addressing either pointer may be pinned
+ * host memory, so a small host<->device copy issued this way runs beside
+ * large DMA transfers instead of queueing behind them. */
+int lzb_copy_bytes(void *dst, const void *src, uint64_t n, void *stream);
+
 /* ---------------------------------------------------------------------
  * Field range + finiteness.  Replaces Field.from_array / ingest's
  * min/max/_check_finite (P/grid.py:155-202).

@@ -36,6 +36,7 @@ _GP = ctypes.POINTER(Geom)
 SIGNATURES = {
     "lzb_version": (ctypes.c_char_p, []),
     "lzb_strerror": (ctypes.c_char_p, [_I]),
+    "lzb_copy_bytes": (_I, [_P, _P, _U64, _P]),
     "lzb_field_range": (_I, [_P, _I, _U64, _P, _P]),
     "lzb_prequantize": (_I, [_P, _I, _U64, _D, _P, _P, _P]),
     "lzb_quantize_scratch_bytes": (_SZ, [_GP, _U64]),
@@ -125,9 +126,55 @@ class Status:
         return float(np.array([self.u[i]], np.uint64).view(np.float64)[0])
 
 
+_STAGE = {}
+
+
+def _pinned_stage(n: int):
+    """Reusable pinned host buffer for the small host<->device transfers."""
+    import torch
+
+    b = _STAGE.get("buf")
+    if b is None or b.numel() < n:
+        b = torch.empty(max(int(n), 1 << 16), dtype=torch.uint8, pin_memory=True)
+        _STAGE["buf"] = b
+        _STAGE["off"] = 0
+    return b
+
+
+def small_h2d(dst, data: bytes) -> None:
+    """Copy a few host bytes into a device tensor without the DMA queues: an SM
+    copy kernel reads them from mapped pinned memory, so the write never waits
+    behind a large transfer on a copy engine (a rotating region of the stage
+    keeps earlier, still pending copies intact)."""
+    import numpy as _np
+
+    n = len(data)
+    if n == 0:
+        return
+    b = _pinned_stage(8192 + n)
+    off = max(_STAGE["off"], 4096)  # [0, 4096) belongs to read_status
+    if off + n > b.numel():
+        off = 4096
+    b[off: off + n].numpy()[:] = _np.frombuffer(data, _np.uint8)
+    _STAGE["off"] = (off + n + 255) & ~255
+    check_rc(lib().lzb_copy_bytes(dst.data_ptr(), b.data_ptr() + off, n, stream_ptr()), "copy")
+
+
 def read_status(block) -> list[Status]:
-    """One device->host read of a (k x 64)-byte status tensor (synchronises)."""
-    raw = block.cpu().numpy().reshape(-1, STATUS_BYTES)
+    """One device->host read of a (k x 64)-byte status tensor (synchronises).
+    Done by an SM copy kernel into mapped pinned memory, not a copy engine, so
+    it never waits behind a large transfer in flight on another stream."""
+    import torch
+
+    if not block.is_cuda:
+        return [Status(r) for r in block.numpy().reshape(-1, STATUS_BYTES)]
+    n = block.numel()
+    if n > 4096:
+        raise ValueError("status block larger than the read-back region")
+    h = _pinned_stage(8192)
+    check_rc(lib().lzb_copy_bytes(h.data_ptr(), block.data_ptr(), n, stream_ptr()), "copy")
+    torch.cuda.current_stream().synchronize()
+    raw = h[:n].numpy().copy().reshape(-1, STATUS_BYTES)
     return [Status(r) for r in raw]
 
 

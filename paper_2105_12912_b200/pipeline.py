@@ -387,10 +387,7 @@ def _new_archive(total: int, dev):
 
 
 def _h2d(arc, off: int, data: bytes) -> None:
-    import torch
-
-    src = torch.frombuffer(bytearray(data), dtype=torch.uint8)
-    arc[off: off + len(data)].copy_(src)
+    N.small_h2d(arc[off: off + len(data)], data)
 
 
 def compress(field: Field, eb: float, eb_mode: str = "rel", cap: int = 1024, workflow=None,
