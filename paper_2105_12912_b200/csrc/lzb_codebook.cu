@@ -354,8 +354,8 @@ extern "C" int lzb_histogram(const void *sym, int sym_bytes, uint64_t n, uint32_
                              lzb_dstatus *st, void *stream) {
     if (!hist || !st || (sym_bytes != 2 && sym_bytes != 4) || cap == 0) return LZB_E_ARG;
     cudaStream_t s = as_stream(stream);
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
-    LZB_CUDA_TRY(fill_async(hist, 0, cap * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(hist, 0, cap * sizeof(uint64_t), s));
     if (n == 0) return LZB_OK;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -390,7 +390,7 @@ extern "C" int lzb_codebook(const uint64_t *hist, uint32_t cap, uint8_t *lengths
     c.parent = sc.take<uint32_t>(2 * cap);
     c.depth = sc.take<uint8_t>(2 * cap);
     if (!c.depth) return LZB_E_ARG;
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     size_t smem = (size_t)np * 8 + (size_t)cap * 8 + (size_t)cap * 8 + (size_t)cap * 2;
     int use_smem = smem <= 160 * 1024;
     if (use_smem)
@@ -409,7 +409,7 @@ extern "C" int lzb_codebook_from_lengths(const uint8_t *lengths, uint32_t cap, u
     (void)scratch_bytes;
     if (!lengths || !codes || !st || cap == 0) return LZB_E_ARG;
     cudaStream_t s = as_stream(stream);
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     k_from_lengths<<<1, kCbThreads, 0, s>>>(lengths, cap, codes, st);
     LZB_LAUNCH_CHECK();
     return LZB_OK;

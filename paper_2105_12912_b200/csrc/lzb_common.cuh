@@ -34,20 +34,6 @@ static PFN_cuTensorMapEncodeTiled_v12000 tma_encode() {
 }
 
 
-// Small fills (status blocks, look-back words, tickets) by a kernel rather
-// than cudaMemsetAsync, which may be served by a copy engine and would then
-// queue behind large host<->device transfers issued on other streams.
-static __global__ void k_fill_bytes(uint8_t *p, uint32_t v, uint64_t n) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) p[i] = (uint8_t)v;
-}
-static inline cudaError_t fill_async(void *p, int v, size_t n, cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
-    const uint64_t blocks = (n + 255) / 256 < 2048 ? (n + 255) / 256 : 2048;
-    k_fill_bytes<<<(unsigned)blocks, 256, 0, s>>>(static_cast<uint8_t *>(p), (uint32_t)v, n);
-    return cudaGetLastError();
-}
-
 constexpr int kNumSMs = 148;  // B200; launch sizes are re-derived from the device at runtime
 
 static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }

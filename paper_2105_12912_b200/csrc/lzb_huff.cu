@@ -1276,9 +1276,9 @@ static int huff_encode_w(const void *sym, uint64_t n, const uint8_t *lengths, co
     p.ticket = sc.take<unsigned int>(4);
     p.frag = sc.take<uint32_t>(2 * ntw);
     if (!p.frag) return LZB_E_ARG;
-    LZB_CUDA_TRY(fill_async(p.lb, 0, (nscan + 1) * sizeof(uint64_t), s));
-    LZB_CUDA_TRY(fill_async(p.ticket, 0, 4 * sizeof(unsigned int), s));
-    LZB_CUDA_TRY(fill_async(p.cnt + ntw, 0, sizeof(uint32_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.lb, 0, (nscan + 1) * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.ticket, 0, 4 * sizeof(unsigned int), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.cnt + ntw, 0, sizeof(uint32_t), s));
     p.sym = static_cast<const uint16_t *>(sym);
     p.n = n;
     p.lengths = lengths;
@@ -1317,7 +1317,7 @@ static int huff_encode_impl(const void *sym, int sym_bytes, uint64_t n, const ui
     if (!lengths || !codes || !st || (sym_bytes != 2 && sym_bytes != 4) || cap == 0)
         return LZB_E_ARG;
     cudaStream_t s = as_stream(stream);
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     if (n == 0) return LZB_OK;
     if (!sym || !out) return LZB_E_ARG;
     if (sym_bytes == 2 && maxlen >= 1 && maxlen <= 32 && cap <= 4096 &&
@@ -1331,8 +1331,8 @@ static int huff_encode_impl(const void *sym, int sym_bytes, uint64_t n, const ui
     p.ticket = sc.take<unsigned int>(4);
     p.frag = sc.take<uint64_t>(4 * nt);
     if (!p.frag) return LZB_E_ARG;
-    LZB_CUDA_TRY(fill_async(p.lb, 0, nt * sizeof(uint64_t), s));
-    LZB_CUDA_TRY(fill_async(p.ticket, 0, 4 * sizeof(unsigned int), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.lb, 0, nt * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.ticket, 0, 4 * sizeof(unsigned int), s));
     p.sym = sym;
     p.n = n;
     p.lengths = lengths;
@@ -1457,7 +1457,7 @@ static int dec_setup(const uint8_t *bits, uint32_t bit_phase, uint64_t bit_len, 
 // the lengths as corrupt), then the uniform-exit scan.
 static int dec_maps(DecParams &p, const DecLayout &L, cudaStream_t s) {
     const int sms = dev_sms();
-    LZB_CUDA_TRY(fill_async(p.nonuni, 0, 4 * sizeof(unsigned int), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.nonuni, 0, 4 * sizeof(unsigned int), s));
     k_dec_maps3<<<(unsigned)umin64((L.T + kD3Warps - 1) / kD3Warps, (uint64_t)sms * 16), kD3Warps * 32, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
     return LZB_OK;
@@ -1478,8 +1478,8 @@ static int dec_compose(DecParams &p, const DecLayout &L, cudaStream_t s, const u
 // composed hierarchy top-down), then the final decode into p.out.
 static int dec_resolve_final(DecParams &p, const DecLayout &L, cudaStream_t s, int sym_bytes, uint32_t cap) {
     const int sms = dev_sms();
-    LZB_CUDA_TRY(fill_async(p.uticket, 0, sizeof(unsigned int), s));
-    LZB_CUDA_TRY(fill_async(p.ulb, 0, (L.T / 2048 + 2) * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.uticket, 0, sizeof(unsigned int), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.ulb, 0, (L.T / 2048 + 2) * sizeof(uint64_t), s));
     k_dec_scan_uniform<<<(unsigned)umin64((L.T + 2047) / 2048, (uint64_t)sms * 4), 256, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
     k_dec_top<<<1, 32, 0, s>>>(p);
@@ -1512,7 +1512,7 @@ static int huff_decode_impl(const uint8_t *bits, uint32_t bit_phase, uint64_t bi
         maxlen > 64 || bit_phase > 7)
         return LZB_E_ARG;
     cudaStream_t s = as_stream(stream);
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     if (count == 0) {
         // P/huffman.py:114-117: tables are still validated
         Scratch sc(scratch, scratch_bytes);
@@ -1585,7 +1585,7 @@ extern "C" int lzb_huff_range_maps(const uint8_t *bits, uint64_t bit_len, uint64
     int rc = range_args(bits, bit_len, bit_lo, bit_hi, lengths, cap, maxlen, st);
     if (rc != LZB_OK || !fmap) return rc != LZB_OK ? rc : LZB_E_ARG;
     cudaStream_t s = as_stream(stream);
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     DecParams p;
     DecLayout L;
     rc = dec_setup(bits + bit_lo / 8, 0, bit_hi - bit_lo, bit_len - bit_lo, 0, lengths, cap, maxlen, nullptr,
@@ -1594,7 +1594,7 @@ extern "C" int lzb_huff_range_maps(const uint8_t *bits, uint64_t bit_len, uint64
     p.open_end = bit_hi < bit_len;
     if ((rc = dec_maps(p, L, s)) != LZB_OK) return rc;
     // the composition is always needed here (F_k for every entry phase)
-    LZB_CUDA_TRY(fill_async(p.nonuni + 2, 1, sizeof(unsigned int), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(p.nonuni + 2, 1, sizeof(unsigned int), s));
     if ((rc = dec_compose(p, L, s, p.nonuni + 2)) != LZB_OK) return rc;
     k_dec_compose<uint64_t><<<(unsigned)((L.P + 63) / 64), 64, 0, s>>>(p.g2, L.ng2, L.P, (uint32_t)L.ng2,
                                                                      fmap, 1, p.nonuni + 2);

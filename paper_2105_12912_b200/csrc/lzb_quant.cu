@@ -661,13 +661,13 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
         tile_off = sc.take<uint64_t>(L.ntiles);
         slb = sc.take<uint64_t>((L.ntiles + 2047) / 2048 + 1);
         if (!slb) return LZB_E_ARG;
-        LZB_CUDA_TRY(fill_async(slb, 0, ((L.ntiles + 2047) / 2048 + 1) * sizeof(uint64_t), s));
+        LZB_CUDA_TRY(cudaMemsetAsync(slb, 0, ((L.ntiles + 2047) / 2048 + 1) * sizeof(uint64_t), s));
     }
 
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
-    LZB_CUDA_TRY(fill_async(hist, 0, cap * sizeof(uint64_t), s));
-    LZB_CUDA_TRY(fill_async(lb, 0, L.ntiles * sizeof(uint64_t), s));
-    LZB_CUDA_TRY(fill_async(tick, 0, 4 * sizeof(unsigned int), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(hist, 0, cap * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(lb, 0, L.ntiles * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(tick, 0, 4 * sizeof(unsigned int), s));
 
     QuantParams qp;
     qp.x = x;
@@ -785,7 +785,7 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
             }
             LZB_LAUNCH_CHECK();
         }
-        LZB_CUDA_TRY(fill_async(&tick[2], 0, sizeof(unsigned int), s));  // reused below
+        LZB_CUDA_TRY(cudaMemsetAsync(&tick[2], 0, sizeof(unsigned int), s));  // reused below
         rc = LZB_OK;
         goto order;
     }
@@ -833,9 +833,9 @@ order:
     k_check_sorted<<<sms * 4, 256, 0, s>>>(op);
     LZB_LAUNCH_CHECK();
     // the remaining launches exit immediately unless *unsorted was set
-    LZB_CUDA_TRY(fill_async(row_cnt, 0, L.nrows_grid * sizeof(uint32_t), s));
-    LZB_CUDA_TRY(fill_async(seg_end, 0, L.nrows_chunk * sizeof(uint64_t), s));
-    LZB_CUDA_TRY(fill_async(scan_lb, 0, ((L.nrows_grid + 2047) / 2048 + 1) * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(row_cnt, 0, L.nrows_grid * sizeof(uint32_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(seg_end, 0, L.nrows_chunk * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(scan_lb, 0, ((L.nrows_grid + 2047) / 2048 + 1) * sizeof(uint64_t), s));
     k_order_prepare<<<sms * 4, 256, 0, s>>>(op);
     LZB_LAUNCH_CHECK();
     uint64_t scan_tiles = (L.nrows_grid + 2047) / 2048;
@@ -866,7 +866,7 @@ extern "C" int lzb_prequantize(const void *x, int dtype, uint64_t n, double eb_a
                                lzb_dstatus *st, void *stream) {
     if (!x || !out || !st || (dtype != 0 && dtype != 1)) return LZB_E_ARG;
     cudaStream_t s = as_stream(stream);
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     if (n == 0) return LZB_OK;
     unsigned grid = (unsigned)umin64((n + 255) / 256, (uint64_t)device_sms() * 16);
     if (dtype == 0)

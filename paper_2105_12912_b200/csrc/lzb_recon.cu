@@ -719,10 +719,10 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
     unsigned long long *mm = sc.take<unsigned long long>(4);
     unsigned int *tick = sc.take<unsigned int>(4);
     if (!tick) return LZB_E_ARG;
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     k_mm_init<<<1, 32, 0, s>>>(mm, 4);
     LZB_LAUNCH_CHECK();
-    LZB_CUDA_TRY(fill_async(tick, 0, 4 * sizeof(unsigned int), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(tick, 0, 4 * sizeof(unsigned int), s));
     const int sm = nsms();
     const uint64_t n = g.nx * g.ny * g.nz;
     if (L.box) {
@@ -732,9 +732,9 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
         uint64_t *lb = sc.take<uint64_t>((L.ntiles + 1 + 2047) / 2048 + 1);
         uint64_t *brec = sc.take<uint64_t>(2 * (n_out ? n_out : 1));
         if (!brec) return LZB_E_ARG;
-        LZB_CUDA_TRY(fill_async(tile_cnt, 0, (L.ntiles + 1) * sizeof(uint32_t), s));
-        LZB_CUDA_TRY(fill_async(tile_fill, 0, (L.ntiles + 1) * sizeof(uint32_t), s));
-        LZB_CUDA_TRY(fill_async(lb, 0, ((L.ntiles + 1 + 2047) / 2048 + 1) * sizeof(uint64_t), s));
+        LZB_CUDA_TRY(cudaMemsetAsync(tile_cnt, 0, (L.ntiles + 1) * sizeof(uint32_t), s));
+        LZB_CUDA_TRY(cudaMemsetAsync(tile_fill, 0, (L.ntiles + 1) * sizeof(uint32_t), s));
+        LZB_CUDA_TRY(cudaMemsetAsync(lb, 0, ((L.ntiles + 1 + 2047) / 2048 + 1) * sizeof(uint64_t), s));
         OutParams op;
         op.rec = outliers;
         op.n_out = n_out;
@@ -873,7 +873,7 @@ extern "C" int lzb_dequantize(const int64_t *q, uint64_t n, double eb_abs, void 
                               lzb_dstatus *st, void *stream) {
     if (!st || (dtype != 0 && dtype != 1)) return LZB_E_ARG;
     cudaStream_t s = as_stream(stream);
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     unsigned long long *mm = reinterpret_cast<unsigned long long *>(&st->u[3]);
     k_mm_init<<<1, 32, 0, s>>>(mm, 3);
     LZB_LAUNCH_CHECK();
@@ -892,7 +892,7 @@ extern "C" int lzb_dequantize(const int64_t *q, uint64_t n, double eb_abs, void 
 extern "C" int lzb_field_range(const void *x, int dtype, uint64_t n, lzb_dstatus *st, void *stream) {
     if (!x || !st || (dtype != 0 && dtype != 1)) return LZB_E_ARG;
     cudaStream_t s = as_stream(stream);
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     // the status block's u[3..5] double as the reduction slots
     unsigned long long *mm = reinterpret_cast<unsigned long long *>(&st->u[3]);
     k_mm_init<<<1, 32, 0, s>>>(mm, 3);
@@ -924,8 +924,8 @@ extern "C" int lzb_quality(const void *a, const void *b, int dtype, uint64_t n, 
     double *part = sc.take<double>(4096);
     unsigned long long *mk = sc.take<unsigned long long>(2);
     if (!mk) return LZB_E_ARG;
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
-    LZB_CUDA_TRY(fill_async(mk, 0, 2 * sizeof(unsigned long long), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(mk, 0, 2 * sizeof(unsigned long long), s));
     unsigned grid = (unsigned)umin64((n + 255) / 256, 4096);
     if (grid == 0) grid = 1;
     if (dtype == 0) k_quality<float><<<grid, 256, 0, s>>>((const float *)a, (const float *)b, n, part, mk);
@@ -972,6 +972,7 @@ __global__ void __launch_bounds__(256) k_copy_bytes(uint8_t *dst, const uint8_t 
     for (uint64_t i = done + i0; i < n; i += stride) dst[i] = src[i];
 }
 }  // namespace lzb
+
 
 extern "C" int lzb_copy_bytes(void *dst, const void *src, uint64_t n, void *stream) {
     if (n == 0) return LZB_OK;

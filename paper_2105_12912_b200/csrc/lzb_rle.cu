@@ -301,7 +301,7 @@ extern "C" int lzb_count_runs(const void *sym, int sym_bytes, uint64_t n, lzb_ds
                               void *stream) {
     if (!st || (n && !sym) || (sym_bytes != 2 && sym_bytes != 4)) return LZB_E_ARG;
     cudaStream_t s = as_stream(stream);
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     if (n == 0) return LZB_OK;
     const uint64_t ng = (n + 7) / 8;
     const unsigned grid = (unsigned)umin64((ng + 255) / 256, (uint64_t)sms() * 8);
@@ -347,7 +347,7 @@ extern "C" int lzb_rle_encode(const void *sym, int sym_bytes, uint64_t n, uint32
                               lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream) {
     if (!st || (sym_bytes != 2 && sym_bytes != 4) || max_run == 0) return LZB_E_ARG;
     cudaStream_t s = as_stream(stream);
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     if (n == 0) return LZB_OK;
     if (!sym || !values || !lengths) return LZB_E_ARG;
     const uint64_t nt = (n + kRTile - 1) / kRTile;
@@ -364,9 +364,9 @@ extern "C" int lzb_rle_encode(const void *sym, int sym_bytes, uint64_t n, uint32
     uint64_t *pos = sc.take<uint64_t>(c);
     uint64_t *lb2 = sc.take<uint64_t>((c + 2047) / 2048 + 1);
     if (!lb2) return LZB_E_ARG;
-    LZB_CUDA_TRY(fill_async(lb, 0, nt * sizeof(uint64_t), s));
-    LZB_CUDA_TRY(fill_async(tick, 0, 8 * sizeof(unsigned int), s));
-    LZB_CUDA_TRY(fill_async(lb2, 0, ((c + 2047) / 2048 + 1) * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(lb, 0, nt * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(tick, 0, 8 * sizeof(unsigned int), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(lb2, 0, ((c + 2047) / 2048 + 1) * sizeof(uint64_t), s));
     const int nsm = sms();
     unsigned grid = (unsigned)umin64(nt, (uint64_t)nsm * 8);
     if (sym_bytes == 2)
@@ -407,7 +407,7 @@ extern "C" int lzb_rle_decode(const uint8_t *values_le, const uint8_t *lengths_l
                               void *scratch, size_t scratch_bytes, void *stream) {
     if (!st || (sym_bytes != 2 && sym_bytes != 4)) return LZB_E_ARG;
     cudaStream_t s = as_stream(stream);
-    LZB_CUDA_TRY(fill_async(st, 0, sizeof(lzb_dstatus), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     if (runs == 0) {
         if (n != 0) {
             int32_t code = LZB_E_CORRUPT;
@@ -423,8 +423,8 @@ extern "C" int lzb_rle_decode(const uint8_t *values_le, const uint8_t *lengths_l
     uint64_t *lb = sc.take<uint64_t>((runs + 2047) / 2048 + 1);
     unsigned int *tick = sc.take<unsigned int>(4);
     if (!tick) return LZB_E_ARG;
-    LZB_CUDA_TRY(fill_async(lb, 0, ((runs + 2047) / 2048 + 1) * sizeof(uint64_t), s));
-    LZB_CUDA_TRY(fill_async(tick, 0, 4 * sizeof(unsigned int), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(lb, 0, ((runs + 2047) / 2048 + 1) * sizeof(uint64_t), s));
+    LZB_CUDA_TRY(cudaMemsetAsync(tick, 0, 4 * sizeof(unsigned int), s));
     const int nsm = sms();
     k_rld_scan<<<(unsigned)umin64((runs + 2047) / 2048, (uint64_t)nsm * 4), 256, 0, s>>>(
         values_le, lengths_le, runs, cap, vals, starts, lb, &tick[0], st);
