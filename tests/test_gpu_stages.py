@@ -267,3 +267,34 @@ def test_decode_at_bit_phase(cuda):
             (s,) = N.read_status(st)
             assert s.code == 0, (n, phase)
             assert np.array_equal(out.cpu().numpy().view(np.uint16).astype(np.uint32), stream), (n, phase)
+
+
+def test_copy_bytes_and_small_transfers(cuda):
+    """lzb_copy_bytes (SM copies; either side may be mapped pinned host
+    memory), the pinned small-write path and the status read-back."""
+    import torch
+
+    from paper_2105_12912_b200 import _native as N
+
+    L = N.lib()
+    rng = np.random.default_rng(3)
+    for n in (1, 15, 16, 17, 4096, 1 << 20, (1 << 20) + 5):
+        src = torch.from_numpy(rng.integers(0, 256, n).astype(np.uint8))
+        h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        h.copy_(src)
+        d = torch.zeros(n + 16, dtype=torch.uint8, device="cuda")
+        N.check_rc(L.lzb_copy_bytes(d.data_ptr() + 16 * (n % 2), h.data_ptr(), n, N.stream_ptr()), "copy")
+        back = torch.zeros(n, dtype=torch.uint8, pin_memory=True)
+        N.check_rc(L.lzb_copy_bytes(back.data_ptr(), d.data_ptr() + 16 * (n % 2), n, N.stream_ptr()), "copy")
+        torch.cuda.synchronize()
+        assert torch.equal(back, src), n
+    d = torch.zeros(300, dtype=torch.uint8, device="cuda")
+    for k in range(40):  # wraps the rotating stage region several times
+        data = bytes(rng.integers(0, 256, 37).astype(np.uint8))
+        N.small_h2d(d[k % 7: k % 7 + 37], data)
+        torch.cuda.synchronize()
+        assert d[k % 7: k % 7 + 37].cpu().numpy().tobytes() == data
+    st = torch.zeros(2 * N.STATUS_BYTES, dtype=torch.uint8, device="cuda")
+    st[0] = 4
+    s0, s1 = N.read_status(st)
+    assert s0.code == 4 and s1.code == 0
