@@ -294,6 +294,128 @@ def cpu_oracle_run(values, dims, eb, threads):
     return t1 - t0, t2 - t1, len(arc)
 
 
+def _bits_at(data: "np.ndarray", bit_off: int, nbits: int):
+    """nbits of an MSB-first byte stream starting at bit bit_off, re-aligned to
+    bit 0 and zero padded to whole bytes (the layout of a standalone stream)."""
+    import numpy as np
+
+    lo = bit_off // 8
+    hi = (bit_off + nbits + 7) // 8
+    bits = np.unpackbits(np.asarray(data[lo: hi + 1], np.uint8))
+    sh = bit_off - 8 * lo
+    seg = bits[sh: sh + nbits]
+    return np.packbits(seg).tobytes()
+
+
+def parity_check(cfg, x, arc, ybuf, eb, threads):
+    """Bit-exactness of the measured run against the CPU oracle, outside the
+    timed region.
+
+    Small configurations (C1-C4): the whole archive and the whole decoded
+    field are compared with the oracle's.  C5-sized 3D fields (the oracle
+    cannot hold 68 GB of int64 temporaries) are checked segment-wise:
+      1. every 16-plane z-slab (two whole chunk layers, a contiguous range of
+         the chunk-major stream and of the sorted outlier list) goes through
+         the oracle's prequant + construct_stream with the GLOBAL eb_abs; the
+         sum of the slab histograms must equal the device histogram, and the
+         oracle's code book from it must equal the archive's;
+      2. for sampled slabs (first, middle, last) the device code stream range,
+         the archive's outlier records for that slab, the archive's bit stream
+         at the slab's bit offset (oracle huff_encode of the slab stream with
+         the global book) and the decoded slab (oracle reconstruct + dequant)
+         must equal the oracle's, byte for byte."""
+    import numpy as np
+    import torch
+
+    from oracle import oracle as O
+    from paper_2105_12912_b200 import pipeline as PL
+
+    t0 = time.perf_counter()
+    hdr = arc.header
+    shape = cfg["shape"]
+    dims = dims_tuple(shape)
+    n = x.numel()
+    if n <= 400_000_000:
+        xh = x.cpu().numpy()
+        ref = O.compress(xh, dims, hdr.vmin, hdr.vmax, eb, threads=threads)
+        got = arc.to_bytes()
+        ok_arc = got == ref
+        first = None
+        if not ok_arc and len(got) == len(ref):
+            first = int(np.flatnonzero(np.frombuffer(got, np.uint8) != np.frombuffer(ref, np.uint8))[0])
+        want = O.decompress(ref, threads=threads)[0]
+        ok_dec = bool(np.array_equal(ybuf[:n].cpu().numpy().view(np.uint8), want.view(np.uint8)))
+        return {"ok": bool(ok_arc and ok_dec), "mode": "whole archive vs oracle",
+                "archive_equal": bool(ok_arc), "first_diff_byte": first,
+                "decode_equal": ok_dec, "oracle_threads": threads,
+                "seconds": round(time.perf_counter() - t0, 1)}
+    assert len(shape) == 3 and hdr.chunk.as_tuple() == (8, 8, 8)
+    nz, ny, nx = shape
+    plane = nx * ny
+    P = 16
+    nslab = nz // P
+    cap, r = hdr.cap, hdr.cap // 2
+    eb_abs = hdr.eb_abs
+    sample = sorted({0, nslab // 2, nslab - 1})
+    codes_dev = PL._pool.bufs[("codes", str(x.device))]
+    hist_dev = PL._pool.bufs[("hist", str(x.device))][: cap * 8].cpu().numpy().view(np.int64)
+    cb_off = hdr.codebook[0]
+    lens_dev = arc.data[cb_off: cb_off + cap].cpu().numpy()
+    out_off = hdr.outliers[0]
+    rec_dev = arc.data[out_off: out_off + 16 * hdr.outlier_count].cpu().numpy().view(
+        [("i", "<u8"), ("d", "<i8")])
+    ghist = np.zeros(cap, np.int64)
+    slab_hist = []
+    kept = {}
+    res = {"mode": "segment-wise (SURVEY 8(c) steps 1-3 + decoded slabs)", "slabs": nslab,
+           "slab_planes": P, "sampled_slabs": sample, "oracle_threads": threads}
+    ok = True
+    for k in range(nslab):
+        lo = k * P * plane
+        xs = x[lo: lo + P * plane].cpu().numpy()
+        pre = O.prequantize(xs, eb_abs, threads)
+        stream, oi, od = O.construct_stream(pre, (nx, ny, P, 3), (8, 8, 8), r, threads)
+        h = O.histogram(stream, cap)
+        ghist += h
+        slab_hist.append(h)
+        if k in sample:
+            dev_codes = codes_dev[2 * lo: 2 * (lo + P * plane)].cpu().numpy().view(np.uint16)
+            c_ok = bool(np.array_equal(dev_codes, stream))
+            a = np.searchsorted(rec_dev["i"], lo)
+            b = np.searchsorted(rec_dev["i"], lo + P * plane)
+            o_ok = bool(b - a == len(oi) and np.array_equal(rec_dev["i"][a:b] - lo, oi)
+                        and np.array_equal(rec_dev["d"][a:b], od))
+            kept[k] = (stream, oi, od, lo)
+            res[f"slab{k}"] = {"codes_equal": c_ok, "outliers_equal": o_ok, "outliers": int(len(oi))}
+            ok &= c_ok and o_ok
+    h_ok = bool(np.array_equal(ghist, hist_dev))
+    lens = O.huffman_lengths(ghist)
+    b_ok = bool(np.array_equal(lens, lens_dev))
+    res["histogram_equal"] = h_ok
+    res["codebook_equal"] = b_ok
+    ok &= h_ok and b_ok
+    codes = O.canonical_codes(lens)
+    L64 = lens.astype(np.int64)
+    bit_before = np.cumsum([0] + [int((hh * L64).sum()) for hh in slab_hist])
+    sym_off = hdr.symbols[0]
+    for k, (stream, oi, od, lo) in kept.items():
+        nb, _, data = O.huff_encode(stream, lens, codes)
+        boff = int(bit_before[k])
+        dlo = sym_off + 16 + boff // 8
+        dhi = sym_off + 16 + (boff + nb + 7) // 8 + 1
+        seg = arc.data[dlo: min(dhi, sym_off + hdr.symbols[1])].cpu().numpy()
+        bits_ok = _bits_at(seg, boff % 8, nb) == data
+        vals = O.reconstruct(stream, (nx, ny, P, 3), (8, 8, 8), r, oi, od, eb_abs, "f32", threads)
+        d_ok = bool(np.array_equal(ybuf[lo: lo + P * plane].cpu().numpy().view(np.uint32),
+                                   vals.view(np.uint32)))
+        res[f"slab{k}"].update({"bit_offset": boff, "bits": nb, "bits_equal": bool(bits_ok),
+                                "decode_equal": d_ok})
+        ok &= bits_ok and d_ok
+    res["ok"] = bool(ok)
+    res["seconds"] = round(time.perf_counter() - t0, 1)
+    return res
+
+
 def sample_planes_for(cfg, target_elems):
     shape = cfg["shape"]
     per_plane = 1
@@ -629,6 +751,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
     pipe_c = (nbytes + arc_len) / tc / 1e9
     pipe_d = (arc_len + nbytes) / td / 1e9
 
+    # ---- bit-exactness of this run against the oracle (outside the timed region) ----
+    parity = None
+    if not args.no_parity:
+        parity = parity_check(cfg, x, arc, ybuf, eb, os.cpu_count() or 1)
+
     # ---- e2e: host (pinned) buffers through the public device API ----
     # A stream of fields, pipelined the way a production loop would run it:
     # two device input buffers, so field k+2 uploads (copy engine, its own
@@ -699,6 +826,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
         one_step(0, 0)  # warm-up: pinned paths, pools
         torch.cuda.synchronize()
         ok_e2e = bool(torch.equal(yh[:1 << 20].to(dev), ybuf[:1 << 20]))
+        # slices of the finished step-0 result: every timed step decodes the same
+        # field, so the LAST timed step's downloaded result must match them
+        probe = [0, n // 2 - (1 << 19), n - (1 << 20)] if n > (1 << 21) else [0]
+        pw = min(n, 1 << 20)
+        ref_sl = [ybuf[a: a + pw].clone() for a in probe]
         K = args.e2e_steps
         t0 = time.perf_counter()
         upload(1)
@@ -709,12 +841,15 @@ def run_gpu(args, cfg, rank, world, local_rank):
         down.synchronize()
         torch.cuda.synchronize()
         te = (time.perf_counter() - t0) / K
+        ok_e2e = ok_e2e and all(bool(torch.equal(yh[a: a + pw].to(dev), rs))
+                                for a, rs in zip(probe, ref_sl))
         e2e = {"value": round(nbytes / te / 1e9, 4), "unit": "GB/s",
                "h2d_bytes_per_step": nbytes + arc_len, "d2h_bytes_per_step": arc_len + nbytes,
                "ms_per_step": round(te * 1e3, 2), "steps": K,
                "pipelined": "field uploads run two steps ahead (two device input buffers); "
                             "archive copies by SM kernels beside the DMA transfers",
-               "result_check": ok_e2e}
+               "result_check": ok_e2e,
+               "result_check_what": "last timed step's downloaded field == step-0 result at 3 slices"}
         del xh, ah, yh, xds, flds, ad
 
     # ---- CPU baseline: oracle port, 1 thread, bounded sub-slab ----
@@ -752,7 +887,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "stages_ms": stage_ms, "stage_roofline": per_stage_roofline,
         "bound_ok": bool(bound_ok), "max_abs_err": err, "eb_abs": hdr.eb_abs,
         "gpu_launches": launches_per_step(hdr) * args.steps,
-        "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+        "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
     }
     print(json.dumps(line), flush=True)
 
@@ -766,6 +901,8 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the post-run oracle comparison (profiling runs)")
     ap.add_argument("--cpu-sample-elems", type=int, default=2048 * 2048 * 32)
     ap.add_argument("--ref-sample-elems", type=int, default=2048 * 2048 * 16)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],

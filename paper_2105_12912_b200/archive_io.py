@@ -42,6 +42,21 @@ def _host_u8(x) -> np.ndarray:
     return np.asarray(x).view(np.uint8).reshape(-1)
 
 
+def _pwrite_all(fd: int, data, off: int) -> None:
+    """os.pwrite until every byte is written (one call moves at most ~2 GiB on
+    Linux, and may move less)."""
+    mv = memoryview(data).cast("B")
+    done = 0
+    while done < len(mv):
+        k = os.pwrite(fd, mv[done: done + _PWRITE_MAX], off + done)
+        if k <= 0:
+            raise OSError(f"pwrite wrote {k} bytes at offset {off + done}")
+        done += k
+
+
+_PWRITE_MAX = 1 << 30
+
+
 def save(arc, path: str) -> int:
     """Write an archive (DeviceArchive, CUDA/CPU uint8 tensor or bytes) to
     `path`; returns the byte count."""
@@ -57,7 +72,7 @@ def save(arc, path: str) -> int:
     fd = os.open(path, os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644)
     try:
         if not data.is_cuda:
-            os.pwrite(fd, data[:n].numpy().tobytes(), 0)
+            _pwrite_all(fd, data[:n].numpy(), 0)
             return n
         bufs = [torch.empty(min(_PIECE, max(n, 1)), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
         events = [None, None]
@@ -74,12 +89,12 @@ def save(arc, path: str) -> int:
             if pending is not None:  # write the previous piece while this one copies
                 pb, poff, pln = pending
                 events[pb].synchronize()
-                os.pwrite(fd, bufs[pb][:pln].numpy().tobytes(), poff)
+                _pwrite_all(fd, bufs[pb][:pln].numpy(), poff)
             pending = (b, off, ln)
         if pending is not None:
             pb, poff, pln = pending
             events[pb].synchronize()
-            os.pwrite(fd, bufs[pb][:pln].numpy().tobytes(), poff)
+            _pwrite_all(fd, bufs[pb][:pln].numpy(), poff)
         return n
     finally:
         os.close(fd)
@@ -148,11 +163,15 @@ def write_sharded(res, path: str, lengths_bytes: bytes | None = None, group=None
     sl = _host_u8(res.bits) if res.bits is not None else np.zeros(0, np.uint8)
     first = res.byte_start
     last = res.byte_start + len(sl) - 1
+    # NCCL groups have no CPU transport: the exchange tensors live where the
+    # backend can move them
+    tdev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
     mine = torch.tensor([len(sl), first, last, int(sl[0]) if len(sl) else 0,
-                         int(sl[-1]) if len(sl) else 0], dtype=torch.int64)
-    allv = [torch.zeros(5, dtype=torch.int64) for _ in range(world)]
+                         int(sl[-1]) if len(sl) else 0], dtype=torch.int64, device=tdev)
+    allv = [torch.zeros(5, dtype=torch.int64, device=tdev) for _ in range(world)]
     dist.all_gather(allv, mine, group=group)
-    info = [tuple(int(x) for x in v) for v in allv]
+    info = [tuple(int(x) for x in v.cpu()) for v in allv]
     # boundary bytes: OR of every rank's contribution, written by the lowest contributor
     merged: dict[int, list] = {}
     for k, (ln, f, l, fv, lv) in enumerate(info):
@@ -166,13 +185,13 @@ def write_sharded(res, path: str, lengths_bytes: bytes | None = None, group=None
         fd = os.open(path, os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644)
         os.ftruncate(fd, lay["total"])  # zero padding between sections
         lens = lengths_bytes if lengths_bytes is not None else _host_u8(m["lengths"]).tobytes()
-        os.pwrite(fd, _header(m, lay), 0)
-        os.pwrite(fd, bytes(lens[: m["cap"]]), lay["cb_off"])
+        _pwrite_all(fd, _header(m, lay), 0)
+        _pwrite_all(fd, bytes(lens[: m["cap"]]), lay["cb_off"])
         if lay["vle"]:
-            os.pwrite(fd, struct.pack("<QQQ", m["n_runs"], m["total_bits"], m["n_runs"]),
-                      lay["sym_off"])
+            _pwrite_all(fd, struct.pack("<QQQ", m["n_runs"], m["total_bits"], m["n_runs"]),
+                        lay["sym_off"])
         else:
-            os.pwrite(fd, struct.pack("<QQ", m["total_bits"], m["dims"].count), lay["sym_off"])
+            _pwrite_all(fd, struct.pack("<QQ", m["total_bits"], m["dims"].count), lay["sym_off"])
         os.close(fd)
     dist.barrier(group=group)
     fd = os.open(path, os.O_WRONLY)
@@ -182,21 +201,21 @@ def write_sharded(res, path: str, lengths_bytes: bytes | None = None, group=None
             if first in merged:
                 val, owner = merged[first]
                 if owner == rank:
-                    os.pwrite(fd, bytes([val]), lay["data_off"] + first)
+                    _pwrite_all(fd, bytes([val]), lay["data_off"] + first)
                 lo = 1
             if last in merged and hi > lo:
                 val, owner = merged[last]
                 if owner == rank:
-                    os.pwrite(fd, bytes([val]), lay["data_off"] + last)
+                    _pwrite_all(fd, bytes([val]), lay["data_off"] + last)
                 hi -= 1
             if hi > lo:
-                os.pwrite(fd, sl[lo:hi].tobytes(), lay["data_off"] + first + lo)
+                _pwrite_all(fd, sl[lo:hi], lay["data_off"] + first + lo)
         if res.records is not None and res.n_out:
-            os.pwrite(fd, _host_u8(res.records)[: 16 * res.n_out].tobytes(),
-                      lay["out_off"] + 16 * res.record_start)
+            _pwrite_all(fd, _host_u8(res.records)[: 16 * res.n_out],
+                        lay["out_off"] + 16 * res.record_start)
         if lay["vle"] and res.rle is not None and res.rle["n_runs"]:
             ln = _host_u8(res.rle["lens"])[: 4 * res.rle["n_runs"]]
-            os.pwrite(fd, ln.tobytes(), lay["lens_off"] + 4 * res.rle["run_start"])
+            _pwrite_all(fd, ln, lay["lens_off"] + 4 * res.rle["run_start"])
     finally:
         os.close(fd)
     dist.barrier(group=group)

@@ -426,6 +426,8 @@ def compress_sharded(ops: SlabOps, values, dims: Dims, vmin: float, vmax: float,
     world = dist.get_world_size(group)
     eb_abs = _resolve_eb(eb_mode, eb, vmin, vmax)
     _check_cfg(eb_abs, cap)
+    if device is None:  # an empty slab still joins the collectives on the ops' device
+        device = getattr(ops, "device", None)
     lo, hi = slab_bounds(dims, chunk, rank, world)
     sd = slab_dims(dims, lo, hi) if hi > lo else None
     if sd is not None:
@@ -730,7 +732,9 @@ class DeviceSlabOps(SlabOps):
         return records
 
     def to_tensor(self, x):
-        return x
+        import torch
+
+        return torch.as_tensor(x, device=self.device)
 
     def decode_at(self, bits, phase, nbits, count, lengths, cap, maxlen):
         import torch
@@ -873,6 +877,16 @@ class DeviceSlabOps(SlabOps):
             return None, 0
         off = hdr.outliers[0]
         r = arc[off: off + 16 * n].view(torch.int64).view(-1, 2)
+        # P/pipeline.py:306-315: indices strictly increasing and < count, else the
+        # archive is corrupt -- checked on every rank, so all ranks fail alike
+        idx = r[:, 0]
+        bad = (idx[0] < 0) | (idx[-1] >= hdr.count)
+        if n > 1:
+            bad = bad | (idx[1:] <= idx[:-1]).any()
+        if bool(bad):
+            from .errors import CorruptArchiveError
+
+            raise CorruptArchiveError("invalid outlier list")
         b = torch.searchsorted(r[:, 0].contiguous(),
                                torch.tensor([idx_lo, idx_hi], dtype=torch.int64, device=arc.device))
         a, z = (int(v) for v in b.cpu())

@@ -298,3 +298,36 @@ def test_copy_bytes_and_small_transfers(cuda):
     st[0] = 4
     s0, s1 = N.read_status(st)
     assert s0.code == 4 and s1.code == 0
+
+
+def test_reconstruct_fuse_and_layout_kats_on_device(golden, cuda):
+    """The remaining reference KATs, asserted on the CUDA path:
+    fuse (T/test_reconstruct.py:20-25) through K6 (fuse + 1D partial sum),
+    including codes that are NOT the placeholder r at outlier positions
+    (q'[idx] += delta adds, it does not overwrite: P/reconstruct.py:22-32);
+    all-ones 2x2 (T/test_quantize.py:84-88) through K1; chunk-major order
+    (T/test_pipeline.py:220-227) through lzb_chunk_major."""
+    import paper_2105_12912_b200 as lzb
+
+    _, _, k = golden
+    cfg = lzb.QuantConfig(0.1, 8)  # radius 4
+    for codes, want_fused in (([4, 6, 4, 1, 4], k["fuse"]), ([4, 6, 5, 1, 3], None)):
+        quant = lzb.QuantGrid(lzb.Dims.of(5), np.array(codes, np.uint32))
+        outl = lzb.OutlierList(np.array([2, 4], np.int64), np.array([99, -99], np.int64))
+        fused = np.array(codes, np.int64) - 4
+        fused[[2, 4]] += [99, -99]
+        if want_fused is not None:
+            assert fused.tolist() == want_fused
+        pre = lzb.reconstruct_grid(quant, outl, cfg, lzb.ChunkSpec(5))
+        assert pre.codes.tolist() == np.cumsum(fused).tolist()
+        _, opre = O.reconstruct(np.array(codes, np.uint32), (5, 1, 1, 1), (5, 1, 1), 4,
+                                np.array([2, 4]), np.array([99, -99]), 0.1, "f64", want_pre=True)
+        assert pre.codes.tolist() == opre.tolist()
+    ones = lzb.PrequantGrid(lzb.Dims.of(2, 2), np.ones(4, np.int64))
+    q, o = lzb.quantize.construct_grid(ones, lzb.QuantConfig(0.1, 1024), lzb.ChunkSpec(2, 2))
+    assert q.codes.tolist() == k["ones_2x2"] and len(o) == 0
+    grid = lzb.QuantGrid(lzb.Dims.of(4, 2), np.arange(8, dtype=np.uint32))
+    assert lzb.pipeline.gather_chunk_major(grid, lzb.ChunkSpec(2, 2)).tolist() == k["chunk_major_4x2"]
+    back = lzb.pipeline.scatter_chunk_major(np.array(k["chunk_major_4x2"], np.uint32), lzb.Dims.of(4, 2),
+                                   lzb.ChunkSpec(2, 2))
+    assert back.codes.tolist() == list(range(8))
