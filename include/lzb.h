@@ -45,6 +45,8 @@ extern "C" {
 #define LZB_E_CUDA 5       /* CUDA launch / runtime error                      */
 #define LZB_E_ASSERT 6     /* the reference's debug assert (P/quantize.py:106) */
 #define LZB_E_CAPACITY 7   /* output buffer too small; true size in st->u[..]  */
+#define LZB_E_RETRY 8      /* fast decoder could not resolve the stream: call  */
+                           /* lzb_huff_decode_robust (also judges corruption)  */
 
 /* Dims + ChunkSpec (P/grid.py:27-93) */
 typedef struct lzb_geom {
@@ -162,18 +164,29 @@ int lzb_huff_encode_at(const void *sym, int sym_bytes, uint64_t n, const uint8_t
 
 /* ---------------------------------------------------------------------
  * K5: self-synchronising parallel Huffman decode of a dense MSB-first bit
- * stream (P/huffman.py:64-122).  `bits` holds ceil(bit_len/8) bytes, any
- * alignment.  Writes `count` symbols.  `maxlen` is the largest entry of
- * `lengths` (the host reads it from the archive's code book section; the
- * device re-checks it).  code = LZB_E_CORRUPT for an invalid code book
- * (Codebook.from_lengths rules) or when the stream does not decode to
- * exactly `count` code words ending at bit_len.  st->u[0] = symbols decoded.
+ * stream (replaces lzebc.huffman.decode, P/huffman.py:64-122, and its numba
+ * kernel _decode_kernel, P/huffman.py:85-106).  `bits` holds ceil(bit_len/8)
+ * bytes, any alignment.  Writes `count` symbols.  `maxlen` is the largest
+ * entry of `lengths` (the host reads it from the archive's code book
+ * section; the device re-checks it).  code = LZB_E_CORRUPT for an invalid
+ * code book (Codebook.from_lengths rules) or when the stream does not decode
+ * to exactly `count` code words ending at bit_len.
+ *
+ * lzb_huff_decode is the fast two-pass decoder (u16 symbols): it may end with
+ * code = LZB_E_RETRY instead (a book that does not resynchronise within a
+ * 128-bit microblock, or any irregular/corrupt stream); the caller then runs
+ * lzb_huff_decode_robust on the same arguments, the exhaustive decoder
+ * (transfer maps of every entry phase), which also reports corruption.
  * ------------------------------------------------------------------- */
 size_t lzb_huff_decode_scratch_bytes(uint64_t bit_len, uint32_t maxlen, uint32_t cap);
 int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t count,
                     const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym,
                     int sym_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
                     void *stream);
+int lzb_huff_decode_robust(const uint8_t *bits, uint64_t bit_len, uint64_t count,
+                           const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym,
+                           int sym_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
+                           void *stream);
 
 /* Multi-GPU slab variant: the stream's first bit is bit
  * `bit_phase` (0..7, MSB first) of bits[0] -- a rank's slice as produced by
@@ -237,6 +250,26 @@ size_t lzb_rle_decode_scratch_bytes(uint64_t runs);
 int lzb_rle_decode(const uint8_t *values_le, const uint8_t *lengths_le, uint64_t runs,
                    uint32_t cap, void *sym, int sym_bytes, uint64_t n, lzb_dstatus *st,
                    void *scratch, size_t scratch_bytes, void *stream);
+
+/* ---------------------------------------------------------------------
+ * Fused K5 + K6: decompress a Huffman archive's symbol stream straight into
+ * the field (replaces lzebc.decompress's Huffman branch, P/pipeline.py:318-326
+ * = decode P/huffman.py:64-122 + scatter P/pipeline.py:108-117 + fuse /
+ * partial sums / dequantize P/reconstruct.py:22-88).  Tiles of 16 chunks
+ * are decoded into shared memory and reconstructed there; the symbol stream
+ * never reaches HBM.  Eligible grids (lzb_decompress_fused_ok): ChunkSpec
+ * (8,8,8), nx/ny/nz multiples of 8, f32 output, cap <= 65536.  `y` is
+ * 16-byte aligned.  On return st->code = 0 and st->u[0]/u[1] = f64 bits of
+ * the output min/max; any other code (LZB_E_RETRY included) means: decode
+ * with lzb_huff_decode(_robust) + lzb_reconstruct for the exact verdict.
+ * ------------------------------------------------------------------- */
+int lzb_decompress_fused_ok(const lzb_geom *g, uint32_t cap, int dtype);
+size_t lzb_decompress_scratch_bytes(const lzb_geom *g, uint64_t bit_len, uint64_t count, uint32_t cap,
+                                    uint64_t n_out);
+int lzb_decompress_huff(const uint8_t *bits, uint64_t bit_len, uint64_t count, const uint8_t *lengths,
+                        uint32_t cap, uint32_t maxlen, const uint8_t *outliers, uint64_t n_out,
+                        const lzb_geom *g, double eb_abs, void *y, int dtype, lzb_dstatus *st,
+                        void *scratch, size_t scratch_bytes, void *stream);
 
 /* ---------------------------------------------------------------------
  * K6: fused outlier fuse + chunk-wise multi-dimensional partial-sum

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "liblzb.so")
 
 LZB_OK, LZB_E_ARG, LZB_E_DATA, LZB_E_OVERFLOW = 0, 1, 2, 3
 LZB_E_CORRUPT, LZB_E_CUDA, LZB_E_ASSERT, LZB_E_CAPACITY = 4, 5, 6, 7
+LZB_E_RETRY = 8  # the fast decoder could not resolve the stream: run the robust one
 
 STATUS_BYTES = 64
 
@@ -50,6 +51,7 @@ SIGNATURES = {
     "lzb_huff_encode_at": (_I, [_P, _I, _U64, _P, _P, _U32, _U32, _U64, _P, _U64, _P, _P, _SZ, _P]),
     "lzb_huff_decode_scratch_bytes": (_SZ, [_U64, _U32, _U32]),
     "lzb_huff_decode": (_I, [_P, _U64, _U64, _P, _U32, _U32, _P, _I, _P, _P, _SZ, _P]),
+    "lzb_huff_decode_robust": (_I, [_P, _U64, _U64, _P, _U32, _U32, _P, _I, _P, _P, _SZ, _P]),
     "lzb_huff_decode_at": (_I, [_P, _U64, _U64, _U64, _P, _U32, _U32, _P, _I, _P, _P, _SZ, _P]),
     "lzb_huff_range_scratch_bytes": (_SZ, [_U64, _U32, _U32]),
     "lzb_huff_range_maps": (_I, [_P, _U64, _U64, _U64, _P, _U32, _U32, _P, _P, _P, _SZ, _P]),
@@ -60,6 +62,9 @@ SIGNATURES = {
     "lzb_rle_encode": (_I, [_P, _I, _U64, _P, _P, _U64, _U64, _P, _P, _SZ, _P]),
     "lzb_rle_decode_scratch_bytes": (_SZ, [_U64]),
     "lzb_rle_decode": (_I, [_P, _P, _U64, _U32, _P, _I, _U64, _P, _P, _SZ, _P]),
+    "lzb_decompress_fused_ok": (_I, [_GP, _U32, _I]),
+    "lzb_decompress_scratch_bytes": (_SZ, [_GP, _U64, _U64, _U32, _U64]),
+    "lzb_decompress_huff": (_I, [_P, _U64, _U64, _P, _U32, _U32, _P, _U64, _GP, _D, _P, _I, _P, _P, _SZ, _P]),
     "lzb_reconstruct_scratch_bytes": (_SZ, [_GP, _U64]),
     "lzb_reconstruct": (_I, [_P, _I, _P, _U64, _GP, _D, _U32, _P, _I, _P, _P, _P, _SZ, _P]),
     "lzb_dequantize": (_I, [_P, _U64, _D, _P, _I, _P, _P]),

@@ -26,6 +26,9 @@
 // decodes from the true entries, staging 32 symbols per lane in shared memory
 // so each warp writes coalesced runs.
 #include "lzb_common.cuh"
+#include "lzb_dectab.cuh"
+#define LZB_DEC4_KERNELS
+#include "lzb_dec4.cuh"
 
 namespace lzb {
 
@@ -625,54 +628,6 @@ __global__ void k_huff_fixup_w(const __grid_constant__ EncWParams p) {
 // ============================================================================
 // K5 decode
 // ============================================================================
-constexpr int kLutBits = 12;
-constexpr uint32_t kLutSize = 1u << kLutBits;
-constexpr uint8_t kExitInvalid = 0xFF;
-constexpr uint8_t kExitEnd = 0xFE;
-
-struct DecTables {
-    // Multi-symbol LUT on the next 12 bits: up to three complete code words
-    // greedily decoded from the window.  bits 0-1 count (0 = first code word
-    // longer than 12 bits or invalid prefix), 2-5/6-9/10-13 their lengths,
-    // 16-31/32-47/48-63 their symbols (books with cap > 65536 use count 0).
-    uint64_t lutm[kLutSize];
-    uint8_t lut1[kLutSize];  // first code word: len <= 12, or 0x80 | shortest long len, 0 invalid
-    // Byte LUT for the final decode (u16 books, symbols near the radius):
-    // up to six code words whose symbols s satisfy 0 <= s - (cap/2 - 128) < 255,
-    // stored as those byte deltas; bits 48-50 count (0: first code word longer
-    // than 12 bits, invalid, or its symbol out of byte range), 51-54 bits used.
-    uint64_t lut8[kLutSize];
-    uint16_t lut8s[kLutSize];  // code-word start mask of lut8's code words
-    uint16_t lut1s[kLutSize];  // symbol of the first code word (when <= 12 bits)
-    // Boundary LUT for the map pass: n | used << 4 | starts << 8, where bit i
-    // of `starts` marks a code word starting at window offset i (up to 12
-    // complete code words greedily decoded from the 12-bit window).
-    uint32_t lutb[kLutSize];
-    uint64_t first[65];
-    uint64_t cnt[65];
-    uint32_t off[65];
-    uint32_t maxlen;
-    uint32_t nsym;
-};
-
-// The canonical tables for code words longer than the LUT, copied to shared
-// memory by each decode CTA.
-struct DecCanon {
-    uint64_t first[65];
-    uint64_t cnt[65];
-    uint32_t off[65];
-    uint32_t maxlen;
-};
-
-__device__ __forceinline__ void load_canon(DecCanon &c, const DecTables *t) {
-    for (uint32_t i = threadIdx.x; i < 65; i += blockDim.x) {
-        c.first[i] = t->first[i];
-        c.cnt[i] = t->cnt[i];
-        c.off[i] = t->off[i];
-    }
-    if (threadIdx.x == 0) c.maxlen = t->maxlen;
-}
-
 struct DecParams {
     const uint32_t *words;  // 4-byte aligned base covering the stream
     uint32_t head;          // bit offset of the stream inside words[0]
@@ -704,6 +659,9 @@ struct DecParams {
     unsigned int *nonuni;  // count of subsequences whose valid entries exit differently
     uint64_t *ulb;     // look-back words of the uniform scan
     unsigned int *uticket;
+    // plan mode (K5 v4, lzb_dec4.cuh): entries / offsets from the plan's
+    // per-microblock arrays (cp above, these offsets), no irregular entries
+    const uint64_t *pmboff;
     // bit-range mode (multi-GPU decode of one stream, lzb_huff_range_*):
     // the range starts in phase entry0 and must leave in phase exit_expect
     // (kExitEnd when it ends the stream); an open range's last subsequence
@@ -935,6 +893,7 @@ __global__ void __launch_bounds__(1024) k_dec_luts(DecTables *tab, const uint32_
             u += len[i];
         }
         tab->lutb[v] = n | (u << 4) | (sm << 8);
+        tab->lutc[v] = n ? (u | (n << 16)) : 0x80000000u;
     }
     // lut1: first code word: its length if <= 12 bits, else 0x80 | the shortest
     // length of a code word with this 12-bit prefix, 0 = invalid prefix
@@ -947,6 +906,16 @@ __global__ void __launch_bounds__(1024) k_dec_luts(DecTables *tab, const uint32_
             if ((f >> sh) <= v && v <= ((f + (k - 1)) >> sh)) l1 = 0x80u | L;
         }
         tab->lut1[v] = (uint8_t)l1;
+    }
+    // lut6: the first six code words as u16 symbols
+    {
+        const uint32_t m = wide_cap ? 0u : (n < 6 ? n : 6u);
+        uint32_t w[3] = {0, 0, 0}, u = 0;
+        for (uint32_t i = 0; i < m; i++) {
+            w[i >> 1] |= (sym[i] & 0xFFFFu) << (16 * (i & 1));
+            u += len[i];
+        }
+        tab->lut6[v] = make_uint4(w[0], w[1], w[2], m | (u << 8));
     }
 }
 
@@ -1240,6 +1209,76 @@ static int dev_sms() {
     return sms > 0 ? sms : 148;
 }
 
+// ---- K5 v4 plan (lzb_dec4.cuh) ----
+// scratch order: tables, syms, cp, mboff, tfirst, sbm, srest, sx0, sexit, look-back + ticket
+static void d4_sizes(ScratchSize &sc, uint64_t T, uint64_t ntiles, uint32_t cap) {
+    const uint64_t ntl = (T + kD4ResolveThreads - 1) / kD4ResolveThreads;
+    sc.take<DecTables>(1);
+    sc.take<uint32_t>(cap);
+    sc.take<uint16_t>(32 * T);
+    sc.take<uint64_t>(32 * T);
+    sc.take<uint64_t>(ntiles + 1);
+    sc.take<uint64_t>(T);
+    sc.take<uint32_t>(T);
+    sc.take<uint8_t>(T);
+    sc.take<uint8_t>(T);
+    sc.take<uint64_t>(ntl + 2);
+}
+
+static bool d4_take(Scratch &sc, uint64_t T, uint64_t ntiles, uint32_t cap, D4Plan &p) {
+    const uint64_t ntl = (T + kD4ResolveThreads - 1) / kD4ResolveThreads;
+    p.tab = sc.take<DecTables>(1);
+    p.syms = sc.take<uint32_t>(cap);
+    p.cp = sc.take<uint16_t>(32 * T);
+    p.mboff = sc.take<uint64_t>(32 * T);
+    p.tfirst = sc.take<uint64_t>(ntiles + 1);
+    p.sbm = sc.take<uint64_t>(T);
+    p.srest = sc.take<uint32_t>(T);
+    p.sx0 = sc.take<uint8_t>(T);
+    p.sexit = sc.take<uint8_t>(T);
+    p.lb = sc.take<uint64_t>(ntl + 2);  // + the ticket word (one memset)
+    p.ticket = p.lb ? reinterpret_cast<unsigned int *>(p.lb + ntl + 1) : nullptr;
+    return p.ticket != nullptr;
+}
+
+size_t d4_scratch_bytes(uint64_t bit_len, uint64_t count, uint32_t cap) {
+    ScratchSize s;
+    const uint64_t T = bit_len ? (bit_len + kD4S - 1) / kD4S : 1;
+    d4_sizes(s, T, (count + kD4Tile - 1) / kD4Tile, cap);
+    return s.bytes();
+}
+
+int d4_plan(const uint8_t *bits, uint32_t bit_phase, uint64_t bit_len, uint64_t count,
+            const uint8_t *lengths, uint32_t cap, uint32_t maxlen, lzb_dstatus *st, Scratch &sc,
+            cudaStream_t s, D4Plan &p) {
+    if (!bits || bit_len == 0 || count == 0) return LZB_E_ARG;
+    p.bit_len = bit_len;
+    p.count = count;
+    p.T = (bit_len + kD4S - 1) / kD4S;
+    p.nmb = (bit_len + kD4MB - 1) / kD4MB;
+    p.ntiles = (count + kD4Tile - 1) / kD4Tile;
+    if (!d4_take(sc, p.T, p.ntiles, cap, p)) return LZB_E_ARG;
+    uintptr_t a = reinterpret_cast<uintptr_t>(bits);
+    p.words = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
+    p.head = (uint32_t)(a & 3) * 8 + bit_phase;
+    p.nwords = ((p.head + bit_len + 7) / 8 + 3) / 4;
+    p.base8 = (int32_t)(cap / 2) - 128;
+    p.st = st;
+    const uint64_t ntl = (p.T + kD4ResolveThreads - 1) / kD4ResolveThreads;
+    LZB_CUDA_TRY(cudaMemsetAsync(p.lb, 0, (ntl + 2) * sizeof(uint64_t), s));
+    k_dec_tables<<<1, 1024, 0, s>>>(lengths, cap, maxlen, const_cast<DecTables *>(p.tab),
+                                    const_cast<uint32_t *>(p.syms), st);
+    LZB_LAUNCH_CHECK();
+    k_dec_luts<<<kLutSize / 1024, 1024, 0, s>>>(const_cast<DecTables *>(p.tab), p.syms, cap, st);
+    LZB_LAUNCH_CHECK();
+    const int sms = dev_sms();
+    k_dec4_count<<<(unsigned)umin64((p.T + kD4Warps - 1) / kD4Warps, (uint64_t)sms * 8), kD4Warps * 32, 0, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    k_dec4_resolve<<<(unsigned)umin64(ntl, (uint64_t)sms * 4), kD4ResolveThreads, 0, s>>>(p);
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}
+
 }  // namespace lzb
 
 using namespace lzb;
@@ -1392,7 +1431,10 @@ extern "C" int lzb_huff_encode_at(const void *sym, int sym_bytes, uint64_t n, co
 extern "C" size_t lzb_huff_decode_scratch_bytes(uint64_t bit_len, uint32_t maxlen, uint32_t cap) {
     ScratchSize s;
     dec_scratch(s, dec_layout(bit_len, maxlen), cap);
-    return s.bytes();
+    // the fast path's plan is sized by symbols too; a stream of bit_len bits
+    // holds at most bit_len code words
+    const size_t f = d4_scratch_bytes(bit_len, bit_len, cap);
+    return s.bytes() > f ? s.bytes() : f;
 }
 
 // Tables + LUTs + the scratch carve-up shared by the whole-stream and the
@@ -1425,6 +1467,7 @@ static int dec_setup(const uint8_t *bits, uint32_t bit_phase, uint64_t bit_len, 
     p.open_end = 0;
     p.tab = tab;
     p.syms = syms;
+    p.pmboff = nullptr;
     p.S = L.S;
     p.T = L.T;
     p.P = L.P;
@@ -1540,10 +1583,59 @@ static int huff_decode_impl(const uint8_t *bits, uint32_t bit_phase, uint64_t bi
     return dec_resolve_final(p, L, s, sym_bytes, cap);
 }
 
+// Fast path (K5 v4, lzb_dec4.cuh) for u16 symbols; LZB_E_RETRY in st sends the
+// caller to lzb_huff_decode_robust.
 extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t count,
                                const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym,
                                int sym_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
                                void *stream) {
+    if (sym_bytes != 2 || cap > 65536 || count == 0 || bit_len == 0 || !bits || !sym || !lengths || !st ||
+        maxlen == 0 || maxlen > 64 || (reinterpret_cast<uintptr_t>(sym) & 1))
+        return huff_decode_impl(bits, 0, bit_len, count, lengths, cap, maxlen, sym, sym_bytes, st, scratch,
+                                scratch_bytes, stream);
+    cudaStream_t s = as_stream(stream);
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
+    Scratch sc(scratch, scratch_bytes);
+    D4Plan p;
+    int rc = d4_plan(bits, 0, bit_len, count, lengths, cap, maxlen, st, sc, s, p);
+    if (rc != LZB_OK) return rc;
+    // final decode: k_dec_final9 (warp per subsequence, byte stage, coalesced
+    // u16 stores) reading the entries and offsets of the plan
+    DecParams q{};
+    q.words = p.words;
+    q.head = p.head;
+    q.nwords = p.nwords;
+    q.bit_len = bit_len;
+    q.total_bits = bit_len;
+    q.count = count;
+    q.tab = p.tab;
+    q.syms = p.syms;
+    q.S = kS3;
+    q.T = p.T;
+    q.P = maxlen;
+    q.cp = p.cp;
+    q.pmboff = p.mboff;
+    q.st = st;
+    q.out = sym;
+    q.entry0 = 0;
+    q.exit_expect = kExitEnd;
+    q.open_end = 0;
+    const int sms = dev_sms();
+    const size_t f9 = (size_t)kLutSize * (8 + 2 + 2 + 1) + (size_t)kF9Warps * kF9Stage +
+                      (size_t)kF9Warps * 2 * kStgWords * 4;
+    LZB_CUDA_TRY(cudaFuncSetAttribute(k_dec_final9, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f9));
+    const unsigned g9 = (unsigned)umin64((p.T + kF9Warps - 1) / kF9Warps, (uint64_t)sms);
+    k_dec_final9<<<g9, kF9Warps * 32, f9, s>>>(q, cap);
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}
+
+// The exhaustive decoder: transfer maps of every entry phase composed over the
+// whole stream (any prefix code, also books that never resynchronise).
+extern "C" int lzb_huff_decode_robust(const uint8_t *bits, uint64_t bit_len, uint64_t count,
+                                      const uint8_t *lengths, uint32_t cap, uint32_t maxlen, void *sym,
+                                      int sym_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
+                                      void *stream) {
     return huff_decode_impl(bits, 0, bit_len, count, lengths, cap, maxlen, sym, sym_bytes, st, scratch,
                             scratch_bytes, stream);
 }

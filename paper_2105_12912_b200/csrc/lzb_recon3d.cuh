@@ -99,6 +99,128 @@ __device__ __forceinline__ void r3_add_reg(uint32_t rkey, int32_t rd, uint32_t n
     }
 }
 
+// ---------------------------------------------------------------------------
+// Packed 16-bit reconstruction (cap <= 4096).  All partial sums are taken
+// modulo 2^16, two x-neighbours per register (VIADD.16x2); the results are
+// exact whenever every partial sum of the chunk fits int16, which holds when
+// sum |q'| over the chunk < 2^15 -- checked first, exactly (codes give |q'| <
+// 2048, at most 8 per 16-bit half, so the packed sum of |q'| cannot wrap).
+// Chunks that fail the check take the int32 path.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t v2add(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("add.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t v2min(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("min.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t v2max(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+// v += (value of lane - o inside the 2^k-lane segment given by c), if that lane exists
+__device__ __forceinline__ void v2_shfl_add(uint32_t &v, uint32_t src, uint32_t o, uint32_t c) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+        "shfl.sync.up.b32 t|p, %1, %2, %3, -1;\n\t"
+        "@p add.s16x2 %0, %0, t;\n\t}"
+        : "+r"(v)
+        : "r"(src), "r"(o), "r"(c));
+}
+__device__ __forceinline__ int32_t v2lo(uint32_t v) { return (int32_t)(v << 16) >> 16; }
+__device__ __forceinline__ int32_t v2hi(uint32_t v) { return (int32_t)v >> 16; }
+
+// Returns false (nothing written) when the chunk is not provably exact in 16 bits.
+// qa / qb: the lane's two code rows (ly, lz0) and (ly, lz0 + 1).
+__device__ __forceinline__ bool r3_chunk16(const R3Params &p, const uint4 qa, const uint4 qb, uint32_t k,
+                                          uint32_t lane, uint32_t &mn, uint32_t &mx, uint32_t rkey, int32_t rd,
+                                          uint32_t nrec, uint32_t ybuf_s) {
+    const uint32_t ly = lane & 7, lz0 = (lane >> 3) * 2;
+    const uint32_t nr = ((uint32_t)(-p.r) & 0xFFFFu) * 0x10001u;  // -r in both halves
+    uint32_t a[4] = {v2add(qa.x, nr), v2add(qa.y, nr), v2add(qa.z, nr), v2add(qa.w, nr)};
+    uint32_t b[4] = {v2add(qb.x, nr), v2add(qb.y, nr), v2add(qb.z, nr), v2add(qb.w, nr)};
+    // exactness: sum |q'| over the chunk (codes, then the outlier deltas) < 2^15
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        acc = v2add(acc, v2max(a[i], v2add(~a[i], 0x00010001u)));
+        acc = v2add(acc, v2max(b[i], v2add(~b[i], 0x00010001u)));
+    }
+    const bool mine_rec = lane < nrec && (rkey >> 9) == k;
+    const uint32_t dabs = mine_rec ? (uint32_t)min(abs(rd), 0x8000) : 0u;
+    const uint32_t S = __reduce_add_sync(f3::kFull, (acc & 0xFFFFu) + (acc >> 16) + dabs);
+    if (S >= 0x8000u) return false;
+    // outliers: q'[idx] += delta (mod 2^16 in its half)
+    for (uint32_t m = __ballot_sync(f3::kFull, mine_rec); m; m &= m - 1) {
+        const uint32_t i = __ffs(m) - 1;
+        const uint32_t key = __shfl_sync(f3::kFull, rkey, i);
+        const uint32_t d16 = (uint32_t)__shfl_sync(f3::kFull, rd, i) & 0xFFFFu;
+        const uint32_t lx = key & 7, oy = (key >> 3) & 7, oz = (key >> 6) & 7;
+        const bool own = oy == ly && (oz & ~1u) == lz0;
+        const uint32_t add = own ? (d16 << (16 * (lx & 1))) : 0u;
+        const uint32_t w = lx >> 1;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint32_t aj = (j == (int)w && !(oz & 1)) ? add : 0u, bj = (j == (int)w && (oz & 1)) ? add : 0u;
+            a[j] = v2add(a[j], aj);
+            b[j] = v2add(b[j], bj);
+        }
+    }
+    // x: inside each pair, then the running pair totals
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        a[i] = v2add(a[i], a[i] << 16);
+        b[i] = v2add(b[i], b[i] << 16);
+    }
+#pragma unroll
+    for (int i = 1; i < 4; i++) {
+        a[i] = v2add(a[i], __byte_perm(a[i - 1], 0, 0x3232));
+        b[i] = v2add(b[i], __byte_perm(b[i - 1], 0, 0x3232));
+    }
+    // y: previous rows in the 8-lane group
+#pragma unroll
+    for (uint32_t o = 1; o < 8; o <<= 1) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            v2_shfl_add(a[i], a[i], o, 0x1800u);
+            v2_shfl_add(b[i], b[i], o, 0x1800u);
+        }
+    }
+    // z: the lane's pair, then the groups of 8 lanes below
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        b[i] = v2add(b[i], a[i]);
+        uint32_t e = 0;
+        v2_shfl_add(e, b[i], 8, 0u);
+        const uint32_t s2 = v2add(e, b[i]);
+        v2_shfl_add(e, s2, 16, 0u);
+        a[i] = v2add(a[i], e);
+        b[i] = v2add(b[i], e);
+        mn = v2min(mn, v2min(a[i], b[i]));
+        mx = v2max(mx, v2max(a[i], b[i]));
+    }
+    // dequantise (f64 multiply, RN to f32) into the TMA tile
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const uint32_t(&v)[4] = h ? b : a;
+        float o[8];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            o[2 * i] = (float)__dmul_rn((double)v2lo(v[i]), p.two_eb);
+            o[2 * i + 1] = (float)__dmul_rn((double)v2hi(v[i]), p.two_eb);
+        }
+        const uint32_t sa = ybuf_s + (ly + 8 * (lz0 + h)) * 32;
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(sa), "f"(o[0]), "f"(o[1]), "f"(o[2]),
+                     "f"(o[3]));
+        asm volatile("st.shared.v4.f32 [%0+16], {%1, %2, %3, %4};" ::"r"(sa), "f"(o[4]), "f"(o[5]), "f"(o[6]),
+                     "f"(o[7]));
+    }
+    return true;
+}
+
 template <typename SymT, typename OutT, typename I>
 __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch, uint32_t k,
                                          uint64_t r0, uint64_t r1, uint32_t lane, OutT &vmin,
@@ -270,6 +392,8 @@ __global__ void __launch_bounds__(kR3Threads, TMA ? 2 : 3)
     const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(&s_stage[warp][0][0]) + lane * 16;
     constexpr uint32_t kBuf = 32 * 16 * sizeof(SymT);
     OutT vmin = (OutT)INFINITY, vmax = (OutT)-INFINITY;
+    uint32_t qmn = 0x7FFF7FFFu, qmx = 0x80008000u;  // packed int16 min / max of the 16-bit path's q
+    const bool narrow = p.r <= 2048;                 // cap <= 4096
     bool overflow = false;
     while (true) {
         uint64_t t = 0;
@@ -343,9 +467,20 @@ __global__ void __launch_bounds__(kR3Threads, TMA ? 2 : 3)
                     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                     __syncwarp();
                 }
-                r3_chunk<SymT, OutT, int32_t>(p, cur, k, r0, r1, lane, vmin, vmax, overflow,
-                                              cur_pf ? reinterpret_cast<const SymT *>(reinterpret_cast<const unsigned char *>(&s_stage[warp][sb][0]) + lane * 16) : nullptr,
-                                              reg_out, rkey, rd, nrec, yb);
+                const SymT *stg = cur_pf ? reinterpret_cast<const SymT *>(
+                                               reinterpret_cast<const unsigned char *>(&s_stage[warp][sb][0]) + lane * 16)
+                                         : nullptr;
+                bool done = false;
+                if constexpr (sizeof(SymT) == 2 && sizeof(OutT) == 4 && TMA) {
+                    // packed 16-bit partial sums when provably exact (cap <= 4096)
+                    if (narrow && reg_out && __all_sync(f3::kFull, cur_pf))
+                        done = r3_chunk16(p, reinterpret_cast<const uint4 *>(stg)[0],
+                                          reinterpret_cast<const uint4 *>(stg)[32], k, lane, qmn, qmx, rkey, rd, nrec,
+                                          yb);
+                }
+                if (!done)
+                    r3_chunk<SymT, OutT, int32_t>(p, cur, k, r0, r1, lane, vmin, vmax, overflow, stg, reg_out, rkey,
+                                                  rd, nrec, yb);
                 if (tma) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
@@ -360,6 +495,13 @@ __global__ void __launch_bounds__(kR3Threads, TMA ? 2 : 3)
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     if (TMA && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    {  // the 16-bit path's extremes: the dequantisation is monotone in q
+        const int32_t lo = min(v2lo(qmn), v2hi(qmn)), hi = max(v2lo(qmx), v2hi(qmx));
+        if (lo <= hi) {
+            vmin = fmin(vmin, (OutT)__dmul_rn((double)lo, p.two_eb));
+            vmax = fmax(vmax, (OutT)__dmul_rn((double)hi, p.two_eb));
+        }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         OutT a = __shfl_xor_sync(f3::kFull, vmin, o), b = __shfl_xor_sync(f3::kFull, vmax, o);

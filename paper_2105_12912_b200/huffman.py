@@ -96,10 +96,13 @@ def decode(stream: BitStream, book: Codebook) -> np.ndarray:
     st = N.empty_bytes(N.STATUS_BYTES)
     ds = L.lzb_huff_decode_scratch_bytes(stream.bit_len, maxlen, book.cap)
     scr = N.empty_bytes(ds)
-    N.check_rc(L.lzb_huff_decode(data.data_ptr(), stream.bit_len, stream.count, lens.data_ptr(),
-                                 book.cap, maxlen, out.data_ptr(), sb, st.data_ptr(),
-                                 scr.data_ptr(), ds, N.stream_ptr()), "huff_decode")
-    (s,) = N.read_status(st)
+    for fn in (L.lzb_huff_decode, L.lzb_huff_decode_robust):
+        N.check_rc(fn(data.data_ptr(), stream.bit_len, stream.count, lens.data_ptr(),
+                      book.cap, maxlen, out.data_ptr(), sb, st.data_ptr(),
+                      scr.data_ptr(), ds, N.stream_ptr()), "huff_decode")
+        (s,) = N.read_status(st)
+        if s.code != N.LZB_E_RETRY:  # else: a stream the fast decoder cannot resolve
+            break
     if s.code:
         raise CorruptArchiveError("bit stream does not decode to its declared symbols")
     if sb == 2:

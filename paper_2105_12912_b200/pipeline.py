@@ -45,6 +45,9 @@ _OUTLIER_DT = np.dtype([("index", "<u8"), ("delta", "<i8")])
 _WORKFLOW_ALIASES = {"auto": None, "huffman": Workflow.HUFFMAN, "huff": Workflow.HUFFMAN,
                      "rle": Workflow.RLE, "rlevle": Workflow.RLE_VLE}
 _MAX_RUN = 0xFFFFFFFF  # P/rle.py:14
+# the fused decode + reconstruct kernel (lzb_decompress_huff); off by default:
+# on C5 it measures slower than K5 (plan + final decode) followed by K6
+_FUSED = __import__("os").environ.get("LZB_FUSED", "0") == "1"
 
 
 @dataclass(frozen=True)
@@ -492,9 +495,10 @@ def decompress_device(arc, raw_host: bytes | None = None, prof=None, out=None):
     st = _pool.get("dstatus", 4 * N.STATUS_BYTES, dev)
     stp = _dev(st)
     st.zero_()
-    codes = _pool.get("dcodes", n * cb, dev)
     base = _dev(arc)
     sym_off, sym_len = hdr.symbols
+    huff = None  # (bits ptr, bit_len, count, maxlen) of the Huffman stream, if any
+    vals_rle = None
     if hdr.workflow is Workflow.HUFFMAN:
         if known is not None:  # written by compress_device: no host round trip
             bit_len, count, maxlen = known
@@ -509,12 +513,7 @@ def decompress_device(arc, raw_host: bytes | None = None, prof=None, out=None):
             raise CorruptArchiveError("bit stream data truncated")
         if count != n:
             raise CorruptArchiveError("decoded stream length does not match the grid")
-        ds = L.lzb_huff_decode_scratch_bytes(bit_len, maxlen, cap)
-        d_scr = _pool.get("d_scratch", ds, dev)
-        with _Stage(prof, "K5_huff_decode"):
-            N.check_rc(L.lzb_huff_decode(base + sym_off + 16, bit_len, count,
-                                         base + hdr.codebook[0], cap, maxlen, _dev(codes), cb,
-                                         stp, _dev(d_scr), ds, sp), "huff_decode")
+        huff = (base + sym_off + 16, bit_len, count, maxlen)
     else:
         if sym_len < 8:
             raise CorruptArchiveError("run section shorter than its count")
@@ -537,28 +536,71 @@ def decompress_device(arc, raw_host: bytes | None = None, prof=None, out=None):
             cbytes = np.frombuffer(host_bytes(hdr.codebook[0], sum(hdr.codebook)), np.uint8)
             maxlen = _validate_lengths_host(cbytes)
             vals = _pool.get("dvals", 4 * max(R, 1), dev)
-            ds = L.lzb_huff_decode_scratch_bytes(bit_len, maxlen, cap)
-            d_scr = _pool.get("d_scratch", ds, dev)
-            N.check_rc(L.lzb_huff_decode(base + sym_off + 24, bit_len, R, base + hdr.codebook[0],
-                                         cap, maxlen, _dev(vals), 4, stp, _dev(d_scr), ds, sp),
-                       "huff_decode")
+            vals_rle = (base + sym_off + 24, bit_len, R, maxlen, vals)
             vptr, lptr = _dev(vals), base + sym_off + 8 + sub
-        rs = L.lzb_rle_decode_scratch_bytes(R)
-        r_scr = _pool.get("rd_scratch", rs, dev)
-        N.check_rc(L.lzb_rle_decode(vptr, lptr, R, cap, _dev(codes), cb, n,
-                                    stp + N.STATUS_BYTES, _dev(r_scr), rs, sp), "rle_decode")
     out_off, out_len = hdr.outliers
     dtn = torch.float32 if hdr.dtype == "f32" else torch.float64
     y = out if out is not None else torch.empty(n, dtype=dtn, device=dev)
     g = N.geom(dims.as_tuple(), chunk.as_tuple())
-    rcs = L.lzb_reconstruct_scratch_bytes(g, hdr.outlier_count)
-    rc_scr = _pool.get("rc_scratch", rcs, dev)
-    with _Stage(prof, "K6_reconstruct"):
-        N.check_rc(L.lzb_reconstruct(_dev(codes), cb, base + out_off, hdr.outlier_count, g,
-                                     hdr.eb_abs, cap, y.data_ptr(), _DTYPE_CODES[hdr.dtype], None,
-                                     stp + 2 * N.STATUS_BYTES, _dev(rc_scr), rcs, sp),
-                   "reconstruct")
-    sd, sr, sk = N.read_status(st[: 3 * N.STATUS_BYTES])  # the one sync
+
+    dtc = _DTYPE_CODES[hdr.dtype]
+    # Huffman archives of whole 8^3 chunks (f32): K5 decodes tile by tile
+    # straight into K6's shared memory (lzb_decompress_huff), no code array
+    fused = huff is not None and bool(L.lzb_decompress_fused_ok(g, cap, dtc)) and _FUSED
+
+    def run(robust: bool) -> None:
+        """Launch the decode + reconstruct kernels (no host sync)."""
+        if fused and not robust:
+            bptr, bit_len, count, maxlen = huff
+            fs = L.lzb_decompress_scratch_bytes(g, bit_len, count, cap, hdr.outlier_count)
+            f_scr = _pool.get("f_scratch", fs, dev)
+            with _Stage(prof, "K5K6_decode_reconstruct"):
+                N.check_rc(L.lzb_decompress_huff(bptr, bit_len, count, base + hdr.codebook[0], cap, maxlen,
+                                                 base + out_off, hdr.outlier_count, g, hdr.eb_abs,
+                                                 y.data_ptr(), dtc, stp, _dev(f_scr), fs, sp),
+                           "decompress")
+            return
+        dec = L.lzb_huff_decode_robust if robust else L.lzb_huff_decode
+        codes = _pool.get("dcodes", n * cb, dev)
+        if huff is not None:
+            bptr, bit_len, count, maxlen = huff
+            ds = L.lzb_huff_decode_scratch_bytes(bit_len, maxlen, cap)
+            d_scr = _pool.get("d_scratch", ds, dev)
+            with _Stage(prof, "K5_huff_decode"):
+                N.check_rc(dec(bptr, bit_len, count, base + hdr.codebook[0], cap, maxlen, _dev(codes), cb,
+                               stp, _dev(d_scr), ds, sp), "huff_decode")
+        else:
+            if vals_rle is not None:
+                vb, bit_len, R_, maxlen, vals = vals_rle
+                ds = L.lzb_huff_decode_scratch_bytes(bit_len, maxlen, cap)
+                d_scr = _pool.get("d_scratch", ds, dev)
+                N.check_rc(dec(vb, bit_len, R_, base + hdr.codebook[0], cap, maxlen, _dev(vals), 4,
+                               stp, _dev(d_scr), ds, sp), "huff_decode")
+            rs = L.lzb_rle_decode_scratch_bytes(R)
+            r_scr = _pool.get("rd_scratch", rs, dev)
+            N.check_rc(L.lzb_rle_decode(vptr, lptr, R, cap, _dev(codes), cb, n,
+                                        stp + N.STATUS_BYTES, _dev(r_scr), rs, sp), "rle_decode")
+        rcs = L.lzb_reconstruct_scratch_bytes(g, hdr.outlier_count)
+        rc_scr = _pool.get("rc_scratch", rcs, dev)
+        with _Stage(prof, "K6_reconstruct"):
+            N.check_rc(L.lzb_reconstruct(_dev(codes), cb, base + out_off, hdr.outlier_count, g,
+                                         hdr.eb_abs, cap, y.data_ptr(), _DTYPE_CODES[hdr.dtype], None,
+                                         stp + 2 * N.STATUS_BYTES, _dev(rc_scr), rcs, sp),
+                       "reconstruct")
+
+    run(False)
+    if fused:
+        (sf,) = N.read_status(st[: N.STATUS_BYTES])  # the one sync
+        if sf.code == N.LZB_OK:
+            return y, hdr, sf.f64(0), sf.f64(1)
+        # retry or any error: the separate robust stages give the exact verdict
+        run(True)
+        sd, sr, sk = N.read_status(st[: 3 * N.STATUS_BYTES])
+    else:
+        sd, sr, sk = N.read_status(st[: 3 * N.STATUS_BYTES])  # the one sync
+    if sd.code == N.LZB_E_RETRY:  # a stream the fast decoder cannot resolve (rare)
+        run(True)
+        sd, sr, sk = N.read_status(st[: 3 * N.STATUS_BYTES])
     N.raise_for(sd, "decode", "bit stream does not decode to its declared symbols")
     N.raise_for(sr, "rle_decode", "run section does not decode to the grid")
     if sk.code == N.LZB_E_CORRUPT:

@@ -3,7 +3,7 @@
 TAG=${1:-q}
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k 'regex:lzb|k_' \
   --log-file gpurun_out/launches_${TAG}.csv \
-  python bench.py --config c5q --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/launches_${TAG}.log 2>&1
+  python bench.py --config c5q --steps 1 --warmup 3 --no-cpu-baseline --no-parity --e2e-steps 0 > gpurun_out/launches_${TAG}.log 2>&1
 python3 - "$TAG" <<'PY'
 import csv, sys, collections
 tag = sys.argv[1]
