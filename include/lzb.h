@@ -91,6 +91,17 @@ int lzb_prequantize(const void *x, int dtype, uint64_t n, double eb_abs, int64_t
                     lzb_dstatus *st, void *stream);
 
 /* ---------------------------------------------------------------------
+ * Verification hook for K1's fast prequantizers (the f32 double-single and
+ * f64 magic-number paths that replace the reference's f64 division,
+ * P/quantize.py:95-110).  dtype 0: the f32 bit patterns [lo, lo + count);
+ * dtype 1: `count` f64 values from hashed bit patterns starting at lo.
+ * st->u[0] = fast results that disagree with the exact rule (must be 0),
+ * u[1] = inputs the fast path accepted, u[2] = finite inputs examined.
+ * ------------------------------------------------------------------- */
+int lzb_prequant_verify(double eb_abs, uint64_t lo, uint64_t count, int dtype, lzb_dstatus *st,
+                        void *stream);
+
+/* ---------------------------------------------------------------------
  * K1: fused prequantize + Lorenzo delta + quant code + histogram +
  * outlier gather, emitting the CHUNK-MAJOR symbol stream.
  * Replaces prequantize + construct_grid + gather_chunk_major + histogram

@@ -880,6 +880,70 @@ extern "C" int lzb_prequantize(const void *x, int dtype, uint64_t n, double eb_a
 }
 
 // ----------------------------------------------------------------------------
+// Verification of K1's fast prequantizers against the exact reference rule
+// (P/quantize.py:95-110): f32 inputs exhaustively by bit pattern range, f64
+// inputs on hashed bit patterns.  A fast result that is ACCEPTED must equal
+// the exact one (value, and no overflow / assert flag); rejected inputs take
+// the exact path in K1, so they cannot disagree.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t pq_mix(uint64_t z) {  // splitmix64
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_pq_verify(uint64_t lo, uint64_t count, int dtype, double two_eb, double slack, double inv,
+                            float inv_hi, float inv_lo, unsigned long long *cnt) {
+    unsigned long long bad = 0, fast = 0, finite = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        double v;
+        bool ok = true;
+        int64_t f;
+        if (dtype == 0) {
+            const float x = __uint_as_float((uint32_t)(lo + i));
+            if (!isfinite(x)) continue;
+            f = f3::pq_fast_f32(x, inv_hi, inv_lo, ok);
+            v = (double)x;
+        } else {
+            v = __longlong_as_double((long long)pq_mix(lo + i));
+            if (!isfinite(v)) continue;
+            f = f3::pq_fast(v, inv, ok);
+        }
+        finite++;
+        if (!ok) continue;
+        fast++;
+        int flags = 0;
+        const int64_t e = prequant(v, two_eb, slack, flags);
+        if (flags || e != f) bad++;
+    }
+    bad = __reduce_add_sync(0xffffffffu, (unsigned)bad);
+    fast = __reduce_add_sync(0xffffffffu, (unsigned)fast);
+    finite = __reduce_add_sync(0xffffffffu, (unsigned)finite);
+    if (lane_id() == 0) {
+        if (bad) atomicAdd(&cnt[0], bad);
+        atomicAdd(&cnt[1], fast);
+        atomicAdd(&cnt[2], finite);
+    }
+}
+
+extern "C" int lzb_prequant_verify(double eb_abs, uint64_t lo, uint64_t count, int dtype, lzb_dstatus *st,
+                                   void *stream) {
+    if (!st || (dtype != 0 && dtype != 1) || !(eb_abs > 0)) return LZB_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
+    if (count == 0) return LZB_OK;
+    const double inv = 1.0 / (2.0 * eb_abs);  // exactly as lzb_quantize derives it
+    const float inv_hi = (float)inv, inv_lo = (float)(inv - (double)inv_hi);
+    unsigned grid = (unsigned)umin64((count + 255) / 256, (uint64_t)device_sms() * 32);
+    k_pq_verify<<<grid, 256, 0, s>>>(lo, count, dtype, 2.0 * eb_abs, eb_abs * (1.0 + 1e-12), inv, inv_hi,
+                                     inv_lo, reinterpret_cast<unsigned long long *>(st->u));
+    LZB_LAUNCH_CHECK();
+    return LZB_OK;
+}
+
+// ----------------------------------------------------------------------------
 // Grid <-> chunk-major reorder (P/pipeline.py:102-117)
 // ----------------------------------------------------------------------------
 template <typename T>

@@ -331,3 +331,24 @@ def test_reconstruct_fuse_and_layout_kats_on_device(golden, cuda):
     back = lzb.pipeline.scatter_chunk_major(np.array(k["chunk_major_4x2"], np.uint32), lzb.Dims.of(4, 2),
                                    lzb.ChunkSpec(2, 2))
     assert back.codes.tolist() == list(range(8))
+
+
+@pytest.mark.slow
+def test_fast_prequant_exhaustive_f32(cuda):
+    """K1's f32 fast prequantizer against the exact reference rule
+    (P/quantize.py:95-110) on EVERY f32 bit pattern (4,278,190,080 finite
+    values) for six error bounds, plus 2^28 hashed f64 values for the f64
+    fast path: 0 mismatches among the accepted fast results."""
+    from paper_2105_12912_b200 import _native as N
+
+    L = N.lib()
+    st = N.empty_bytes(N.STATUS_BYTES)
+    for eb in (1e-4, 2.9345040893554688e-2, 0.5, 1e-7, 123.456, 3.0e-3 / 7):
+        N.check_rc(L.lzb_prequant_verify(eb, 0, 1 << 32, 0, st.data_ptr(), N.stream_ptr()), "verify")
+        (s,) = N.read_status(st)
+        assert s.u[2] == (1 << 32) - 2 * (1 << 23), eb  # every finite f32 examined
+        assert s.u[1] > 0, eb
+        assert s.u[0] == 0, (eb, s.u[0])
+        N.check_rc(L.lzb_prequant_verify(eb, 12345, 1 << 28, 1, st.data_ptr(), N.stream_ptr()), "verify")
+        (s,) = N.read_status(st)
+        assert s.u[0] == 0, (eb, "f64", s.u[0])
