@@ -277,7 +277,6 @@ def stage_bytes(name, n, s, arc_bits_bytes, n_out):
         "K3_huff_encode": n * 2 + arc_bits_bytes,
         "K5_huff_decode": arc_bits_bytes + n * 2,
         "K6_reconstruct": n * 2 + 16 * n_out + n * s,
-        "K5K6_decode_reconstruct": arc_bits_bytes + 16 * n_out + n * s,
     }.get(name)
 
 

@@ -263,26 +263,6 @@ int lzb_rle_decode(const uint8_t *values_le, const uint8_t *lengths_le, uint64_t
                    void *scratch, size_t scratch_bytes, void *stream);
 
 /* ---------------------------------------------------------------------
- * Fused K5 + K6: decompress a Huffman archive's symbol stream straight into
- * the field (replaces lzebc.decompress's Huffman branch, P/pipeline.py:318-326
- * = decode P/huffman.py:64-122 + scatter P/pipeline.py:108-117 + fuse /
- * partial sums / dequantize P/reconstruct.py:22-88).  Tiles of 16 chunks
- * are decoded into shared memory and reconstructed there; the symbol stream
- * never reaches HBM.  Eligible grids (lzb_decompress_fused_ok): ChunkSpec
- * (8,8,8), nx/ny/nz multiples of 8, f32 output, cap <= 65536.  `y` is
- * 16-byte aligned.  On return st->code = 0 and st->u[0]/u[1] = f64 bits of
- * the output min/max; any other code (LZB_E_RETRY included) means: decode
- * with lzb_huff_decode(_robust) + lzb_reconstruct for the exact verdict.
- * ------------------------------------------------------------------- */
-int lzb_decompress_fused_ok(const lzb_geom *g, uint32_t cap, int dtype);
-size_t lzb_decompress_scratch_bytes(const lzb_geom *g, uint64_t bit_len, uint64_t count, uint32_t cap,
-                                    uint64_t n_out);
-int lzb_decompress_huff(const uint8_t *bits, uint64_t bit_len, uint64_t count, const uint8_t *lengths,
-                        uint32_t cap, uint32_t maxlen, const uint8_t *outliers, uint64_t n_out,
-                        const lzb_geom *g, double eb_abs, void *y, int dtype, lzb_dstatus *st,
-                        void *scratch, size_t scratch_bytes, void *stream);
-
-/* ---------------------------------------------------------------------
  * K6: fused outlier fuse + chunk-wise multi-dimensional partial-sum
  * reconstruction + dequantization + range/finiteness.  Replaces
  * scatter_chunk_major + _decode_outliers validation + reconstruct_grid +

@@ -63,9 +63,6 @@ SIGNATURES = {
     "lzb_rle_encode": (_I, [_P, _I, _U64, _P, _P, _U64, _U64, _P, _P, _SZ, _P]),
     "lzb_rle_decode_scratch_bytes": (_SZ, [_U64]),
     "lzb_rle_decode": (_I, [_P, _P, _U64, _U32, _P, _I, _U64, _P, _P, _SZ, _P]),
-    "lzb_decompress_fused_ok": (_I, [_GP, _U32, _I]),
-    "lzb_decompress_scratch_bytes": (_SZ, [_GP, _U64, _U64, _U32, _U64]),
-    "lzb_decompress_huff": (_I, [_P, _U64, _U64, _P, _U32, _U32, _P, _U64, _GP, _D, _P, _I, _P, _P, _SZ, _P]),
     "lzb_reconstruct_scratch_bytes": (_SZ, [_GP, _U64]),
     "lzb_reconstruct": (_I, [_P, _I, _P, _U64, _GP, _D, _U32, _P, _I, _P, _P, _P, _SZ, _P]),
     "lzb_dequantize": (_I, [_P, _U64, _D, _P, _I, _P, _P]),

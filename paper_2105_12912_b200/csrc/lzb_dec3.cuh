@@ -500,15 +500,15 @@ __global__ void __launch_bounds__(kF9Warps * 32, 1) k_dec_final9(DecParams p, ui
         d3_stage(p, t + nw, str_s + (sb ^ 1) * kStgWords * 4, lane);
         d3_stage_wait();
         const uint32_t *stg = wstr + sb * kStgWords;
-        const bool plan = p.pmboff != nullptr;
+        const bool plan = p.psoff != nullptr;
         const uint32_t e = plan ? (p.cp[t * 32] & 0xFFu) : p.ent0[t];
         if (e == kExitInvalid || e == kExitEnd) continue;
         const uint64_t t0 = t * kS3;
         const bool last = t == p.T - 1;
         const uint32_t stop = last ? (uint32_t)(p.bit_len - t0) : kS3;
         const uint32_t la = (stop + kMB - 1) / kMB - 1;
-        const uint64_t base = plan ? p.pmboff[t * 32] : p.off0[t];
-        const uint64_t endo = last ? p.count : plan ? p.pmboff[(t + 1) * 32] : p.off0[t + 1];
+        const uint64_t base = plan ? p.psoff[t] : p.off0[t];
+        const uint64_t endo = last ? p.count : plan ? p.psoff[t + 1] : p.off0[t + 1];
         const uint32_t total = (uint32_t)(endo - base);
         const uint32_t b = lane * kMB;
         const bool act = lane <= la;

@@ -27,13 +27,17 @@
 //   128 bits), any invalid code word, a count mismatch or a missing END
 //   raises LZB_E_RETRY: the caller then runs the exhaustive decoder
 //   (lzb_huff_decode_robust, transfer maps over every entry phase), which
-//   also adjudicates corrupt streams.  Outputs: every microblock's true entry,
-//   count and first symbol offset, and for every tile of kD4Tile symbols the
-//   microblock holding its first symbol.
-// Tile decode (d4_tile_decode): the microblocks overlapping a tile decode in
-// parallel (thread per microblock) into a shared-memory u16 tile; consumers
-// are k_dec4_emit (copies the tile to a code array) and the fused K5+K6
-// kernel in lzb_recon.cu (reconstructs the tile's chunks in place).
+//   also adjudicates corrupt streams.  Outputs: every microblock's true entry
+//   and count, every subsequence's first symbol offset.
+// The final decode (k_dec_final9 in plan mode, lzb_dec3.cuh) then writes the
+// symbols: warp per subsequence, lane per microblock from its planned entry.
+//
+// Measured and rejected (C5q, 512x2048^2 f32): fusing the final decode into
+// K6 (tiles of chunks decoded straight into shared memory and reconstructed
+// there, no code array in HBM) -- 6.5 ms for the fused kernel against 2.4 ms
+// (final decode) + 2.9 ms (K6) separately: the fused CTA either idles its
+// lanes on partially covered tiles or runs at 16-24 resident warps, and the
+// thread-per-microblock decode chains are latency-bound at that occupancy.
 #pragma once
 
 #include "lzb_common.cuh"
@@ -44,7 +48,6 @@ namespace lzb {
 constexpr uint32_t kFullMask = 0xffffffffu;
 constexpr uint32_t kD4MB = 128;            // bits per microblock (lane)
 constexpr uint32_t kD4S = 32 * kD4MB;      // bits per subsequence (warp)
-constexpr uint32_t kD4Tile = 4096;         // symbols per decode tile (8 chunks of 8^3)
 constexpr uint8_t kD4Bad = 0xFF;
 constexpr int kD4Warps = 8;                // k_dec4_count CTA
 constexpr int kD4ResolveThreads = 256;     // k_dec4_resolve CTA (one subsequence per thread)
@@ -56,13 +59,11 @@ struct D4Plan {
     uint64_t bit_len, count;
     uint64_t T;       // subsequences
     uint64_t nmb;     // microblocks holding stream bits
-    uint64_t ntiles;  // ceil(count / kD4Tile)
     const DecTables *tab;
     const uint32_t *syms;  // symbols in (length, symbol) order
     int32_t base8;         // lut8 byte deltas are relative to this symbol
     uint16_t *cp;     // per microblock (32 T): count << 8 | entry offset
-    uint64_t *mboff;  // per microblock: stream index of its first code word's symbol
-    uint64_t *tfirst; // per tile (+1 sentinel): microblock holding the tile's first symbol
+    uint64_t *soff;   // per subsequence: stream index of its first code word's symbol
     uint64_t *sbm;    // per subsequence: lane 0 phase-0 starts in bits 0..63
     uint32_t *srest;  // per subsequence: code words of lanes 1..31 (chain)
     uint8_t *sx0;     // per subsequence: lane 0 phase-0 exit (kD4Bad: invalid)
@@ -304,151 +305,6 @@ __device__ __forceinline__ uint32_t d4_rank64(uint64_t bm, uint32_t q) {  // set
     return __popcll(bm & ((1ull << q) - 1ull));
 }
 
-// ---------------------------------------------------------------------------
-// Tile decode: one microblock's code words into a u16 tile [A, A + kD4Tile)
-// of the symbol stream (stage = the tile in shared memory).  Symbols decoded
-// past the microblock's last code word belong to the next microblock and are
-// written with their true values (same path), so overlaps are harmless.
-// ---------------------------------------------------------------------------
-struct D4Luts {
-    const uint64_t *lut8;  // DecTables::lut8 (byte deltas, 6 code words) in global memory
-    uint32_t lut8_s;       // ... or its copy in shared memory (shared address; 0 = none)
-    uint32_t bb;      // base8 in both 16-bit halves
-    const uint8_t *lut1;
-    const uint16_t *lut1s;
-    const DecCanon *can;
-    const uint32_t *syms;
-};
-
-__device__ __forceinline__ uint64_t lds64(uint32_t a) {
-    uint64_t v;
-    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sts16(uint16_t *p, uint32_t v) { *p = (uint16_t)v; }
-__device__ __forceinline__ uint32_t add16x2(uint32_t a, uint32_t b) {  // per-half add, no carry between
-    uint32_t d;
-    asm("add.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-    return d;
-}
-
-template <uint32_t TS, typename Rd>
-__device__ __forceinline__ void d4_tile_decode_rd(Rd &r, const D4Luts &L, int32_t j0, uint32_t kend,
-                                                  uint16_t *stage) {
-    // Shared-memory stores are the decoder's bottleneck (lanes write to
-    // scattered positions: every store instruction costs several wavefronts),
-    // so symbols leave as aligned u16 PAIRS: three 32-bit stores per LUT step.
-    // For an odd position the first pair is completed with `last`, the lane's
-    // previous symbol.  Slots past the step's n symbols are overwritten by the
-    // lane's next step, so the paired path is used only while six more of the
-    // microblock's own code words remain; the rest go symbol by symbol.
-    uint32_t *stage32 = reinterpret_cast<uint32_t *>(stage);
-    uint32_t k = 0, last = 0;
-    while (k < kend) {
-        const uint32_t pk = r.peek12();
-        const uint64_t e = L.lut8_s ? lds64(L.lut8_s + 8 * pk) : __ldg(&L.lut8[pk]);
-        const uint32_t hi = (uint32_t)(e >> 32), lo = (uint32_t)e;
-        const uint32_t n = (hi >> 16) & 7u;
-        const int32_t j = j0 + (int32_t)k;
-        if (n == 0) {  // a code word longer than the LUT, or a symbol outside the byte window
-            const uint32_t l1 = __ldg(&L.lut1[pk]);
-            uint32_t sym = 0, len = 0;
-            if (l1 & 0x80u) {
-                len = d4_sym_long(L.can, L.syms, r.peek64(), l1 & 0x7Fu, sym);
-            } else {
-                len = l1;
-                sym = __ldg(&L.lut1s[pk]);
-            }
-            if (len == 0) return;  // unreachable on a resolved stream (pass M checked it)
-            if (k > 0 && j >= 1 && j <= (int32_t)TS) stage[j - 1] = (uint16_t)last;  // see below
-            if ((uint32_t)j < TS) stage[j] = (uint16_t)sym;
-            last = sym;
-            k++;
-            r.adv64(len);
-            continue;
-        }
-        // the six byte deltas as u16 symbol pairs
-        const uint32_t s01 = add16x2(__byte_perm(lo, 0, 0x4140), L.bb);
-        const uint32_t s23 = add16x2(__byte_perm(lo, 0, 0x4342), L.bb);
-        const uint32_t s45 = add16x2(__byte_perm(hi, 0, 0x4140), L.bb);
-        if (k > 0 && k + 6 <= kend && j >= 1 && j + 6 <= (int32_t)TS) {
-            const bool odd = j & 1;
-            const uint32_t w0 = odd ? __byte_perm(last, s01, 0x5410) : s01;  // (last, s0) or (s0, s1)
-            const uint32_t w1 = odd ? __funnelshift_r(s01, s23, 16) : s23;   // (s1, s2) or (s2, s3)
-            const uint32_t w2 = odd ? __funnelshift_r(s23, s45, 16) : s45;   // (s3, s4) or (s4, s5)
-            uint32_t *d = stage32 + ((j - (odd ? 1 : 0)) >> 1);
-#ifdef LZB_DBG_NOSTORE
-            if (w0 == 0x12345678u && w1 == w2) d[0] = w0;  // keep the work, drop the stores
-#else
-            d[0] = w0;
-            d[1] = w1;
-            d[2] = w2;
-#endif
-        } else {  // exactly the n decoded symbols that fall inside the tile
-            // (and the previous symbol again: an odd paired step leaves its last one to us)
-            if (k > 0 && j >= 1 && j <= (int32_t)TS) stage[j - 1] = (uint16_t)last;
-            const int32_t from = j < 0 ? -j : 0;
-            const int32_t to = min((int32_t)n, (int32_t)TS - j);
-            if (from <= 0 && 0 < to) stage[j] = (uint16_t)s01;
-            if (from <= 1 && 1 < to) stage[j + 1] = (uint16_t)(s01 >> 16);
-            if (from <= 2 && 2 < to) stage[j + 2] = (uint16_t)s23;
-            if (from <= 3 && 3 < to) stage[j + 3] = (uint16_t)(s23 >> 16);
-            if (from <= 4 && 4 < to) stage[j + 4] = (uint16_t)s45;
-            if (from <= 5 && 5 < to) stage[j + 5] = (uint16_t)(s45 >> 16);
-        }
-        // the step's last symbol (for an odd-aligned next step)
-        const uint32_t lp = n <= 2 ? s01 : n <= 4 ? s23 : s45;
-        last = (n & 1) ? (lp & 0xFFFFu) : (lp >> 16);
-        k += n;
-        r.adv((hi >> 19) & 15u);
-    }
-    const int32_t jl = j0 + (int32_t)k - 1;  // the final symbol (a paired odd step may have left it)
-    if (k > 0 && jl >= 0 && jl < (int32_t)TS) stage[jl] = (uint16_t)last;
-}
-
-// microblock m from global memory (tiles whose bits exceed the word stage)
-__device__ __forceinline__ void d4_tile_decode_mb(const D4Plan &p, const D4Luts &L, uint64_t m, uint64_t A,
-                                                  uint16_t *stage) {
-    const uint32_t cpv = p.cp[m];
-    const uint32_t c = cpv >> 8;
-    const uint64_t o = p.mboff[m];
-    if (c == 0 || o + c <= A || o >= A + kD4Tile) return;
-    D4Win r;
-    d4_window(p, m, cpv & 0xFFu, r);
-    d4_tile_decode_rd<kD4Tile>(r, L, (int32_t)((int64_t)o - (int64_t)A), (uint32_t)umin64(c, A + kD4Tile - o), stage);
-}
-
-// microblock m from the tile's word stage (stream words [wlo, ...) at stg_s)
-__device__ __forceinline__ void d4_tile_decode_mb_s(const D4Plan &p, const D4Luts &L, uint64_t m, uint64_t A,
-                                                    uint16_t *stage, uint32_t stg_s, uint64_t wlo) {
-    const uint32_t cpv = p.cp[m];
-    const uint32_t c = cpv >> 8;
-    const uint64_t o = p.mboff[m];
-    if (c == 0 || o + c <= A || o >= A + kD4Tile) return;
-    SRd r;
-    r.init(stg_s, (uint32_t)((uint64_t)p.head + m * kD4MB - 32 * wlo) + (cpv & 0xFFu));
-    d4_tile_decode_rd<kD4Tile>(r, L, (int32_t)((int64_t)o - (int64_t)A), (uint32_t)umin64(c, A + kD4Tile - o), stage);
-}
-
-// microblock m with its plan entry (cpv, o) already at hand (staged)
-__device__ __forceinline__ void d4_tile_decode_mb_v(const D4Plan &p, const D4Luts &L, uint64_t m, uint32_t cpv,
-                                                    uint64_t o, uint64_t A, uint16_t *stage, uint32_t stg_s,
-                                                    uint64_t wlo) {
-    const uint32_t c = cpv >> 8;
-    if (c == 0 || o + c <= A || o >= A + kD4Tile) return;
-    SRd r;
-    r.init(stg_s, (uint32_t)((uint64_t)p.head + m * kD4MB - 32 * wlo) + (cpv & 0xFFu));
-    d4_tile_decode_rd<kD4Tile>(r, L, (int32_t)((int64_t)o - (int64_t)A), (uint32_t)umin64(c, A + kD4Tile - o), stage);
-}
-
-// The tile's microblocks [ma, mb] read stream words [wlo, wlo + nw).
-__device__ __forceinline__ void d4_tile_words(const D4Plan &p, uint64_t ma, uint64_t mb, uint64_t &wlo,
-                                              uint32_t &nw) {
-    wlo = ((uint64_t)p.head + ma * kD4MB) >> 5;
-    const uint64_t whi = (((uint64_t)p.head + (mb + 1) * kD4MB) >> 5) + 4;  // + a 64-bit code word + peek
-    nw = (uint32_t)umin64(whi - wlo, 0xFFFFFFFFu);
-}
-
 // Asynchronous copy of stream words [wlo, wlo + nw) into shared memory at
 // dst_s (4-byte pieces, zero past the stream), by threads tid = 0..nthr-1.
 __device__ __forceinline__ void d4_stage_words(const D4Plan &p, uint64_t wlo, uint32_t nw, uint32_t dst_s,
@@ -595,7 +451,6 @@ __global__ void __launch_bounds__(kD4Warps * 32) k_dec4_count(D4Plan p) {
 __global__ void __launch_bounds__(kD4ResolveThreads) k_dec4_resolve(D4Plan p) {
     __shared__ uint64_t s_scan[33];
     __shared__ uint64_t s_tile, s_ex;
-    __shared__ uint64_t s_off[kD4ResolveThreads];
     __shared__ int s_retry;
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     const uint64_t ntl = (p.T + kD4ResolveThreads - 1) / kD4ResolveThreads;
@@ -650,85 +505,17 @@ __global__ void __launch_bounds__(kD4ResolveThreads) k_dec4_resolve(D4Plan p) {
         if (retry) s_retry = 1;
         __syncthreads();
         const uint64_t soff = s_ex + off;
-        s_off[threadIdx.x] = soff;
         if (s < p.T) {
             p.cp[s * 32] = (uint16_t)((cnt0 << 8) | e);
             if (s == p.T - 1 && soff + total != p.count) s_retry = 1;
         }
         __syncthreads();
-        if (s_retry) {
-            if (threadIdx.x == 0) set_status(p.st, LZB_E_RETRY);
-        } else {
-            // per-microblock offsets and tile starts, one subsequence per warp step
-            for (uint32_t j = 0; j < 32; j++) {
-                const uint64_t ss = tl * kD4ResolveThreads + warp * 32 + j;
-                if (ss >= p.T) break;
-                const uint64_t mm = ss * 32 + lane;
-                const uint32_t c = p.cp[mm] >> 8;
-                uint32_t inc = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t v = __shfl_up_sync(kFullMask, inc, o);
-                    if (lane >= (uint32_t)o) inc += v;
-                }
-                const uint64_t o = s_off[warp * 32 + j] + inc - c;
-                p.mboff[mm] = o;
-                if (c) {
-                    const uint64_t kt = (o + kD4Tile - 1) / kD4Tile;
-                    if (kt * kD4Tile < o + c) p.tfirst[kt] = mm;
-                }
-                if (mm == p.nmb - 1) p.tfirst[p.ntiles] = mm;
-            }
-        }
+        if (s_retry && threadIdx.x == 0) set_status(p.st, LZB_E_RETRY);
+        if (s < p.T) p.soff[s] = soff;
         __syncthreads();
     }
 }
 
-// ---------------------------------------------------------------------------
-// Tile decode -> code array (consumers other than the fused 3D kernel)
-// ---------------------------------------------------------------------------
-constexpr int kD4EmitThreads = 256;
-constexpr uint32_t kD4TileWords = 1024;  // word stage per tile (4 KB: up to 8 bits per symbol)
-
-__global__ void __launch_bounds__(kD4EmitThreads) k_dec4_emit(D4Plan p, uint16_t *out) {
-    __shared__ __align__(16) uint16_t s_tile[kD4Tile];
-    __shared__ __align__(16) uint32_t s_w[kD4TileWords];
-    __shared__ DecCanon s_can;
-    load_canon(s_can, p.tab);
-    __syncthreads();
-    if (p.st->code) return;
-    const uint32_t b8 = (uint32_t)p.base8 & 0xFFFFu;
-    const D4Luts L{p.tab->lut8, 0u, b8 | (b8 << 16), p.tab->lut1, p.tab->lut1s, &s_can, p.syms};
-    const uint32_t w_s = smem_addr(s_w);
-    for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        const uint64_t A = t * kD4Tile;
-        const uint64_t ma = p.tfirst[t], mb = p.tfirst[t + 1];
-        uint64_t wlo;
-        uint32_t nw;
-        d4_tile_words(p, ma, mb, wlo, nw);
-        const bool staged = nw <= kD4TileWords;
-        if (staged) {
-            d4_stage_words(p, wlo, nw, w_s, threadIdx.x, blockDim.x);
-            asm volatile("cp.async.commit_group;" ::: "memory");
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            __syncthreads();
-            for (uint64_t m = ma + threadIdx.x; m <= mb; m += blockDim.x)
-                d4_tile_decode_mb_s(p, L, m, A, s_tile, w_s, wlo);
-        } else {
-            for (uint64_t m = ma + threadIdx.x; m <= mb; m += blockDim.x) d4_tile_decode_mb(p, L, m, A, s_tile);
-        }
-        __syncthreads();
-        const uint32_t n = (uint32_t)umin64(kD4Tile, p.count - A);
-        if (n == kD4Tile && (reinterpret_cast<uintptr_t>(out + A) & 15) == 0) {
-            const uint4 *src = reinterpret_cast<const uint4 *>(s_tile);
-            uint4 *dst = reinterpret_cast<uint4 *>(out + A);
-            for (uint32_t i = threadIdx.x; i < kD4Tile / 8; i += blockDim.x) dst[i] = src[i];
-        } else {
-            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[A + i] = s_tile[i];
-        }
-        __syncthreads();
-    }
-}
 #endif  // LZB_DEC4_KERNELS
 
 }  // namespace lzb

@@ -659,9 +659,9 @@ struct DecParams {
     unsigned int *nonuni;  // count of subsequences whose valid entries exit differently
     uint64_t *ulb;     // look-back words of the uniform scan
     unsigned int *uticket;
-    // plan mode (K5 v4, lzb_dec4.cuh): entries / offsets from the plan's
-    // per-microblock arrays (cp above, these offsets), no irregular entries
-    const uint64_t *pmboff;
+    // plan mode (K5 v4, lzb_dec4.cuh): entries from the plan's per-microblock
+    // cp (above), offsets per subsequence, no irregular entries
+    const uint64_t *psoff;
     // bit-range mode (multi-GPU decode of one stream, lzb_huff_range_*):
     // the range starts in phase entry0 and must leave in phase exit_expect
     // (kExitEnd when it ends the stream); an open range's last subsequence
@@ -1210,14 +1210,13 @@ static int dev_sms() {
 }
 
 // ---- K5 v4 plan (lzb_dec4.cuh) ----
-// scratch order: tables, syms, cp, mboff, tfirst, sbm, srest, sx0, sexit, look-back + ticket
-static void d4_sizes(ScratchSize &sc, uint64_t T, uint64_t ntiles, uint32_t cap) {
+// scratch order: tables, syms, cp, soff, sbm, srest, sx0, sexit, look-back + ticket
+static void d4_sizes(ScratchSize &sc, uint64_t T, uint32_t cap) {
     const uint64_t ntl = (T + kD4ResolveThreads - 1) / kD4ResolveThreads;
     sc.take<DecTables>(1);
     sc.take<uint32_t>(cap);
     sc.take<uint16_t>(32 * T);
-    sc.take<uint64_t>(32 * T);
-    sc.take<uint64_t>(ntiles + 1);
+    sc.take<uint64_t>(T);
     sc.take<uint64_t>(T);
     sc.take<uint32_t>(T);
     sc.take<uint8_t>(T);
@@ -1225,13 +1224,12 @@ static void d4_sizes(ScratchSize &sc, uint64_t T, uint64_t ntiles, uint32_t cap)
     sc.take<uint64_t>(ntl + 2);
 }
 
-static bool d4_take(Scratch &sc, uint64_t T, uint64_t ntiles, uint32_t cap, D4Plan &p) {
+static bool d4_take(Scratch &sc, uint64_t T, uint32_t cap, D4Plan &p) {
     const uint64_t ntl = (T + kD4ResolveThreads - 1) / kD4ResolveThreads;
     p.tab = sc.take<DecTables>(1);
     p.syms = sc.take<uint32_t>(cap);
     p.cp = sc.take<uint16_t>(32 * T);
-    p.mboff = sc.take<uint64_t>(32 * T);
-    p.tfirst = sc.take<uint64_t>(ntiles + 1);
+    p.soff = sc.take<uint64_t>(T);
     p.sbm = sc.take<uint64_t>(T);
     p.srest = sc.take<uint32_t>(T);
     p.sx0 = sc.take<uint8_t>(T);
@@ -1244,7 +1242,8 @@ static bool d4_take(Scratch &sc, uint64_t T, uint64_t ntiles, uint32_t cap, D4Pl
 size_t d4_scratch_bytes(uint64_t bit_len, uint64_t count, uint32_t cap) {
     ScratchSize s;
     const uint64_t T = bit_len ? (bit_len + kD4S - 1) / kD4S : 1;
-    d4_sizes(s, T, (count + kD4Tile - 1) / kD4Tile, cap);
+    (void)count;
+    d4_sizes(s, T, cap);
     return s.bytes();
 }
 
@@ -1256,8 +1255,7 @@ int d4_plan(const uint8_t *bits, uint32_t bit_phase, uint64_t bit_len, uint64_t 
     p.count = count;
     p.T = (bit_len + kD4S - 1) / kD4S;
     p.nmb = (bit_len + kD4MB - 1) / kD4MB;
-    p.ntiles = (count + kD4Tile - 1) / kD4Tile;
-    if (!d4_take(sc, p.T, p.ntiles, cap, p)) return LZB_E_ARG;
+    if (!d4_take(sc, p.T, cap, p)) return LZB_E_ARG;
     uintptr_t a = reinterpret_cast<uintptr_t>(bits);
     p.words = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
     p.head = (uint32_t)(a & 3) * 8 + bit_phase;
@@ -1467,7 +1465,7 @@ static int dec_setup(const uint8_t *bits, uint32_t bit_phase, uint64_t bit_len, 
     p.open_end = 0;
     p.tab = tab;
     p.syms = syms;
-    p.pmboff = nullptr;
+    p.psoff = nullptr;
     p.S = L.S;
     p.T = L.T;
     p.P = L.P;
@@ -1614,7 +1612,7 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
     q.T = p.T;
     q.P = maxlen;
     q.cp = p.cp;
-    q.pmboff = p.mboff;
+    q.psoff = p.soff;
     q.st = st;
     q.out = sym;
     q.entry0 = 0;

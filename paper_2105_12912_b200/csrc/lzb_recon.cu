@@ -21,11 +21,9 @@
 // written in grid order (coalesced along x) with a fused min/max/finite
 // reduction.  Prefix sums along different axes commute, so the order of the
 // three passes does not matter for the (exact integer) result.
-#include <stdlib.h>
 #include <string.h>
 
 #include "lzb_common.cuh"
-#include "lzb_decrecon.cuh"
 #include "lzb_recon3d.cuh"
 
 namespace lzb {
@@ -868,145 +866,6 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
             k_gen_dequant<double><<<grid, 256, 0, s>>>(q, n, 2.0 * eb_abs, (double *)y, prequant_out, mm);
         LZB_LAUNCH_CHECK();
     }
-    k_rc_finish<<<1, 1, 0, s>>>(st, mm);
-    LZB_LAUNCH_CHECK();
-    return LZB_OK;
-}
-
-// ---------------------------------------------------------------------------
-// Fused decompress (K5 v4 plan + k_decrecon3d8): Huffman archives of
-// ChunkSpec(8,8,8) grids of whole chunks, f32 output.
-// ---------------------------------------------------------------------------
-extern "C" int lzb_decompress_fused_ok(const lzb_geom *gg, uint32_t cap, int dtype) {
-    if (!gg) return 0;
-    const Geom g = make_geom(*gg);
-    return g.cx == 8 && g.cy == 8 && g.cz == 8 && g.nx % 8 == 0 && g.ny % 8 == 0 && g.nz % 8 == 0 &&
-           g.nx > 0 && g.ny > 0 && g.nz > 0 && dtype == 0 && cap >= 4 && cap <= 65536 &&
-           (g.nx * 4) % 16 == 0 && g.nbx * g.nby * g.nbz + kFChunks < (1ull << 32) &&
-           tma_encode() != nullptr;
-}
-
-static void fused_sizes(ScratchSize &s, const Geom &g, uint64_t n_out) {
-    const uint64_t nt = (g.nbx * g.nby * g.nbz + kFChunks - 1) / kFChunks;
-    s.take<unsigned long long>(4);
-    s.take<unsigned int>(4);
-    s.take<uint32_t>(nt + 1);
-    s.take<uint32_t>(nt + 1);
-    s.take<uint64_t>(nt + 1);
-    s.take<uint64_t>((nt + 1 + 2047) / 2048 + 1);
-    s.take<uint64_t>(2 * (n_out ? n_out : 1));
-}
-
-extern "C" size_t lzb_decompress_scratch_bytes(const lzb_geom *gg, uint64_t bit_len, uint64_t count,
-                                               uint32_t cap, uint64_t n_out) {
-    if (!gg) return 0;
-    const Geom g = make_geom(*gg);
-    ScratchSize s;
-    fused_sizes(s, g, n_out);
-    return s.bytes() + d4_scratch_bytes(bit_len, count, cap) + 256;
-}
-
-extern "C" int lzb_decompress_huff(const uint8_t *bits, uint64_t bit_len, uint64_t count,
-                                   const uint8_t *lengths, uint32_t cap, uint32_t maxlen,
-                                   const uint8_t *outliers, uint64_t n_out, const lzb_geom *gg,
-                                   double eb_abs, void *y, int dtype, lzb_dstatus *st, void *scratch,
-                                   size_t scratch_bytes, void *stream) {
-    if (!lzb_decompress_fused_ok(gg, cap, dtype) || !bits || !lengths || !y || !st ||
-        (n_out && !outliers) || maxlen == 0 || maxlen > 64 || count == 0 || bit_len == 0 ||
-        (reinterpret_cast<uintptr_t>(y) & 15))
-        return LZB_E_ARG;
-    const Geom g = make_geom(*gg);
-    const uint64_t n = g.nx * g.ny * g.nz;
-    if (count != n) return LZB_E_ARG;
-    cudaStream_t s = as_stream(stream);
-    const uint64_t nchunks = g.nbx * g.nby * g.nbz;
-    const uint64_t nt = (nchunks + kFChunks - 1) / kFChunks;
-    Scratch sc(scratch, scratch_bytes);
-    unsigned long long *mm = sc.take<unsigned long long>(4);
-    unsigned int *tick = sc.take<unsigned int>(4);
-    uint32_t *tile_cnt = sc.take<uint32_t>(nt + 1);
-    uint32_t *tile_fill = sc.take<uint32_t>(nt + 1);
-    uint64_t *tile_start = sc.take<uint64_t>(nt + 1);
-    uint64_t *lb = sc.take<uint64_t>((nt + 1 + 2047) / 2048 + 1);
-    uint64_t *brec = sc.take<uint64_t>(2 * (n_out ? n_out : 1));
-    if (!brec) return LZB_E_ARG;
-    LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
-    k_mm_init<<<1, 32, 0, s>>>(mm, 4);
-    LZB_LAUNCH_CHECK();
-    // tick, tile_cnt, tile_fill, tile_start, lb are consecutive: one memset
-    LZB_CUDA_TRY(cudaMemsetAsync(tick, 0, reinterpret_cast<char *>(brec) - reinterpret_cast<char *>(tick), s));
-    const int sm = nsms();
-    OutParams op;
-    op.rec = outliers;
-    op.n_out = n_out;
-    op.fast3d = 1;
-    op.tshift = kFTileShift;
-    op.g = g;
-    op.K = 0;
-    op.tiles_per_row = 0;
-    op.ntiles = nt;
-    op.tile_cnt = tile_cnt;
-    op.tile_fill = tile_fill;
-    op.tile_start = tile_start;
-    op.brec = brec;
-    op.st = st;
-    const unsigned go = (unsigned)umin64((n_out + 255) / 256, (uint64_t)sm * 8);
-    if (n_out) {
-        k_out_count<<<go, 256, 0, s>>>(op);
-        LZB_LAUNCH_CHECK();
-    }
-    k_scan_tiles<<<(unsigned)umin64((nt + 1 + 2047) / 2048, (uint64_t)sm * 4), 256, 0, s>>>(
-        tile_cnt, tile_start, nt, lb, &tick[0]);
-    LZB_LAUNCH_CHECK();
-    if (n_out) {
-        k_out_scatter<<<go, 256, 0, s>>>(op);
-        LZB_LAUNCH_CHECK();
-    }
-    FParams fp;
-    {
-        const char *e = getenv("LZB_FUSED_DBG");
-        fp.dbg = e ? atoi(e) : 0;
-    }
-    int rc = d4_plan(bits, 0, bit_len, count, lengths, cap, maxlen, st, sc, s, fp.d);
-    if (rc != LZB_OK) return rc;
-    R3Params &r3 = fp.r;
-    r3.codes = nullptr;
-    r3.g = g;
-    r3.two_eb = 2.0 * eb_abs;
-    r3.r = (int32_t)(cap / 2);
-    r3.y = y;
-    r3.pre = nullptr;
-    r3.st = st;
-    r3.mm = mm;
-    r3.nchunks = nchunks;
-    r3.ntiles = nt;
-    r3.tile_start = tile_start;
-    r3.brec = brec;
-    r3.ticket = &tick[1];
-    r3.vec_ok = 1;
-    CUtensorMap ymap;
-    memset(&ymap, 0, sizeof(ymap));
-    {
-        cuuint64_t dims[3] = {g.nx, g.ny, g.nz};
-        cuuint64_t strides[2] = {g.nx * 4, g.nx * g.ny * 4};
-        cuuint32_t box[3] = {8, 8, 8};
-        cuuint32_t estr[3] = {1, 1, 1};
-        if (tma_encode()(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, y, dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return LZB_E_ARG;
-    }
-    const size_t fsm = kFSmem;
-    LZB_CUDA_TRY(cudaFuncSetAttribute(k_decrecon3d8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-    int per_sm = 0;
-    LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decrecon3d8, kFThreads, fsm));
-    if (per_sm < 1) per_sm = 1;
-    const uint64_t grid = umin64((uint64_t)sm * per_sm, (nchunks + kFRangeChunks - 1) / kFRangeChunks);
-    k_decrecon3d8<<<(unsigned)(grid ? grid : 1), kFThreads, fsm, s>>>(fp, ymap);
-    LZB_LAUNCH_CHECK();
-    const unsigned gf = (unsigned)umin64((n + 255) / 256, (uint64_t)sm * 8);
-    k_first_nonfinite<float><<<gf, 256, 0, s>>>((const float *)y, n, mm);
-    LZB_LAUNCH_CHECK();
     k_rc_finish<<<1, 1, 0, s>>>(st, mm);
     LZB_LAUNCH_CHECK();
     return LZB_OK;

@@ -45,9 +45,7 @@ _OUTLIER_DT = np.dtype([("index", "<u8"), ("delta", "<i8")])
 _WORKFLOW_ALIASES = {"auto": None, "huffman": Workflow.HUFFMAN, "huff": Workflow.HUFFMAN,
                      "rle": Workflow.RLE, "rlevle": Workflow.RLE_VLE}
 _MAX_RUN = 0xFFFFFFFF  # P/rle.py:14
-# the fused decode + reconstruct kernel (lzb_decompress_huff); off by default:
-# on C5 it measures slower than K5 (plan + final decode) followed by K6
-_FUSED = __import__("os").environ.get("LZB_FUSED", "0") == "1"
+
 
 
 @dataclass(frozen=True)
@@ -543,23 +541,10 @@ def decompress_device(arc, raw_host: bytes | None = None, prof=None, out=None):
     y = out if out is not None else torch.empty(n, dtype=dtn, device=dev)
     g = N.geom(dims.as_tuple(), chunk.as_tuple())
 
-    dtc = _DTYPE_CODES[hdr.dtype]
-    # Huffman archives of whole 8^3 chunks (f32): K5 decodes tile by tile
-    # straight into K6's shared memory (lzb_decompress_huff), no code array
-    fused = huff is not None and bool(L.lzb_decompress_fused_ok(g, cap, dtc)) and _FUSED
+
 
     def run(robust: bool) -> None:
         """Launch the decode + reconstruct kernels (no host sync)."""
-        if fused and not robust:
-            bptr, bit_len, count, maxlen = huff
-            fs = L.lzb_decompress_scratch_bytes(g, bit_len, count, cap, hdr.outlier_count)
-            f_scr = _pool.get("f_scratch", fs, dev)
-            with _Stage(prof, "K5K6_decode_reconstruct"):
-                N.check_rc(L.lzb_decompress_huff(bptr, bit_len, count, base + hdr.codebook[0], cap, maxlen,
-                                                 base + out_off, hdr.outlier_count, g, hdr.eb_abs,
-                                                 y.data_ptr(), dtc, stp, _dev(f_scr), fs, sp),
-                           "decompress")
-            return
         dec = L.lzb_huff_decode_robust if robust else L.lzb_huff_decode
         codes = _pool.get("dcodes", n * cb, dev)
         if huff is not None:
@@ -589,15 +574,7 @@ def decompress_device(arc, raw_host: bytes | None = None, prof=None, out=None):
                        "reconstruct")
 
     run(False)
-    if fused:
-        (sf,) = N.read_status(st[: N.STATUS_BYTES])  # the one sync
-        if sf.code == N.LZB_OK:
-            return y, hdr, sf.f64(0), sf.f64(1)
-        # retry or any error: the separate robust stages give the exact verdict
-        run(True)
-        sd, sr, sk = N.read_status(st[: 3 * N.STATUS_BYTES])
-    else:
-        sd, sr, sk = N.read_status(st[: 3 * N.STATUS_BYTES])  # the one sync
+    sd, sr, sk = N.read_status(st[: 3 * N.STATUS_BYTES])  # the one sync
     if sd.code == N.LZB_E_RETRY:  # a stream the fast decoder cannot resolve (rare)
         run(True)
         sd, sr, sk = N.read_status(st[: 3 * N.STATUS_BYTES])
