@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(kF9Warps * 32, 1) k_dec_final9(DecParams p, ui
         uint32_t cnt = act ? (cpv >> 8) : 0u;
         uint32_t start = act ? b + (cpv & 0xFFu) : b;
         if (lane == 0) start = e;
-        const bool irregular = !plan && e != 0 && ((p.irr[t] >> e) & 1ull);
+        const bool irregular = plan ? p.pirr[t] != 0 : (e != 0 && ((p.irr[t] >> e) & 1ull));
         if (irregular) {
             // the true path joins the chain after microblock 0: re-resolve the
             // lanes' starts and counts (count-only, lane by lane)

@@ -68,6 +68,7 @@ struct D4Plan {
     uint32_t *srest;  // per subsequence: code words of lanes 1..31 (chain)
     uint8_t *sx0;     // per subsequence: lane 0 phase-0 exit (kD4Bad: invalid)
     uint8_t *sexit;   // per subsequence: chain exit phase into the next one / kExitEnd / kD4Bad
+    uint8_t *sirr;    // per subsequence: 1 = the true path joins the chain after microblock 0
     uint64_t *lb;     // look-back words, one per k_dec4_resolve tile
     unsigned int *ticket;
     lzb_dstatus *st;
@@ -127,6 +128,28 @@ __device__ __forceinline__ void d4_window(const D4Plan &p, uint64_t m, uint32_t 
     const uint64_t a = (uint64_t)p.head + m * kD4MB;  // absolute word-stream bit
     r.load(p, a >> 5, (uint32_t)(a & 31) + rel);
 }
+
+// Streaming reader over the whole stream in global memory (pass S's rare
+// full-subsequence walks): two or three word loads per peek, no state.
+struct GRd {
+    const D4Plan *p;
+    uint64_t pos;  // absolute word-stream bit
+    __device__ __forceinline__ uint32_t word(uint64_t w) const {
+        return w < p->nwords ? bswap32(__ldg(p->words + w)) : 0u;
+    }
+    __device__ __forceinline__ uint32_t peek32() const {
+        const uint64_t w = pos >> 5;
+        return __funnelshift_l(word(w + 1), word(w), (uint32_t)(pos & 31));
+    }
+    __device__ __forceinline__ uint32_t peek12() const { return peek32() >> (32 - kLutBits); }
+    __device__ __forceinline__ uint64_t peek64() const {
+        const uint64_t w = pos >> 5;
+        const uint32_t sh = (uint32_t)(pos & 31), w1 = word(w + 1);
+        return ((uint64_t)__funnelshift_l(w1, word(w), sh) << 32) | __funnelshift_l(word(w + 2), w1, sh);
+    }
+    __device__ __forceinline__ void adv(uint32_t L) { pos += L; }
+    __device__ __forceinline__ void adv64(uint32_t L) { pos += L; }
+};
 
 // ---------------------------------------------------------------------------
 // shared-memory access through 32-bit shared addresses (no generic->shared
@@ -467,7 +490,7 @@ __global__ void __launch_bounds__(kD4ResolveThreads) k_dec4_resolve(D4Plan p) {
         const uint64_t s = tl * kD4ResolveThreads + threadIdx.x;
         uint64_t total = 0;
         uint32_t cnt0 = 0, e = 0;
-        bool retry = p.st->code != 0;
+        bool retry = p.st->code != 0, irregular = false;
         if (s < p.T) {
             const uint32_t ev = s == 0 ? 0u : p.sexit[s - 1];
             const uint32_t x0 = p.sx0[s];
@@ -490,11 +513,30 @@ __global__ void __launch_bounds__(kD4ResolveThreads) k_dec4_resolve(D4Plan p) {
                     const int w = d4_walk(r, lt, pos, stop, endrel, bm, k);
                     if (w == 1) cnt0 = k + c0 - d4_rank64(bm, pos);
                     else if (w == 0 && pos == x0) cnt0 = k;
-                    else retry = true;
+                    else if (w == 2) retry = true;
+                    else irregular = true;
                 }
             }
-            total = (uint64_t)cnt0 + p.srest[s];
-            if (s == p.T - 1 && p.sexit[s] != kExitEnd) retry = true;
+            if (irregular) {
+                // the true path has not joined the chain by the end of
+                // microblock 0: count the whole subsequence from e (rare; the
+                // final decode re-resolves its microblock entries)
+                const uint32_t sbits = (uint32_t)umin64(kD4S, p.bit_len - b0);
+                const uint32_t endrel = (uint32_t)umin64(p.bit_len - b0, 0xFFFFFF00u);
+                GRd g{&p, (uint64_t)p.head + b0 + e};
+                uint32_t rel = e, c = 0;
+                uint64_t dummy = 0;
+                if (!d4_count<false>(g, lt, rel, sbits, endrel, c, dummy)) retry = true;
+                const bool lastsub = s == p.T - 1;
+                if (lastsub ? rel != sbits : rel - kD4S != (uint32_t)p.sexit[s]) retry = true;  // exit must agree
+                total = c;
+                cnt0 = c0;
+                p.sirr[s] = 1;
+            } else {
+                total = (uint64_t)cnt0 + p.srest[s];
+                if (s == p.T - 1 && p.sexit[s] != kExitEnd) retry = true;
+                p.sirr[s] = 0;
+            }
         }
         uint64_t tot;
         const uint64_t off = block_exclusive_scan<uint64_t>(total, s_scan, &tot);

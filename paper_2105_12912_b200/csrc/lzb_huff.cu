@@ -662,6 +662,7 @@ struct DecParams {
     // plan mode (K5 v4, lzb_dec4.cuh): entries from the plan's per-microblock
     // cp (above), offsets per subsequence, no irregular entries
     const uint64_t *psoff;
+    const uint8_t *pirr;
     // bit-range mode (multi-GPU decode of one stream, lzb_huff_range_*):
     // the range starts in phase entry0 and must leave in phase exit_expect
     // (kExitEnd when it ends the stream); an open range's last subsequence
@@ -1221,6 +1222,7 @@ static void d4_sizes(ScratchSize &sc, uint64_t T, uint32_t cap) {
     sc.take<uint32_t>(T);
     sc.take<uint8_t>(T);
     sc.take<uint8_t>(T);
+    sc.take<uint8_t>(T);
     sc.take<uint64_t>(ntl + 2);
 }
 
@@ -1234,6 +1236,7 @@ static bool d4_take(Scratch &sc, uint64_t T, uint32_t cap, D4Plan &p) {
     p.srest = sc.take<uint32_t>(T);
     p.sx0 = sc.take<uint8_t>(T);
     p.sexit = sc.take<uint8_t>(T);
+    p.sirr = sc.take<uint8_t>(T);
     p.lb = sc.take<uint64_t>(ntl + 2);  // + the ticket word (one memset)
     p.ticket = p.lb ? reinterpret_cast<unsigned int *>(p.lb + ntl + 1) : nullptr;
     return p.ticket != nullptr;
@@ -1466,6 +1469,7 @@ static int dec_setup(const uint8_t *bits, uint32_t bit_phase, uint64_t bit_len, 
     p.tab = tab;
     p.syms = syms;
     p.psoff = nullptr;
+    p.pirr = nullptr;
     p.S = L.S;
     p.T = L.T;
     p.P = L.P;
@@ -1613,6 +1617,7 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
     q.P = maxlen;
     q.cp = p.cp;
     q.psoff = p.soff;
+    q.pirr = p.sirr;
     q.st = st;
     q.out = sym;
     q.entry0 = 0;

@@ -243,6 +243,10 @@ def test_tma_tile_path_3d(cuda):
     noisy = (rng.standard_normal((16, 16, 256)) * 50).astype(np.float32)
     cases.append((noisy, dict(eb=1e-4, cap=64)))                               # many outliers
     cases.append((noisy, dict(eb=1e-2, cap=4)))
+    # a wide code distribution at cap 1024: many codes outside the u8 code
+    # stream's byte window (escapes, include/lzb.h) in K1 -> K3
+    cases.append(((rng.standard_normal((16, 8, 128)) * 3).cumsum(axis=2).astype(np.float32), dict(eb=2e-4)))
+    cases.append((noisy, dict(eb=3e-4, cap=2048)))
     ties = (np.round(rng.uniform(-300, 300, (8, 8, 128))) + 0.5).astype(np.float32) * np.float32(0.5)
     cases.append((ties, dict(eb=0.25, eb_mode="abs")))                         # x / (2 eb) on a .5 tie
     big = smooth((16, 8, 128)) * np.float32(1e4)
