@@ -883,7 +883,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
                               "bytes": "N*4 + |archive| per direction (SURVEY 8(d))"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": profiled_traffic(dom)},
+                     "frac": round(achieved / peak, 4), "traffic": profiled_traffic(dom),
+                     "traffic_source": "profiles/ncu_traffic.json: ncu dram__bytes_read+write of this "
+                                       "stage's kernels in one step of this command (tools/launch_summary.py)"},
         "stages_ms": stage_ms, "stage_roofline": per_stage_roofline,
         "bound_ok": bool(bound_ok), "max_abs_err": err, "eb_abs": hdr.eb_abs,
         "gpu_launches": launches_per_step(hdr) * args.steps,
