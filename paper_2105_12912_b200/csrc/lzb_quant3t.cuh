@@ -13,9 +13,10 @@
 // path, exact f64 division only for the rare element near a rounding tie),
 // Lorenzo deltas in registers/shuffles, codes stored as 16-byte rows straight
 // into the chunk-major stream, histogram into per-lane shared columns.  No
-// CTA barrier per tile: warps publish their outlier counts / first records
-// in the stage's slots and bump a per-stage counter; the last warp to
-// release a stage publishes the two outlier tiles and issues its TMA refill.
+// CTA barrier per tile: warps leave their outlier counts / first records in
+// the stage's slots and arrive on the stage's named barrier; one rotating
+// publisher warp syncs on it, publishes the two outlier tiles and issues the
+// stage's TMA refill.
 // (Measured alternatives that were slower on C5q: 2 or 4 stages, 8-chunk
 // tiles with 2 CTAs/SM, releasing the stage right after the shared-memory
 // reads -- more TMA traffic in flight costs more than it hides.)
@@ -117,7 +118,8 @@ __global__ void __launch_bounds__(kT1Threads, 1)
     extern __shared__ __align__(1024) unsigned char t1_smem[];
     // [stages x 16 KB tiles][s_col: warps x 16 bins x 32 lanes u32][s_codes: warps x 512 u16][s_hist: cap u32]
     __shared__ __align__(8) uint64_t s_full[kT1Stages];
-    __shared__ uint32_t s_rel[kT1Stages], s_slow[kT1Stages], s_cnt[kT1Stages][kT1Warps];
+    // per stage and warp: outlier count | slow-path flag << 31
+    __shared__ uint32_t s_cnt[kT1Stages][kT1Warps];
     __shared__ uint64_t s_rec[kT1Stages][kT1Warps][kT1Sub][2];
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     const uint32_t tiles_s = ((uint32_t)__cvta_generic_to_shared(t1_smem) + 1023u) & ~1023u;
@@ -127,10 +129,6 @@ __global__ void __launch_bounds__(kT1Threads, 1)
     uint32_t *s_hist = s_col + kT1Warps * 16 * 32 + kT1Warps * 256;
     for (uint32_t i = threadIdx.x; i < kT1Warps * 16 * 32; i += blockDim.x) s_col[i] = 0;
     for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) s_hist[i] = 0;
-    if (threadIdx.x < kT1Stages) {
-        s_rel[threadIdx.x] = 0;
-        s_slow[threadIdx.x] = 0;
-    }
     const uint32_t full_s = (uint32_t)__cvta_generic_to_shared(s_full);
     const uint64_t G = gridDim.x;
     T1Pos pos = t1_pos(P, blockIdx.x);
@@ -301,21 +299,22 @@ __global__ void __launch_bounds__(kT1Threads, 1)
                 nout = rr.n;
             }
         }
-        // release the stage; the last warp publishes the tile and refills it
+        // release the stage: the tile's publisher warp (it mod 16, so every
+        // warp publishes one tile in 16) waits on the stage's named barrier
+        // for the other 15 (bar.arrive, non-blocking), publishes the two
+        // outlier tiles and issues the stage's TMA refill.  The refill is what
+        // the other warps wait for before they reuse the stage's slots, so
+        // successive uses of a barrier cannot overlap.
         __syncwarp();
-        uint32_t last = 0;
-        if (lane == 0) {
-            s_cnt[st][warp] = nout;
-            if (slow) s_slow[st] = 1;
-            __threadfence_block();
-            last = atomicAdd(&s_rel[st], 1u) == kT1Warps - 1;
-            __threadfence_block();
-        }
-        last = __shfl_sync(f3::kFull, last, 0);
-        if (last) {
-            __syncwarp();  // order the lanes' reads after lane 0's acquire
+        if (lane == 0) s_cnt[st][warp] = nout | (slow ? 0x80000000u : 0u);
+        const uint32_t pub = it % kT1Warps;
+        if (warp != pub) {
+            asm volatile("bar.arrive %0, %1;" ::"r"(1 + st), "r"(kT1Threads) : "memory");
+        } else {
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + st), "r"(kT1Threads) : "memory");
             // two outlier tiles of 8 chunks: lanes 0-7 and 8-15
-            const uint32_t cl = lane < kT1Warps ? s_cnt[st][lane] : 0u;
+            const uint32_t sv = lane < kT1Warps ? s_cnt[st][lane] : 0u;
+            const uint32_t cl = sv & 0x7FFFFFFFu;
             uint32_t inc = cl;
 #pragma unroll
             for (int o = 1; o < 8; o <<= 1) {
@@ -323,7 +322,7 @@ __global__ void __launch_bounds__(kT1Threads, 1)
                 if ((lane & 7) >= (uint32_t)o) inc += v;
             }
             const uint32_t tot0 = __shfl_sync(f3::kFull, inc, 7), tot1 = __shfl_sync(f3::kFull, inc, 15);
-            const bool slow_st = s_slow[st] != 0;
+            const bool slow_st = __any_sync(f3::kFull, (sv >> 31) != 0);
             const uint32_t big = __ballot_sync(f3::kFull, lane < kT1Warps && cl > (uint32_t)kT1Sub);
             const bool over0 = slow_st || (big & 0xFFu), over1 = slow_st || (big & 0xFF00u);
             const uint64_t tile = 2 * t + (lane >> 3);
@@ -340,8 +339,6 @@ __global__ void __launch_bounds__(kT1Threads, 1)
                 p.tile_cnt[2 * t + 1] = tot1;
                 if (over0) p.over_list[atomicAdd(p.n_over, 1u)] = (uint32_t)(2 * t);
                 if (over1) p.over_list[atomicAdd(p.n_over, 1u)] = (uint32_t)(2 * t + 1);
-                s_rel[st] = 0;
-                s_slow[st] = 0;
                 const uint64_t tn = t + kT1Stages * G;
                 if (tn < P.nst) {
                     T1Pos q = pos;

@@ -3,7 +3,7 @@
 # S=8192 as C5, a quarter of the memory so ncu's save/restore stays cheap).
 set -u
 TAG=${1:-r1c}
-KS=${2:-'regex:k_quantize3d8|k_huff_count_w|k_huff_encode_w|k_dec_maps3|k_dec_final9|k_reconstruct3d8'}
+KS=${2:-'regex:k_quantize3d8_tma|k_huff_count_w|k_huff_encode_w|k_dec4_count|k_dec_final9|k_reconstruct3d8'}
 mkdir -p gpurun_out
 timeout 1500 ncu --set full --clock-control none --import-source on \
   -k "$KS" -c 6 \
