@@ -379,7 +379,7 @@ __device__ __forceinline__ void r3_tma_store(const CUtensorMap *map, uint32_t sr
 // and one TMA tensor store each (the 32-byte row fragments of a chunk are
 // scattered over 64 rows; as plain stores they saturate L1).
 template <typename SymT, typename OutT, bool TMA>
-__global__ void __launch_bounds__(kR3Threads, TMA ? 2 : 3)
+__global__ void __launch_bounds__(kR3Threads, TMA ? 3 : 3)
     k_reconstruct3d8(const __grid_constant__ R3Params p, const __grid_constant__ CUtensorMap ymap) {
     // per-warp double buffer of the next chunk's code rows (16 symbols per lane)
     __shared__ __align__(16) SymT s_stage[kR3Warps][2][32 * 16];
