@@ -785,21 +785,32 @@ def run_gpu(args, cfg, rank, world, local_rank):
         up, down = torch.cuda.Stream(), torch.cuda.Stream()
         xready, xfree = [None, None], [None, None]
         state = {"yfree": None}
+        trace = [] if os.environ.get("LZB_E2E_TRACE") else None
+
+        def mark(stream, k, what):  # optional timeline (LZB_E2E_TRACE=1), off by default
+            if trace is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(stream)
+                trace.append((k, what, ev, time.perf_counter()))
 
         def upload(k):
             b = k % 2
             with torch.cuda.stream(up):
                 if xfree[b] is not None:
                     up.wait_event(xfree[b])  # the compress that read this buffer is done
+                mark(up, k, "up0")
                 xds[b].copy_(xh, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(up)
                 xready[b] = ev
+                mark(up, k, "up1")
 
         def one_step(k, last):
             b = k % 2
             cs.wait_event(xready[b])
+            mark(cs, k, "c0")
             a = lzb.compress_device(flds[b], eb)  # returns after its status read (K1 done)
+            mark(cs, k, "c1")
             ev = torch.cuda.Event()
             ev.record(cs)
             xfree[b] = ev
@@ -808,18 +819,23 @@ def run_gpu(args, cfg, rank, world, local_rank):
             sp = N.stream_ptr()
             N.check_rc(L.lzb_copy_bytes(ah.data_ptr(), a.data.data_ptr(), a.nbytes, sp), "copy")  # D2H
             N.check_rc(L.lzb_copy_bytes(ad.data_ptr(), ah.data_ptr(), a.nbytes, sp), "copy")      # H2D
+            mark(cs, k, "arc")
             cs.synchronize()  # the host copy of the archive is complete
             pre = ah[: a.header.symbols[0] + 32].numpy().tobytes()
             if state["yfree"] is not None:
                 cs.wait_event(state["yfree"])  # the previous result has left ybuf
+            mark(cs, k, "d0")
             yy, _, _, _ = lzb.decompress_device(ad[: a.nbytes], raw_host=pre, out=ybuf)
             done = torch.cuda.Event()
             done.record(cs)
+            mark(cs, k, "d1")
             with torch.cuda.stream(down):
                 down.wait_event(done)
+                mark(down, k, "dn0")
                 yh.copy_(yy, non_blocking=True)
                 yf = torch.cuda.Event()
                 yf.record(down)
+                mark(down, k, "dn1")
             state["yfree"] = yf
 
         upload(0)
@@ -841,6 +857,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
         down.synchronize()
         torch.cuda.synchronize()
         te = (time.perf_counter() - t0) / K
+        if trace:
+            base = next(ev for kk, w, ev, _ in trace if kk == 1 and w == "up0")
+            for kk, w, ev, th in trace:
+                if kk >= 1:
+                    print(f"e2e-trace step {kk:2d} {w:4s} gpu {base.elapsed_time(ev):9.1f} ms "
+                          f"host {1e3 * (th - t0):9.1f} ms", file=sys.stderr)
         ok_e2e = ok_e2e and all(bool(torch.equal(yh[a: a + pw].to(dev), rs))
                                 for a, rs in zip(probe, ref_sl))
         e2e = {"value": round(nbytes / te / 1e9, 4), "unit": "GB/s",
