@@ -467,11 +467,23 @@ def run_reference(args, cfg, rank, world):
 
 def run_sharded(args, cfg, rank, world, dev, local_rank):
     """--gpus N (torchrun): strong scaling of the same field over N slabs of
-    whole chunk layers.  A step = sharded compress (histogram
-    all-reduce, (bits, outliers) all-gather, bit-phase encode: every rank ends
-    holding its byte-exact slice of the archive) + slab-local decompress of
-    that slice (decode at the slice's bit phase + K6).  Same metric as N=1:
-    N*s / step time, the step time the max over ranks (CUDA events)."""
+    whole chunk layers.  A step is the round trip N=1 times:
+
+      compress   = distributed.compress_sharded: histogram all-reduce,
+                   (bits, outliers) all-gather, bit-phase encode -- every
+                   rank ends holding its byte-exact slice of the archive;
+      decompress = distributed.decompress_archive_sharded of the STORED
+                   archive (every rank holds the whole archive, as after a
+                   read): per-rank bit-range transfer maps, their
+                   all-gather, range decode, all-to-all of the symbols to
+                   the slab owners, slab reconstruct.
+
+    The stored archive is built once, before timing, from the ranks' slices
+    with one all-gather (distributed.allgather_archive) -- no rank
+    compresses the full field.  Same metric as N=1: N*s / step time, each
+    phase's time the max over ranks (CUDA events).  The slice-local
+    decompress (a rank decoding the slice it just wrote, no exchange) is
+    reported beside it as ``decompress_slice_local``."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -489,21 +501,35 @@ def run_sharded(args, cfg, rank, world, dev, local_rank):
     vmin, vmax = float(mm[0]), float(-mm[1])
     ops = D.DeviceSlabOps(dev)
     eb = cfg["eb"]
+    slack = float(np.spacing(np.float32(max(abs(vmin), abs(vmax))))) / 2
+    bound = eb * (vmax - vmin) * (1 + 1e-12) + slack
+
+    def compress(xin):
+        return D.compress_sharded(ops, xin, dims, vmin, vmax, eb, "rel", 1024, chunk, 0)
+
+    res = compress(x)
+    arc = D.allgather_archive(res, device=dev)  # the stored archive, built once
+    del res
 
     def step(xin):
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record()
-        res = D.compress_sharded(ops, xin, dims, vmin, vmax, eb, "rel", 1024, chunk, 0)
+        res = compress(xin)
         e1.record()
-        y = D.decompress_sharded(ops, res)
+        y, (alo, ahi), _ = D.decompress_archive_sharded(ops, arc)
         e2.record()
+        assert (alo, ahi) == (lo, hi)
         return res, y, (e0, e1, e2)
+
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(v) for v in t.cpu()]
 
     for _ in range(args.warmup):
         res, y, _ = step(x)
     torch.cuda.synchronize()
-    slack = float(np.spacing(np.float32(max(abs(vmin), abs(vmax))))) / 2
-    ok = (y.double() - x.double()).abs().max().item() <= eb * (vmax - vmin) * (1 + 1e-12) + slack
+    ok = y is None or (y.double() - x.double()).abs().max().item() <= bound
     okt = torch.tensor([1 if ok else 0], device=dev, dtype=torch.int64)
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
     del y
@@ -518,20 +544,37 @@ def run_sharded(args, cfg, rank, world, dev, local_rank):
         torch.cuda.synchronize()
         res, y, (e0, e1, e2) = step(x)
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e2), e0.elapsed_time(e1), e1.elapsed_time(e2)],
-                         device=dev, dtype=torch.float64) / 1e3
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tt.append(float(t[0]))
-        tc.append(float(t[1]))
-        td.append(float(t[2]))
+        t = max_over_ranks([e0.elapsed_time(e2) / 1e3, e0.elapsed_time(e1) / 1e3,
+                            e1.elapsed_time(e2) / 1e3])
+        tt.append(t[0])
+        tc.append(t[1])
+        td.append(t[2])
         del y
     clocks.mark("t1")
     clk = clocks.stop()
     t_step, t_c, t_d = statistics.mean(tt), statistics.mean(tc), statistics.mean(td)
+
+    # side number: each rank decodes the slice it just wrote (no exchange)
+    tl = []
+    for k in range(args.warmup + args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        l0, l1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+        l0.record()
+        yl = D.decompress_sharded(ops, res)
+        l1.record()
+        torch.cuda.synchronize()
+        t = max_over_ranks([l0.elapsed_time(l1) / 1e3])[0]
+        if k >= args.warmup:
+            tl.append(t)
+        ok_l = yl is None or (yl.double() - x.double()).abs().max().item() <= bound
+        del yl
+    okl = torch.tensor([1 if ok_l else 0], device=dev, dtype=torch.int64)
+    dist.all_reduce(okl, op=dist.ReduceOp.MIN)
+
     n = dims.count
     nbytes = n * 4
-    m = res.meta
-    arc_bytes = D._SECTION_BASE + 1024 + 16 + (m["total_bits"] + 7) // 8 + 16 * m["total_out"]
+    arc_bytes = int(arc.numel())
     # per GPU: its slab's algorithmic bytes (N*s + |archive| each way) over the step
     slab_bytes = (hi - lo) * (nbytes // shape[0])
     my_alg = 2 * (slab_bytes + arc_bytes * slab_bytes / nbytes)
@@ -564,35 +607,40 @@ def run_sharded(args, cfg, rank, world, dev, local_rank):
                 res, y, _ = step(xd)
                 yh.copy_(y, non_blocking=True)
                 torch.cuda.synchronize()
-                tk = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
-                dist.all_reduce(tk, op=dist.ReduceOp.MAX)
+                tk = max_over_ranks([time.perf_counter() - t0])[0]
                 if k:
-                    te.append(float(tk))
+                    te.append(tk)
                 del y
             v = statistics.mean(te)
             e2e = {"value": round(nbytes / v / 1e9, 4), "unit": "GB/s",
                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                    "ms_per_step": round(v * 1e3, 2), "steps": args.e2e_steps,
-                   "note": "per rank: its slab H2D, sharded compress + slab decompress, slab D2H; "
-                           "max over ranks"}
+                   "note": "per rank: its slab H2D, sharded compress + stored-archive decompress, "
+                           "slab D2H; max over ranks"}
             del xh, yh, xd
         else:
             e2e = {"error": err or "another rank could not allocate its pinned buffers"}
         bufs = None
-    arch = archive_decompress_sharded(args, cfg, dims, ops, x, lo, hi, eb, vmin, vmax, dev, nbytes)
     if rank == 0:
+        wf = res.meta["workflow"]
         print(json.dumps({
             "metric": METRIC, "value": round(nbytes / t_step / 1e9, 3), "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t_step * 1e3, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["workload"], "elements": n, "bytes": nbytes,
-                       "workflow": "HUFFMAN", "parallelism": f"slab{world}",
+                       "workflow": wf, "parallelism": f"slab{world}",
+                       "backend": dist.get_backend(),
                        "l2": "inputs >> 126 MB L2 (no flush)",
                        "step": "sharded compress (each rank ends with its byte-exact archive slice) + "
-                               "slab-local decompress of that slice"},
+                               "decompress of the stored archive (range maps all-gather, range "
+                               "decode, symbol all-to-all, slab reconstruct)"},
             "compress_gbs": round(nbytes / t_c / 1e9, 3), "decompress_gbs": round(nbytes / t_d / 1e9, 3),
             "compress_ms": round(t_c * 1e3, 3), "decompress_ms": round(t_d * 1e3, 3),
+            "decompress_slice_local": {"decompress_gbs": round(nbytes / statistics.mean(tl) / 1e9, 3),
+                                       "ms": round(statistics.mean(tl) * 1e3, 3),
+                                       "bound_ok": bool(int(okl.item())),
+                                       "what": "each rank decodes the slice it wrote (no exchange)"},
             "compression_ratio": round(nbytes / arc_bytes, 4), "archive_bytes": arc_bytes,
             "roofline": {"bound": "hbm", "kernel": "pipeline (per GPU, rank 0 slab)",
                          "achieved": round(ach, 1), "peak": peak, "peak_kind": peak_kind,
@@ -602,63 +650,8 @@ def run_sharded(args, cfg, rank, world, dev, local_rank):
                              + LAUNCHES["status_and_header_copies"]
                              + LAUNCHES["lzb_huff_decode"] + LAUNCHES["lzb_reconstruct_with_outliers"])
                             * args.steps * world,
-            "clocks": clk, "e2e": e2e, "cpu_baseline": None, "archive_decompress": arch,
+            "clocks": clk, "e2e": e2e, "cpu_baseline": None,
         }), flush=True)
-
-
-def archive_decompress_sharded(args, cfg, dims, ops, x, lo, hi, eb, vmin, vmax, dev, nbytes):
-    """Side measurement (not the headline): decompress ONE stored archive,
-    replicated on every rank, on N GPUs -- per-rank bit-range transfer maps,
-    their all-gather, range decode, all-to-all of symbols to the slab owners,
-    slab reconstruct (distributed.decompress_archive_sharded).  Time = max
-    over ranks (CUDA events)."""
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-
-    import paper_2105_12912_b200 as lzb
-    from paper_2105_12912_b200 import distributed as D
-
-    arc, err = None, None
-    try:  # every rank builds the stored archive; all must succeed before any collective
-        xf = gen_field_device(cfg, dev)
-        fa = lzb.compress_device(lzb.Field.from_array(xf.reshape(cfg["shape"])), eb)
-        arc = fa.data[: fa.nbytes].clone()
-        del xf, fa
-    except Exception as exc:  # pragma: no cover - box dependent
-        err = repr(exc)[:300]
-    oka = torch.tensor([1 if arc is not None else 0], device=dev, dtype=torch.int64)
-    dist.all_reduce(oka, op=dist.ReduceOp.MIN)
-    if int(oka.item()) != 1:
-        return {"error": err or "another rank could not build the archive"}
-    try:
-        ta = []
-        ya = None
-        for k in range(args.warmup + args.steps):
-            dist.barrier()
-            torch.cuda.synchronize()
-            a0, a1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
-            a0.record()
-            ya, (alo, ahi), _ = D.decompress_archive_sharded(ops, arc)
-            a1.record()
-            torch.cuda.synchronize()
-            t = torch.tensor([a0.elapsed_time(a1) / 1e3], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            if k >= args.warmup:
-                ta.append(float(t))
-        assert (alo, ahi) == (lo, hi)
-        slack = float(np.spacing(np.float32(max(abs(vmin), abs(vmax))))) / 2
-        ok = ya is None or (ya.double() - x.double()).abs().max().item() <= \
-            eb * (vmax - vmin) * (1 + 1e-12) + slack
-        okt = torch.tensor([1 if ok else 0], device=dev, dtype=torch.int64)
-        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
-        v = statistics.mean(ta)
-        return {"decompress_gbs": round(nbytes / v / 1e9, 3), "ms_per_step": round(v * 1e3, 3),
-                "steps": args.steps, "bound_ok": bool(int(okt.item())),
-                "note": "one stored archive on every rank -> each rank's slab: range maps, "
-                        "all-gather, range decode, all-to-all, reconstruct; max over ranks"}
-    except Exception as exc:  # reported, never fatal for the headline line
-        return {"error": repr(exc)[:300]}
 
 
 def run_gpu(args, cfg, rank, world, local_rank):

@@ -18,17 +18,12 @@ on-disk format is the reference's, P/pipeline.py:26-39, 184-221).
 from __future__ import annotations
 
 import os
-import struct
 
 import numpy as np
 
-from .distributed import _HEADER, _SECTION_BASE, MAGIC
+from .distributed import archive_header, archive_layout, archive_prefix
 
 _PIECE = 64 << 20
-
-
-def _a8(v: int) -> int:
-    return (v + 7) & ~7
 
 
 def _host_u8(x) -> np.ndarray:
@@ -125,30 +120,6 @@ def load(path: str, device="cuda"):
     return out
 
 
-def layout(meta: dict) -> dict:
-    """Section offsets of a sharded compress's archive (P/pipeline.py:184-221)."""
-    cap, total_bits, total_out = meta["cap"], meta["total_bits"], meta["total_out"]
-    nbytes = (total_bits + 7) // 8
-    vle = meta.get("workflow") == "RLE_VLE"
-    prefix = 24 if vle else 16
-    sym_len = prefix + nbytes + (4 * meta["n_runs"] if vle else 0)
-    cb_off = _SECTION_BASE
-    sym_off = _a8(cb_off + cap)
-    out_off = _a8(sym_off + sym_len)
-    return dict(cb_off=cb_off, sym_off=sym_off, sym_len=sym_len, out_off=out_off,
-                data_off=sym_off + prefix, lens_off=sym_off + prefix + nbytes, nbytes=nbytes,
-                total=out_off + 16 * total_out, vle=vle)
-
-
-def _header(meta: dict, lay: dict) -> bytes:
-    dims, chunk, cap = meta["dims"], meta["chunk"], meta["cap"]
-    return _HEADER.pack(MAGIC, 1, meta["dtype_code"], dims.ndim, dims.nx, dims.ny, dims.nz,
-                        chunk.cx, chunk.cy, chunk.cz, 1 if meta["eb_mode"] == "rel" else 0,
-                        meta["eb"], meta["vmin"], meta["vmax"], cap, 2 if lay["vle"] else 0,
-                        dims.count, meta["total_out"], lay["cb_off"], cap, lay["sym_off"],
-                        lay["sym_len"], lay["out_off"], 16 * meta["total_out"])
-
-
 def write_sharded(res, path: str, lengths_bytes: bytes | None = None, group=None) -> int:
     """Every rank writes its parts of the archive file; returns its size.
     `lengths_bytes` (the cap code lengths) is only needed on rank 0 and
@@ -159,7 +130,7 @@ def write_sharded(res, path: str, lengths_bytes: bytes | None = None, group=None
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     m = res.meta
-    lay = layout(m)
+    lay = archive_layout(m)
     sl = _host_u8(res.bits) if res.bits is not None else np.zeros(0, np.uint8)
     first = res.byte_start
     last = res.byte_start + len(sl) - 1
@@ -184,14 +155,11 @@ def write_sharded(res, path: str, lengths_bytes: bytes | None = None, group=None
     if rank == 0:
         fd = os.open(path, os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644)
         os.ftruncate(fd, lay["total"])  # zero padding between sections
-        lens = lengths_bytes if lengths_bytes is not None else _host_u8(m["lengths"]).tobytes()
-        _pwrite_all(fd, _header(m, lay), 0)
-        _pwrite_all(fd, bytes(lens[: m["cap"]]), lay["cb_off"])
-        if lay["vle"]:
-            _pwrite_all(fd, struct.pack("<QQQ", m["n_runs"], m["total_bits"], m["n_runs"]),
-                        lay["sym_off"])
-        else:
-            _pwrite_all(fd, struct.pack("<QQ", m["total_bits"], m["dims"].count), lay["sym_off"])
+        _pwrite_all(fd, archive_header(m, lay), 0)
+        if lay["cb_len"]:
+            lens = lengths_bytes if lengths_bytes is not None else _host_u8(m["lengths"]).tobytes()
+            _pwrite_all(fd, bytes(lens[: m["cap"]]), lay["cb_off"])
+        _pwrite_all(fd, archive_prefix(m, lay), lay["sym_off"])
         os.close(fd)
     dist.barrier(group=group)
     fd = os.open(path, os.O_WRONLY)
@@ -213,9 +181,11 @@ def write_sharded(res, path: str, lengths_bytes: bytes | None = None, group=None
         if res.records is not None and res.n_out:
             _pwrite_all(fd, _host_u8(res.records)[: 16 * res.n_out],
                         lay["out_off"] + 16 * res.record_start)
-        if lay["vle"] and res.rle is not None and res.rle["n_runs"]:
-            ln = _host_u8(res.rle["lens"])[: 4 * res.rle["n_runs"]]
-            _pwrite_all(fd, ln, lay["lens_off"] + 4 * res.rle["run_start"])
+        if res.rle is not None and res.rle["n_runs"]:
+            k, a = res.rle["n_runs"], 4 * res.rle["run_start"]
+            _pwrite_all(fd, _host_u8(res.rle["lens"])[: 4 * k], lay["lens_off"] + a)
+            if lay["vals_off"] is not None:
+                _pwrite_all(fd, _host_u8(res.rle["vals"])[: 4 * k], lay["vals_off"] + a)
     finally:
         os.close(fd)
     dist.barrier(group=group)

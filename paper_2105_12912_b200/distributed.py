@@ -60,6 +60,56 @@ from .grid import ChunkSpec, Dims
 _HEADER = struct.Struct("<8sHBB3I3IBdddIBQQ6Q")
 _SECTION_BASE = (_HEADER.size + 7) & ~7
 MAGIC = b"LZEBC\x00\x00\x01"
+_WF_CODE = {"HUFFMAN": 0, "RLE": 1, "RLE_VLE": 2}
+
+
+def _a8(x: int) -> int:
+    return (x + 7) & ~7
+
+
+def archive_layout(meta: dict) -> dict:
+    """Section offsets of the archive a sharded compress produces, the same
+    as the single-device writer's (P/pipeline.py:158-221):
+
+      HUFFMAN  [cap code lengths] [bit_len][count][bits]
+      RLE      (no code book)     [runs][u32 values x runs][u32 lengths x runs]
+      RLE_VLE  [cap code lengths] [runs][bit_len][count = runs][value bits][u32 lengths x runs]
+    """
+    wf = meta.get("workflow", "HUFFMAN")
+    cap, runs = meta["cap"], meta.get("n_runs", 0)
+    nbytes = 0 if wf == "RLE" else (meta["total_bits"] + 7) // 8
+    cb_len = 0 if wf == "RLE" else cap
+    cb_off = _SECTION_BASE
+    sym_off = _a8(cb_off + cb_len)
+    prefix = {"HUFFMAN": 16, "RLE": 8, "RLE_VLE": 24}[wf]
+    data_off = sym_off + prefix
+    if wf == "RLE":
+        sym_len, vals_off, lens_off = 8 + 8 * runs, data_off, data_off + 4 * runs
+    else:
+        sym_len = prefix + nbytes + (4 * runs if wf == "RLE_VLE" else 0)
+        vals_off, lens_off = None, data_off + nbytes
+    out_off = _a8(sym_off + sym_len)
+    return dict(wf=wf, cb_off=cb_off, cb_len=cb_len, sym_off=sym_off, sym_len=sym_len,
+                data_off=data_off, vals_off=vals_off, lens_off=lens_off, nbytes=nbytes,
+                out_off=out_off, total=out_off + 16 * meta["total_out"], runs=runs)
+
+
+def archive_prefix(meta: dict, lay: dict) -> bytes:
+    """The symbol section's fixed fields (written once, by rank 0)."""
+    if lay["wf"] == "HUFFMAN":
+        return struct.pack("<QQ", meta["total_bits"], meta["dims"].count)
+    if lay["wf"] == "RLE":
+        return struct.pack("<Q", lay["runs"])
+    return struct.pack("<QQQ", lay["runs"], meta["total_bits"], lay["runs"])
+
+
+def archive_header(meta: dict, lay: dict) -> bytes:
+    dims, chunk = meta["dims"], meta["chunk"]
+    return _HEADER.pack(MAGIC, 1, meta["dtype_code"], dims.ndim, dims.nx, dims.ny, dims.nz,
+                        chunk.cx, chunk.cy, chunk.cz, 1 if meta["eb_mode"] == "rel" else 0,
+                        meta["eb"], meta["vmin"], meta["vmax"], meta["cap"], _WF_CODE[lay["wf"]],
+                        dims.count, meta["total_out"], lay["cb_off"], lay["cb_len"],
+                        lay["sym_off"], lay["sym_len"], lay["out_off"], 16 * meta["total_out"])
 
 
 def slab_bounds(dims: Dims, chunk: ChunkSpec, rank: int, world: int) -> tuple[int, int]:
@@ -371,7 +421,7 @@ def _boundary(hv, hl, tv, tl, r: int) -> tuple:
 
 
 def _compress_sharded_rle(ops, codes, n_local, n_out, recs, dims, lo, cap, meta, rank, world, group,
-                          device, max_run):
+                          device, max_run, vle: bool = True):
     import torch
     import torch.distributed as dist
 
@@ -387,6 +437,17 @@ def _compress_sharded_rle(ops, codes, n_local, n_out, recs, dims, lo, cap, meta,
     a, b = keep[rank]
     e_k = emitted[rank]
     ev, el = (ops.rle_emit(vals, lens, a, b, grp[rank], max_run) if e_k else (None, None))
+    if n_out:
+        recs = ops.offset_records(recs, n_out, slab_index_offset(dims, lo))
+    if not vle:  # RLE alone: the stitched runs are the symbol section; only record offsets remain
+        mv = torch.tensor([n_out], dtype=torch.int64, device=device)
+        allo = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
+        dist.all_gather(allo, mv, group=group)
+        outs = [int(v[0]) for v in allo]
+        meta.update(workflow="RLE", total_bits=0, total_out=sum(outs), lengths=None, maxlen=0,
+                    n_runs=sum(emitted))
+        rle = dict(lens=el, vals=ev, run_start=sum(emitted[:rank]), n_runs=e_k, local=(vals, lens, r_k))
+        return SlabResult(rank, 0, None, recs, sum(outs[:rank]), meta, n_out=n_out, rle=rle)
     # run-value histogram of the stitched runs -> the VLE code book
     vh = ops.value_hist(ev, e_k, cap) if e_k else None
     h = ops.to_tensor(vh) if vh is not None else torch.zeros(cap, dtype=torch.int64, device=device)
@@ -404,8 +465,6 @@ def _compress_sharded_rle(ops, codes, n_local, n_out, recs, dims, lo, cap, meta,
     phase = B_k % 8
     bits = ops.encode_at(ev, e_k, lengths, words, cap, maxlen, phase, my_bits, sym_bytes=4) \
         if e_k else None
-    if n_out:
-        recs = ops.offset_records(recs, n_out, slab_index_offset(dims, lo))
     meta.update(workflow="RLE_VLE", total_bits=total_vbits, total_out=sum(v[1] for v in allb),
                 lengths=lengths, maxlen=maxlen, n_runs=sum(emitted))
     rle = dict(lens=el, run_start=sum(emitted[:rank]), n_runs=e_k, local=(vals, lens, r_k))
@@ -415,12 +474,21 @@ def _compress_sharded_rle(ops, codes, n_local, n_out, recs, dims, lo, cap, meta,
 
 def compress_sharded(ops: SlabOps, values, dims: Dims, vmin: float, vmax: float, eb: float,
                      eb_mode: str, cap: int, chunk: ChunkSpec, dtype_code: int, group=None,
-                     device=None, max_run: int = 0xFFFFFFFF) -> SlabResult:
-    """Rank-local part of the sharded compress (every rank calls this with its slab)."""
+                     device=None, max_run: int = 0xFFFFFFFF, workflow=None,
+                     select_mode: str = "exact") -> SlabResult:
+    """Rank-local part of the sharded compress (every rank calls this with its slab).
+
+    ``workflow`` (None = select, or "huff" / "rle" / "rlevle" / a Workflow)
+    and ``select_mode`` ("exact": the code book's bits per symbol;
+    "estimate": the entropy-bracket midpoint) mean what they mean for
+    ``compress`` (P/pipeline.py:135-182, P/smoothness.py:111-136); the
+    decision is taken from the all-reduced histogram, so every rank takes
+    the same one."""
     import torch
     import torch.distributed as dist
 
-    from .pipeline import _check_cfg, _resolve_eb
+    from .pipeline import _check_cfg, _resolve_eb, resolve_workflow
+    from .smoothness import RLE_THRESHOLD_BITS, Workflow, estimate_bits
 
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
@@ -440,14 +508,24 @@ def compress_sharded(ops: SlabOps, values, dims: Dims, vmin: float, vmax: float,
                                                                  device=device)
     h = h.to(torch.int64).clone()
     dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
-    lengths, words, maxlen, total_bits = ops.codebook(h, cap)
-    n = dims.count
-    b = float(np.float64(total_bits) / np.float64(n))  # P/codebook.py:110-115
+    chosen = resolve_workflow(workflow)
+    if select_mode not in ("exact", "estimate"):
+        raise DataError(f"unknown selection mode {select_mode!r}")
+    book = None
+    if chosen is None:
+        if select_mode == "exact":
+            book = ops.codebook(h, cap)
+            b = float(np.float64(book[3]) / np.float64(dims.count))  # P/codebook.py:110-115
+        else:
+            b = estimate_bits(h.cpu().numpy())
+        chosen = Workflow.RLE_VLE if b <= RLE_THRESHOLD_BITS else Workflow.HUFFMAN
     meta = dict(dims=dims, chunk=chunk, cap=cap, eb=eb, eb_mode=eb_mode, vmin=vmin, vmax=vmax,
                 dtype_code=dtype_code, workflow="HUFFMAN")
-    if b <= 1.09:  # P/smoothness.py:111-136 -> RLE_VLE
+    if chosen is not Workflow.HUFFMAN:
         return _compress_sharded_rle(ops, codes, n_local, n_out, recs, dims, lo, cap, meta, rank,
-                                     world, group, h.device, max_run)
+                                     world, group, h.device, max_run,
+                                     vle=chosen is Workflow.RLE_VLE)
+    lengths, words, maxlen, total_bits = book if book is not None else ops.codebook(h, cap)
     # (2) all-gather of (bits, outliers)
     my_bits = ops.local_bits(hist, lengths) if hist is not None else 0
     mine = torch.tensor([my_bits, n_out], dtype=torch.int64, device=h.device)
@@ -502,49 +580,108 @@ def decompress_sharded(ops: SlabOps, res: SlabResult, group=None):
 def assemble(results: list[SlabResult], lengths_bytes: bytes) -> bytes:
     """Archive bytes from every rank's slice (rank order).  Byte-identical to
     the single-device archive: the dense stream is the OR of the phase-shifted
-    slices (they overlap in at most one byte)."""
+    slices (they overlap in at most one byte); runs and records go to their
+    ranks' offsets."""
     m = results[0].meta
-    dims, chunk, cap = m["dims"], m["chunk"], m["cap"]
-    total_bits, total_out = m["total_bits"], m["total_out"]
-    nbytes = (total_bits + 7) // 8
-    data = np.zeros(nbytes, np.uint8)
+    lay = archive_layout(m)
+    blob = np.zeros(lay["total"], np.uint8)
+    hdr = archive_header(m, lay)
+    blob[: len(hdr)] = np.frombuffer(hdr, np.uint8)
+    if lay["cb_len"]:
+        blob[lay["cb_off"]: lay["cb_off"] + m["cap"]] = np.frombuffer(lengths_bytes, np.uint8)[: m["cap"]]
+    pre = archive_prefix(m, lay)
+    blob[lay["sym_off"]: lay["sym_off"] + len(pre)] = np.frombuffer(pre, np.uint8)
+    data = blob[lay["data_off"]: lay["data_off"] + lay["nbytes"]]
     for r in results:
-        if r.bits is None:
-            continue
-        sl = np.asarray(r.bits, np.uint8)
-        end = min(nbytes, r.byte_start + len(sl))
-        data[r.byte_start:end] |= sl[: end - r.byte_start]
-    recs = np.zeros(16 * total_out, np.uint8)
-    for r in results:
+        if r.bits is not None:
+            sl = np.asarray(r.bits, np.uint8)
+            end = min(lay["nbytes"], r.byte_start + len(sl))
+            data[r.byte_start:end] |= sl[: end - r.byte_start]
         if r.records is not None and len(r.records):
             rb = np.asarray(r.records, np.uint8)
-            recs[16 * r.record_start: 16 * r.record_start + len(rb)] = rb
-    if m.get("workflow") == "RLE_VLE":
-        n_runs = m["n_runs"]
-        lens = np.zeros(n_runs, np.uint32)
-        for r in results:
-            if r.rle is not None and r.rle["n_runs"]:
-                a = r.rle["run_start"]
-                lens[a: a + r.rle["n_runs"]] = np.asarray(r.rle["lens"]).view(np.uint32)[: r.rle["n_runs"]]
-        # P/pipeline.py:158-221: [runs][bit_len][count = runs][value bits][lengths]
-        sym = struct.pack("<QQQ", n_runs, total_bits, n_runs) + data.tobytes() + lens.tobytes()
-        wf = 2
-    else:
-        sym = struct.pack("<QQ", total_bits, dims.count) + data.tobytes()
-        wf = 0
-    cb_off = _SECTION_BASE
-    sym_off = (cb_off + cap + 7) & ~7
-    out_off = (sym_off + len(sym) + 7) & ~7
-    hdr = _HEADER.pack(MAGIC, 1, m["dtype_code"], dims.ndim, dims.nx, dims.ny, dims.nz,
-                       chunk.cx, chunk.cy, chunk.cz, 1 if m["eb_mode"] == "rel" else 0, m["eb"],
-                       m["vmin"], m["vmax"], cap, wf, dims.count, total_out, cb_off, cap,
-                       sym_off, len(sym), out_off, 16 * total_out)
-    blob = bytearray(out_off + 16 * total_out)
-    blob[: len(hdr)] = hdr
-    blob[cb_off: cb_off + cap] = lengths_bytes
-    blob[sym_off: sym_off + len(sym)] = sym
-    blob[out_off:] = recs.tobytes()
-    return bytes(blob)
+            o = lay["out_off"] + 16 * r.record_start
+            blob[o: o + len(rb)] = rb
+        if r.rle is not None and r.rle["n_runs"]:
+            k, a = r.rle["n_runs"], 4 * r.rle["run_start"]
+            blob[lay["lens_off"] + a: lay["lens_off"] + a + 4 * k] = _host_bytes(r.rle["lens"])[: 4 * k]
+            if lay["vals_off"] is not None:
+                blob[lay["vals_off"] + a: lay["vals_off"] + a + 4 * k] = _host_bytes(r.rle["vals"])[: 4 * k]
+    return blob.tobytes()
+
+
+def allgather_archive(res: SlabResult, group=None, device=None, lengths=None):
+    """The whole archive, byte-identical to the single-device one, on EVERY
+    rank, built from the ranks' slices with one all-gather (NCCL on GPUs).
+    Each rank contributes [bits slice | records | run lengths | run values];
+    the receivers OR the bit slices (neighbours share at most one byte) and
+    place the rest at their offsets.  This is how a sharded compress hands
+    a stored archive to ``decompress_archive_sharded`` without any rank
+    compressing the full field.  ``device``: where the returned archive
+    lives (default: where the backend exchanges -- this GPU for NCCL, host
+    memory for gloo); ``lengths``: the code lengths if res.meta has none."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    m = res.meta
+    lay = archive_layout(m)
+    out_device = device
+    # the collective runs where the backend moves data (NCCL: this GPU; gloo: host)
+    device = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
+
+    def u8(x, nbytes):
+        if x is None or nbytes == 0:
+            return torch.empty(0, dtype=torch.uint8, device=device)
+        if isinstance(x, (bytes, bytearray)):
+            x = np.frombuffer(x, np.uint8)
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+        return t.reshape(-1).view(torch.uint8)[:nbytes].to(device)
+
+    k = res.rle["n_runs"] if res.rle is not None else 0
+    nb = 0 if res.bits is None else (res.bits.numel() if isinstance(res.bits, torch.Tensor)
+                                     else np.asarray(res.bits).nbytes)
+    parts = [u8(res.bits, nb), u8(res.records, 16 * res.n_out),
+             u8(res.rle["lens"] if k else None, 4 * k),
+             u8(res.rle.get("vals") if k and lay["vals_off"] is not None else None,
+                4 * k if lay["vals_off"] is not None else 0)]
+    sizes = [p.numel() for p in parts]
+    info = torch.tensor(sizes + [res.byte_start, res.record_start,
+                                 res.rle["run_start"] if k else 0], dtype=torch.int64, device=device)
+    infos = [torch.zeros_like(info) for _ in range(world)]
+    dist.all_gather(infos, info, group=group)
+    infos = [[int(v) for v in t.cpu()] for t in infos]
+    width = max(max(sum(t[:4]) for t in infos), 1)
+    mine = torch.zeros(width, dtype=torch.uint8, device=device)
+    if sum(sizes):
+        torch.cat(parts, out=mine[: sum(sizes)])
+    pieces = [torch.empty(width, dtype=torch.uint8, device=device) for _ in range(world)]
+    dist.all_gather(pieces, mine, group=group)
+
+    arc = torch.zeros(lay["total"], dtype=torch.uint8, device=device)
+    fixed = bytearray(archive_header(m, lay))
+    arc[: len(fixed)] = torch.frombuffer(fixed, dtype=torch.uint8).to(device)
+    if lay["cb_len"]:
+        lens = lengths if lengths is not None else m["lengths"]
+        arc[lay["cb_off"]: lay["cb_off"] + m["cap"]] = u8(lens, m["cap"])
+    pre = bytearray(archive_prefix(m, lay))
+    arc[lay["sym_off"]: lay["sym_off"] + len(pre)] = torch.frombuffer(pre, dtype=torch.uint8).to(device)
+    for (n_bits, n_rec, n_len, n_val, bstart, rstart, runstart), pc in zip(infos, pieces):
+        o = 0
+        if n_bits:  # a slice may run one byte past the stream's end (its phase padding)
+            w = min(n_bits, lay["nbytes"] - bstart)
+            if w > 0:
+                arc[lay["data_off"] + bstart: lay["data_off"] + bstart + w].bitwise_or_(pc[:w])
+            o += n_bits
+        if n_rec:
+            arc[lay["out_off"] + 16 * rstart: lay["out_off"] + 16 * rstart + n_rec] = pc[o: o + n_rec]
+            o += n_rec
+        if n_len:
+            arc[lay["lens_off"] + 4 * runstart: lay["lens_off"] + 4 * runstart + n_len] = pc[o: o + n_len]
+            o += n_len
+        if n_val:
+            arc[lay["vals_off"] + 4 * runstart: lay["vals_off"] + 4 * runstart + n_val] = pc[o: o + n_val]
+    return arc if out_device is None else arc.to(out_device)
 
 
 def gather_results(res: SlabResult, group=None) -> list[SlabResult] | None:
@@ -553,8 +690,8 @@ def gather_results(res: SlabResult, group=None) -> list[SlabResult] | None:
 
     rle = None
     if res.rle is not None:
-        rle = dict(run_start=res.rle["run_start"], n_runs=res.rle["n_runs"],
-                   lens=None if res.rle["lens"] is None else _host_bytes(res.rle["lens"]))
+        rle = {k: (None if res.rle.get(k) is None else _host_bytes(res.rle[k])) for k in ("lens", "vals")}
+        rle.update(run_start=res.rle["run_start"], n_runs=res.rle["n_runs"])
     host = SlabResult(res.rank, res.byte_start,
                       None if res.bits is None else _host_bytes(res.bits),
                       None if res.records is None else _host_bytes(res.records),

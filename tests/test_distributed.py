@@ -203,6 +203,8 @@ def _worker(rank, world, port, case, q):
             assert y is not None and np.array_equal(y, want), rank
         else:
             assert y is None  # more ranks than chunk layers: an empty slab
+        ref_arc = O.compress(vals, dims.as_tuple(), float(vals.min()), float(vals.max()), eb)
+        assert D.allgather_archive(res).numpy().tobytes() == ref_arc, rank
         res.meta.pop("lengths")
         got = D.gather_results(res)
         if rank == 0:
@@ -447,3 +449,84 @@ def test_rle_stitch_plan_matches_global_runs():
             assert emitted[k] == (b - a) + (len(D.split_run(group[k][1], max_run)) if group[k] else 0)
         gv, gl = O.rle_encode(vals, max_run)
         assert ev == list(gv) and el == list(gl), case
+
+
+def _override_worker(rank, world, port, case, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2105_12912_b200 import ChunkSpec, Dims, archive_io
+        from paper_2105_12912_b200 import distributed as D
+
+        vals, shape, eb, workflow, mode, ref_arc, path = case
+        dims = Dims.of(*shape[::-1])
+        chunk = ChunkSpec.default_for(dims.ndim)
+        lo, hi = D.slab_bounds(dims, chunk, rank, world)
+        full = vals.reshape(shape)
+        slab = full[lo:hi].reshape(-1) if dims.ndim > 1 else full[lo:hi]
+        res = D.compress_sharded(OracleSlabOps(), slab, dims, float(vals.min()), float(vals.max()),
+                                 eb, "rel", 1024, chunk, 0, workflow=workflow, select_mode=mode)
+        y = D.decompress_sharded(OracleSlabOps(), res)
+        ref = O.decompress(ref_arc)[0].reshape(shape)
+        want = ref[lo:hi].reshape(-1) if dims.ndim > 1 else ref[lo:hi]
+        if hi > lo:
+            assert y is not None and np.array_equal(y, want), rank
+        h = O.parse_header(ref_arc)
+        lens = np.frombuffer(ref_arc, np.uint8, h["codebook"][1], h["codebook"][0]).tobytes()
+        archive_io.write_sharded(res, path, lens if rank == 0 else None)
+        # every rank ends with the whole archive (one all-gather of the slices)
+        whole = D.allgather_archive(res, lengths=lens).numpy().tobytes()
+        assert whole == ref_arc, rank
+        got = D.gather_results(res)
+        if rank == 0:
+            q.put((res.meta["workflow"], D.assemble(got, lens)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("workflow,mode,kind", [("rle", "exact", "runs"), ("rle", "exact", "smooth"),
+                                                ("rlevle", "exact", "smooth"),
+                                                ("huff", "exact", "runs"), (None, "estimate", "runs"),
+                                                (None, "estimate", "smooth")])
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_workflow_and_select_mode_overrides(workflow, mode, kind, world, tmp_path):
+    """compress_sharded honours a forced workflow (RLE alone included) and the
+    estimate selection mode: the archive (assembled, and written in parallel)
+    is byte-identical to the single-process one with the same arguments
+    (P/pipeline.py:135-182, T/test_acceptance.py:213-223)."""
+    import torch.multiprocessing as mp
+
+    from helpers import smooth
+
+    shape = (24, 20, 36)
+    if kind == "runs":
+        rng = np.random.default_rng(5)
+        vals = np.zeros(int(np.prod(shape)), np.float32)
+        for _ in range(4):
+            a = int(rng.integers(0, vals.size - 12))
+            vals[a: a + 12] = rng.normal(0, 1, 12).astype(np.float32)
+        vals[0], eb = 4.0, 1e-3
+    else:
+        vals, eb = smooth(shape).reshape(-1).astype(np.float32), 1e-4
+    dims = tuple(list(shape[::-1]) + [1] * (3 - len(shape))) + (len(shape),)
+    ref = O.compress(vals, dims, float(vals.min()), float(vals.max()), eb, workflow=workflow,
+                     select_mode=mode)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    path = str(tmp_path / "override.lzb")
+    case = (vals, shape, eb, workflow, mode, ref, path)
+    procs = [ctx.Process(target=_override_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    wf, got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert ["HUFFMAN", "RLE", "RLE_VLE"].index(wf) == O.parse_header(ref)["workflow"]
+    assert got == ref
+    with open(path, "rb") as fh:
+        assert fh.read() == ref
