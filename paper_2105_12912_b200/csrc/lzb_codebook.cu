@@ -151,12 +151,67 @@ __device__ int canonical_from_lengths(const uint8_t *lengths, uint32_t cap, uint
     return 0;
 }
 
+// The two-queue merge, one thread.  Leaves (sorted keys) and internal nodes
+// (created in non-decreasing weight order) are popped smallest first, leaf
+// first on ties.  The heads of both queues live in 4-deep register windows
+// (L0..L3 = leaves li..li+3, I0..I3 = internal nodes ii..ii+3, ~0 = none):
+// a step decides both pops from L0, L1, I0, I1, shifts the windows by the
+// pops with selects, and refills positions 2 and 3 with shared-memory loads
+// that the NEXT step only reads in its shifts -- the load latency is off the
+// dependency chain.  The node created by a step is written to shared memory
+// before the refill loads (so they see it) and patched into positions 0/1
+// directly.  W = uint32_t when the total count fits (half the compare/add
+// work), else uint64_t.
+template <typename W>
+__device__ __forceinline__ void huffman_merge(const CbScratch &sc, uint32_t n) {
+    constexpr W kNone = (W)~(W)0;
+    W *wint = reinterpret_cast<W *>(sc.wint);
+    auto leaf = [&](uint32_t i) -> W { return i < n ? (W)(sc.key[i] >> 20) : kNone; };
+    uint32_t li = 0, ii = 0, ni = 0;
+    W L0 = leaf(0), L1 = leaf(1), L2 = leaf(2), L3 = leaf(3);
+    W I0 = kNone, I1 = kNone, I2 = kNone, I3 = kNone;
+    for (uint32_t k = 0; k + 1 < n; k++) {
+        const bool a_leaf = L0 <= I0;  // first pop
+        const W cl = a_leaf ? L1 : L0, ci = a_leaf ? I0 : I1;
+        const bool b_leaf = cl <= ci;  // second pop
+        const W nw = (a_leaf ? L0 : I0) + (b_leaf ? cl : ci);
+        const uint32_t id0 = a_leaf ? li : n + ii;
+        const uint32_t id1 = b_leaf ? li + (uint32_t)a_leaf : n + ii + (uint32_t)!a_leaf;
+        wint[ni] = nw;
+        sc.parent[id0] = n + ni;
+        sc.parent[id1] = n + ni;
+        const uint32_t dl = (uint32_t)a_leaf + (uint32_t)b_leaf, di = 2u - dl;
+        li += dl;
+        ii += di;
+        const W nL0 = dl == 0 ? L0 : (dl == 1 ? L1 : L2);
+        const W nL1 = dl == 0 ? L1 : (dl == 1 ? L2 : L3);
+        W nI0 = di == 0 ? I0 : (di == 1 ? I1 : I2);
+        W nI1 = di == 0 ? I1 : (di == 1 ? I2 : I3);
+        if (ni == ii) nI0 = nw;          // the new node is the internal head
+        if (ni == ii + 1) nI1 = nw;      // ... or the one after it
+        ni++;
+        L0 = nL0;
+        L1 = nL1;
+        L2 = leaf(li + 2);
+        L3 = leaf(li + 3);
+        I0 = nI0;
+        I1 = nI1;
+        I2 = ii + 2 < ni ? wint[ii + 2] : kNone;
+        I3 = ii + 3 < ni ? wint[ii + 3] : kNone;
+    }
+}
+
+// kSmem: small books, the whole tree lives in shared memory (the pointers
+// are derived from the shared array in this instantiation, so the compiler
+// emits LDS/STS instead of generic loads -- the serial merge is latency bound)
+template <bool kSmem>
 __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long long *hist, uint32_t cap,
                                                         uint8_t *lengths, uint64_t *codes,
-                                                        lzb_dstatus *st, CbScratch sc, uint32_t npow2,
-                                                        int use_smem) {
+                                                        lzb_dstatus *st, CbScratch sc, uint32_t npow2) {
     extern __shared__ __align__(16) unsigned char cb_smem[];
-    if (use_smem) {  // small books: the whole tree lives in shared memory
+    const long long t0 = clock64();  // phase clocks -> st->u[4..5] (diagnostics)
+    __shared__ long long s_clk[4];
+    if constexpr (kSmem) {
         sc.key = reinterpret_cast<uint64_t *>(cb_smem);
         sc.wint = sc.key + npow2;
         sc.parent = reinterpret_cast<uint32_t *>(sc.wint + cap);
@@ -183,6 +238,10 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
         const uint64_t f = s < cap ? hist[s] : 0ull;
         if (s < cap) lengths[s] = 0;
         if (f >= (1ull << 44)) s_err = 1;
+        unsigned long long fs = f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) fs += __shfl_xor_sync(0xffffffffu, fs, o);
+        if ((threadIdx.x & 31) == 0 && fs) atomicAdd(&s_tot, fs);
         const uint32_t m = __ballot_sync(0xffffffffu, f != 0);
         uint32_t k0 = 0;
         if ((threadIdx.x & 31) == 0 && m) k0 = atomicAdd(&s_n, (uint32_t)__popc(m));
@@ -195,39 +254,24 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
         if (threadIdx.x == 0) set_status(st, LZB_E_DATA);  // empty histogram
         return;
     }
-    bitonic_sort_u64(sc.key, npow2);
+    {  // keys past n are ~0: sorting the power-of-two prefix covering n suffices
+        uint32_t np = 1;
+        while (np < n) np <<= 1;
+        bitonic_sort_u64(sc.key, np);
+    }
+    if (threadIdx.x == 0) s_clk[0] = clock64() - t0;
     if (n == 1) {
         if (threadIdx.x == 0) lengths[sc.key[0] & 0xFFFFF] = 1;  // lone symbol -> 1 bit
     } else {
-        // two-queue Huffman merge (sequential; n-1 steps); the heads of both
-        // queues are kept in registers
+        // two-queue Huffman merge (sequential; n-1 steps) on thread 0; see
+        // huffman_merge for the register windows that keep shared-memory
+        // latency off the step's dependency chain
         if (threadIdx.x == 0) {
-            uint32_t li = 0, ii = 0, ni = 0;
-            uint64_t lw = sc.key[0] >> 20;  // head leaf weight (li < n)
-            uint64_t iw = 0;                // head internal weight (ii < ni)
-            for (uint32_t k = 0; k < n - 1; k++) {
-                uint64_t w[2];
-                uint32_t id[2];
-#pragma unroll
-                for (int t = 0; t < 2; t++) {
-                    const bool take_leaf = li < n && (ii >= ni || lw <= iw);  // leaf first on ties
-                    if (take_leaf) {
-                        w[t] = lw;
-                        id[t] = li++;
-                        lw = li < n ? (sc.key[li] >> 20) : 0;
-                    } else {
-                        w[t] = iw;
-                        id[t] = n + ii++;
-                        iw = ii < ni ? sc.wint[ii] : 0;
-                    }
-                }
-                const uint64_t nw = w[0] + w[1];
-                sc.wint[ni] = nw;
-                if (ii == ni) iw = nw;  // the queue was empty: the new node is its head
-                sc.parent[id[0]] = n + ni;
-                sc.parent[id[1]] = n + ni;
-                ni++;
-            }
+            if (s_tot < (1ull << 32) - 1)  // every weight below the u32 "none" marker
+                huffman_merge<uint32_t>(sc, n);
+            else
+                huffman_merge<uint64_t>(sc, n);
+            s_clk[1] = clock64() - t0;
         }
         __syncthreads();
         // depths (number of ancestors) of the 2n-1 nodes, root = node 2n-2
@@ -288,33 +332,29 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
         if (threadIdx.x == 0) set_status(st, LZB_E_DATA);  // code longer than 64 bits
         return;
     }
+    if (threadIdx.x == 0) s_clk[2] = clock64() - t0;
     int rc = canonical_from_lengths(lengths, cap, codes, s_cnt, s_first, s_misc, false);
     if (rc) {
         if (threadIdx.x == 0) set_status(st, LZB_E_DATA);
         return;
     }
     // exact <b> inputs: sum(count * len) and total
-    unsigned long long sum = 0, tot = 0;
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
-        uint64_t f = hist[s];
-        sum += f * lengths[s];
-        tot += f;
+    unsigned long long sum = 0;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {  // the n used symbols, from the sorted keys
+        const uint64_t k = sc.key[i];
+        sum += (k >> 20) * lengths[k & 0xFFFFF];
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {  // warp sums first: 32 shared atomics, not 1024
-        sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&s_sum, sum);
-        atomicAdd(&s_tot, tot);
-    }
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);  // warp sums first
+    if ((threadIdx.x & 31) == 0 && sum) atomicAdd(&s_sum, sum);
     __syncthreads();
     if (threadIdx.x == 0) {
         st->u[0] = s_sum;
         st->u[1] = s_tot;
         st->u[2] = s_misc[1];
         st->u[3] = n;
+        st->u[4] = (uint64_t)(uint32_t)s_clk[0] | (uint64_t)(uint32_t)s_clk[1] << 32;
+        st->u[5] = (uint64_t)(uint32_t)s_clk[2] | (uint64_t)(uint32_t)(clock64() - t0) << 32;
     }
 }
 
@@ -393,11 +433,15 @@ extern "C" int lzb_codebook(const uint64_t *hist, uint32_t cap, uint8_t *lengths
     LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     size_t smem = (size_t)np * 8 + (size_t)cap * 8 + (size_t)cap * 8 + (size_t)cap * 2;
     int use_smem = smem <= 160 * 1024;
-    if (use_smem)
-        LZB_CUDA_TRY(cudaFuncSetAttribute(k_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (use_smem) {
+        LZB_CUDA_TRY(cudaFuncSetAttribute(k_codebook<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
-    k_codebook<<<1, kCbThreads, use_smem ? smem : 0, s>>>((const unsigned long long *)hist, cap,
-                                                          lengths, codes, st, c, np, use_smem);
+        k_codebook<true><<<1, kCbThreads, smem, s>>>((const unsigned long long *)hist, cap, lengths, codes,
+                                                     st, c, np);
+    } else {
+        k_codebook<false><<<1, kCbThreads, 0, s>>>((const unsigned long long *)hist, cap, lengths, codes,
+                                                   st, c, np);
+    }
     LZB_LAUNCH_CHECK();
     return LZB_OK;
 }

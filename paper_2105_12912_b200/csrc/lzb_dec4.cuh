@@ -519,16 +519,33 @@ __global__ void __launch_bounds__(kD4ResolveThreads) k_dec4_resolve(D4Plan p) {
             }
             if (irregular) {
                 // the true path has not joined the chain by the end of
-                // microblock 0: count the whole subsequence from e (rare; the
-                // final decode re-resolves its microblock entries)
+                // microblock 0: walk on microblock by microblock until it
+                // enters one at the chain's entry (pass M's cp[]); from there
+                // on the counts are the chain's.  Otherwise (rare) the walk
+                // covers the whole subsequence and its exit must agree with
+                // pass M's.  The final decode re-resolves the entries.
                 const uint32_t sbits = (uint32_t)umin64(kD4S, p.bit_len - b0);
                 const uint32_t endrel = (uint32_t)umin64(p.bit_len - b0, 0xFFFFFF00u);
                 GRd g{&p, (uint64_t)p.head + b0 + e};
-                uint32_t rel = e, c = 0;
+                uint32_t rel = e, c = 0, rest = p.srest[s];
                 uint64_t dummy = 0;
-                if (!d4_count<false>(g, lt, rel, sbits, endrel, c, dummy)) retry = true;
-                const bool lastsub = s == p.T - 1;
-                if (lastsub ? rel != sbits : rel - kD4S != (uint32_t)p.sexit[s]) retry = true;  // exit must agree
+                bool joined = false;
+                for (uint32_t j = 0; j < 32 && rel < sbits && !retry; j++) {
+                    const uint32_t mb_end = (j + 1) * kD4MB < sbits ? (j + 1) * kD4MB : sbits;
+                    if (!d4_count<false>(g, lt, rel, mb_end, endrel, c, dummy)) retry = true;
+                    if (retry || j == 31 || mb_end == sbits) break;
+                    const uint32_t cj = p.cp[m + j + 1];
+                    if (rel == mb_end + (cj & 0xFFu)) {  // on the chain from here
+                        c += rest;
+                        joined = true;
+                        break;
+                    }
+                    rest -= cj >> 8;
+                }
+                if (!joined) {
+                    const bool lastsub = s == p.T - 1;
+                    if (lastsub ? rel != sbits : rel - kD4S != (uint32_t)p.sexit[s]) retry = true;  // exit must agree
+                }
                 total = c;
                 cnt0 = c0;
                 p.sirr[s] = 1;

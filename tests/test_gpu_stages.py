@@ -21,6 +21,46 @@ def test_codebook_matches_reference_lengths(golden, cuda):
             np.array(want, np.uint8))]
 
 
+def test_codebook_random_books_vs_oracle(cuda):
+    """K2's two-queue merge (32-bit and 64-bit weight windows) against the
+    oracle's heap construction (P/codebook.py:143-176) on histograms built to
+    stress the tie rules: equal counts, runs of ones, geometric tails, a lone
+    symbol, totals across 2^32."""
+    import paper_2105_12912_b200 as lzb
+
+    rng = np.random.default_rng(1234)
+    cases = []
+    for cap in (2, 16, 64, 1024, 4096):
+        for kind in range(6):
+            h = np.zeros(cap, np.int64)
+            k = int(rng.integers(1, cap + 1))
+            idx = rng.choice(cap, k, replace=False)
+            if kind == 0:
+                h[idx] = 1                                   # all ties
+            elif kind == 1:
+                h[idx] = rng.integers(1, 4, k)               # few distinct weights
+            elif kind == 2:
+                h[idx] = (2.0 ** -np.abs(rng.normal(0, 4, k)) * 1e6).astype(np.int64) + 1
+            elif kind == 3:
+                h[idx] = rng.integers(1, 1 << 40, k)         # total far above 2^32
+            elif kind == 4:
+                h[idx] = np.sort(rng.integers(1, 1 << 12, k))[::-1]
+            else:
+                h[idx[:1]] = int(rng.integers(1, 1 << 30))   # lone symbol
+            cases.append(h)
+    for _ in range(60):  # centred quant-code-like books at cap 1024
+        h = np.zeros(1024, np.int64)
+        w = int(rng.integers(2, 400))
+        c = np.arange(512 - w, 512 + w)
+        h[c] = (np.exp(-((c - 512) / (w / rng.uniform(2, 8))) ** 2) * 10 ** rng.uniform(2, 9)).astype(np.int64)
+        h[rng.integers(0, 1024, 5)] += 1
+        cases.append(h)
+    for h in cases:
+        book = lzb.Codebook.from_counts(h)
+        want = O.huffman_lengths(h)
+        assert book.lengths.tolist() == want.tolist(), (len(h), int((h > 0).sum()), int(h.sum()))
+
+
 def test_codebook_kats(golden, cuda):
     import paper_2105_12912_b200 as lzb
 
