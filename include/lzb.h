@@ -156,14 +156,34 @@ int lzb_codebook_from_lengths(const uint8_t *lengths, uint32_t cap, uint64_t *co
  * ceil(bit_len/8) bytes at `out` (MSB first, last byte zero padded); out
  * need not be aligned.  out_bytes must be >= ceil(bit_len/8) where bit_len =
  * sum(len(sym)) (known beforehand from lzb_codebook's u[0]).  maxlen = the
- * book's longest code word (lzb_codebook's u[2]; 0 = unknown, generic path).
+ * book's longest code word (lzb_codebook's u[2]; 0 = unknown, generic path;
+ * LZB_MAXLEN_DEVICE = the book is built by lzb_codebook earlier in the same
+ * stream and not read back: 16-bit symbols, cap <= 4096, buffers sized for
+ * 32-bit code words, code = LZB_E_RETRY if the book has a longer one -- the
+ * output is then unusable and the caller re-runs with the true maxlen).
  * st->u[0] = bit_len.  code = LZB_E_DATA if a symbol has no code word.
  * ------------------------------------------------------------------- */
+#define LZB_MAXLEN_DEVICE 0xFFFFFFFFu
 size_t lzb_huff_encode_scratch_bytes(uint64_t n);
 int lzb_huff_encode(const void *sym, int sym_bytes, uint64_t n, const uint8_t *lengths,
                     const uint64_t *codes, uint32_t cap, uint32_t maxlen, uint8_t *out,
                     uint64_t out_bytes, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
                     void *stream);
+
+/* Device-side assembly of a Huffman archive (single-sync compress; archive
+ * layout of P/pipeline.py:184-221).  `header` (host, 130 bytes) is the packed
+ * header with everything but outlier_count, sym_len, out_off and out_len,
+ * which come from st_quant->u[0] (K1's outlier count) and st_book->u[0]
+ * (K2's bit length).  Writes the header, the code lengths at 136, the
+ * [bit_len][count] prefix at sym_off (= align8(136 + cap); the bit stream
+ * itself is written by lzb_huff_encode at sym_off + 16), the zero padding
+ * and the 16-byte outlier records.  st->u[0] = total archive bytes,
+ * st->u[1] = out_off; code = LZB_E_CAPACITY if total > arc_bytes (nothing
+ * written).  Does nothing if st_quant or st_book carries an error. */
+int lzb_archive_finalize_huff(uint8_t *arc, uint64_t arc_bytes, const uint8_t *header, uint64_t sym_off,
+                              const uint8_t *lengths, uint32_t cap, const lzb_dstatus *st_quant,
+                              const lzb_dstatus *st_book, const void *records, lzb_dstatus *st,
+                              void *stream);
 
 /* Multi-GPU slab variant of lzb_huff_encode: the first bit lands at bit
  * `bit_offset` (0..7, MSB first) of out[0]; bits outside the slab are zero so

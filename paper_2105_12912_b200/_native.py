@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "liblzb.so")
 LZB_OK, LZB_E_ARG, LZB_E_DATA, LZB_E_OVERFLOW = 0, 1, 2, 3
 LZB_E_CORRUPT, LZB_E_CUDA, LZB_E_ASSERT, LZB_E_CAPACITY = 4, 5, 6, 7
 LZB_E_RETRY = 8  # the fast decoder could not resolve the stream: run the robust one
+LZB_MAXLEN_DEVICE = 0xFFFFFFFF  # lzb_huff_encode: the code book is still on the device
 
 STATUS_BYTES = 64
 
@@ -49,6 +50,7 @@ SIGNATURES = {
     "lzb_codebook_from_lengths": (_I, [_P, _U32, _P, _P, _P, _SZ, _P]),
     "lzb_huff_encode_scratch_bytes": (_SZ, [_U64]),
     "lzb_huff_encode": (_I, [_P, _I, _U64, _P, _P, _U32, _U32, _P, _U64, _P, _P, _SZ, _P]),
+    "lzb_archive_finalize_huff": (_I, [_P, _U64, _P, _U64, _P, _U32, _P, _P, _P, _P, _P]),
     "lzb_huff_encode_at": (_I, [_P, _I, _U64, _P, _P, _U32, _U32, _U64, _P, _U64, _P, _P, _SZ, _P]),
     "lzb_huff_decode_scratch_bytes": (_SZ, [_U64, _U32, _U32]),
     "lzb_huff_decode": (_I, [_P, _U64, _U64, _P, _U32, _U32, _P, _I, _P, _P, _SZ, _P]),

@@ -305,8 +305,18 @@ struct EncWParams {
 // Also the DataError checks (symbol >= cap, symbol without a code word).
 __global__ void __launch_bounds__(256) k_huff_count_w(const __grid_constant__ EncWParams p) {
     __shared__ uint8_t s_len[4096];
-    for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) s_len[i] = p.lengths[i];
-    __syncthreads();
+    // code words over 32 bits (possible only when the book was built on the
+    // device in this stream, LZB_MAXLEN_DEVICE): counted as 32 so every
+    // offset stays inside the buffers sized for 32, and reported as RETRY
+    int longer = 0;
+    for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) {
+        const uint32_t L = p.lengths[i];
+        longer |= L > 32;
+        s_len[i] = (uint8_t)(L > 32 ? 32 : L);
+    }
+    if (__syncthreads_or(longer)) {
+        if (threadIdx.x == 0) set_status(p.st, LZB_E_RETRY);
+    }
     const uint32_t lane = lane_id();
     const uint64_t NW = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t capm1 = p.cap - 1;
@@ -480,7 +490,7 @@ __global__ void __launch_bounds__(kWWarps * 32, 4) k_huff_encode_w(const __grid_
     for (uint32_t i = threadIdx.x; i < p.cap; i += blockDim.x) {
         const uint32_t L = p.lengths[i];
         const uint32_t cal = (L && L <= 32) ? (uint32_t)(p.codes[i] << (32 - L)) : 0u;
-        s_tab[i] = (uint64_t)cal | ((uint64_t)L << 32);
+        s_tab[i] = (uint64_t)cal | ((uint64_t)(L > 32 ? 32 : L) << 32);  // > 32: RETRY (count pass)
     }
     __syncthreads();
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -1360,8 +1370,12 @@ static int huff_encode_impl(const void *sym, int sym_bytes, uint64_t n, const ui
     LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
     if (n == 0) return LZB_OK;
     if (!sym || !out) return LZB_E_ARG;
-    if (sym_bytes == 2 && maxlen >= 1 && maxlen <= 32 && cap <= 4096 &&
-        (reinterpret_cast<uintptr_t>(sym) & 1) == 0)
+    const bool wpath = sym_bytes == 2 && cap <= 4096 && (reinterpret_cast<uintptr_t>(sym) & 1) == 0;
+    if (maxlen == LZB_MAXLEN_DEVICE) {  // book built on the device: the 32-bit path, sized for 32
+        if (!wpath) return LZB_E_ARG;
+        return huff_encode_w(sym, n, lengths, codes, cap, 32, out, bit_offset, st, scratch, scratch_bytes, s);
+    }
+    if (wpath && maxlen >= 1 && maxlen <= 32)
         return huff_encode_w(sym, n, lengths, codes, cap, maxlen, out, bit_offset, st, scratch,
                              scratch_bytes, s);
     uint64_t nt = (n + kETile - 1) / kETile;

@@ -208,6 +208,11 @@ def _as_device_values(field: Field):
     return torch.from_numpy(host).to("cuda")
 
 
+# Fields up to this many elements take the single-sync path: its archive
+# buffer is sized for the worst case (32-bit code words), ~4 bytes/element.
+_SINGLE_SYNC_MAX = 1 << 25
+
+
 def compress_device(field: Field, eb: float, eb_mode: str = "rel", cap: int = 1024,
                     workflow=None, chunk: ChunkSpec | None = None, select_mode: str = "exact",
                     threads: int = 1, values=None, prof=None) -> DeviceArchive:
@@ -215,10 +220,93 @@ def compress_device(field: Field, eb: float, eb_mode: str = "rel", cap: int = 10
 
     Same arguments and archive bytes as ``compress``; ``threads`` is accepted
     for API parity and ignored (the GPU is the thread pool).
+
+    Small Huffman-candidate fields run K1 -> K2 -> K3 -> archive assembly as
+    one launch sequence with a single status read at the end (no
+    mid-pipeline read-back, so the GPU never idles on the host); when that
+    read shows the field needs something else (RLE selection, a code word
+    over 32 bits, outlier capacity) the staged path below re-runs it.
     """
     eb_abs = _resolve_eb(eb_mode, eb, field.vmin, field.vmax)
     _check_cfg(eb_abs, cap)
     chunk = chunk or ChunkSpec.default_for(field.dims.ndim)
+    n = field.dims.count
+    chosen = resolve_workflow(workflow)
+    if (0 < n <= _SINGLE_SYNC_MAX and cap <= 4096 and code_bytes_for(cap) == 2 and select_mode == "exact"
+            and chosen in (None, Workflow.HUFFMAN)):
+        arc = _compress_single_sync(field, eb, eb_mode, eb_abs, cap, chosen, chunk, values, prof)
+        if arc is not None:
+            return arc
+    return _compress_staged(field, eb, eb_mode, eb_abs, cap, workflow, chunk, select_mode, values, prof)
+
+
+def _compress_single_sync(field: Field, eb, eb_mode, eb_abs, cap, chosen, chunk, values, prof):
+    """K1, K2, K3 and lzb_archive_finalize_huff back to back; one read-back.
+    Returns None when the staged path must run instead."""
+    dims = field.dims
+    n = dims.count
+    dt = dtype_name(field.values)
+    x = values if values is not None else _as_device_values(field)
+    dev = x.device
+    L = N.lib()
+    sp = N.stream_ptr()
+    g = N.geom(dims.as_tuple(), chunk.as_tuple())
+    codes = _pool.get("codes", n * 2, dev)
+    hist = _pool.get("hist", cap * 8, dev)
+    lengths = _pool.get("lengths", cap, dev)
+    cwords = _pool.get("cwords", cap * 8, dev)
+    st = _pool.get("status", 8 * N.STATUS_BYTES, dev)
+    stp = _dev(st)
+    cb_scr = _pool.get("cb_scratch", L.lzb_codebook_scratch_bytes(cap), dev)
+    cap_out = int(_pool.bufs.get(("outcap", str(dev)), 0) or min(n, n // 128 + 4096))
+    outl = _pool.get("outliers", cap_out * 16, dev)
+    qs = L.lzb_quantize_scratch_bytes(g, cap_out)
+    q_scr = _pool.get("q_scratch", qs, dev)
+    sym_off = _a8(_SECTION_BASE + cap)
+    worst = sym_off + 16 + 4 * n + 8 + 16 * cap_out  # code words <= 32 bits on this path
+    big = _pool.get("arc_stage", worst, dev)
+    es = L.lzb_huff_encode_scratch_bytes(n)
+    e_scr = _pool.get("e_scratch", es, dev)
+    with _Stage(prof, "K1_quantize"):
+        N.check_rc(L.lzb_quantize(_dev(x), _DTYPE_CODES[dt], g, eb_abs, cap, _dev(codes), 2, _dev(hist),
+                                  _dev(outl), cap_out, stp, _dev(q_scr), qs, sp), "quantize")
+    with _Stage(prof, "K2_codebook"):
+        N.check_rc(L.lzb_codebook(_dev(hist), cap, _dev(lengths), _dev(cwords), stp + N.STATUS_BYTES,
+                                  _dev(cb_scr), cb_scr.numel(), sp), "codebook")
+    with _Stage(prof, "K3_huff_encode"):
+        N.check_rc(L.lzb_huff_encode(_dev(codes), 2, n, _dev(lengths), _dev(cwords), cap, N.LZB_MAXLEN_DEVICE,
+                                     _dev(big) + sym_off + 16, worst - sym_off - 16, stp + 2 * N.STATUS_BYTES,
+                                     _dev(e_scr), es, sp), "huff_encode")
+    hdr = _HEADER.pack(MAGIC, VERSION, _DTYPE_CODES[dt], dims.ndim, dims.nx, dims.ny, dims.nz,
+                       chunk.cx, chunk.cy, chunk.cz, _EB_MODES[eb_mode], eb, field.vmin, field.vmax, cap,
+                       int(Workflow.HUFFMAN), n, 0, _SECTION_BASE, cap, sym_off, 0, 0, 0)
+    with _Stage(prof, "assemble"):
+        N.check_rc(L.lzb_archive_finalize_huff(_dev(big), worst, hdr, sym_off, _dev(lengths), cap, stp,
+                                               stp + N.STATUS_BYTES, _dev(outl), stp + 6 * N.STATUS_BYTES, sp),
+                   "finalize")
+    sq, sb, se, _, _, _, sf, _ = N.read_status(st[: 8 * N.STATUS_BYTES])  # the one sync
+    if sq.code == N.LZB_E_CAPACITY:
+        _pool.bufs[("outcap", str(dev))] = sq.u[0] + 1024
+        return None
+    N.raise_for(sq, "quantize")
+    N.raise_for(sb, "codebook")
+    if chosen is None and float(np.float64(sb.u[0]) / np.float64(sb.u[1])) <= RLE_THRESHOLD_BITS:
+        return None  # P/codebook.py:110-115 + P/smoothness.py:111-136 select RLE+VLE
+    if se.code == N.LZB_E_RETRY or sf.code == N.LZB_E_CAPACITY:
+        return None  # a code word over 32 bits
+    N.raise_for(se, "encode")
+    N.raise_for(sf, "finalize")
+    bits, n_out, total = sb.u[0], sq.u[0], sf.u[0]
+    arc = _new_archive(total, dev)
+    arc.copy_(big[:total])
+    header = ArchiveHeader(dt, dims, chunk, eb_mode, eb, field.vmin, field.vmax, cap, Workflow.HUFFMAN, n,
+                           n_out, (_SECTION_BASE, cap), (sym_off, 16 + (bits + 7) // 8),
+                           (sf.u[1], 16 * n_out))
+    return DeviceArchive(arc, header, total, (bits, n, int(sb.u[2])))
+
+
+def _compress_staged(field: Field, eb, eb_mode, eb_abs, cap, workflow, chunk, select_mode, values, prof):
+    """K1 + K2, one read-back, then the workflow's encoder sized from it."""
     dims = field.dims
     n = dims.count
     dt = dtype_name(field.values)
