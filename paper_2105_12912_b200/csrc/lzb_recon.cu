@@ -25,6 +25,7 @@
 
 #include "lzb_common.cuh"
 #include "lzb_recon3d.cuh"
+#include "lzb_recon2d.cuh"
 
 namespace lzb {
 
@@ -323,6 +324,7 @@ struct OutParams {
     const uint8_t *rec;  // 16-byte LE records, any alignment
     uint64_t n_out;
     int fast3d;          // tiles = 2^tshift consecutive chunk ordinals (8: K6, 16: fused K5+K6)
+    int fast2d;          // ChunkSpec(16,16): tiles of 8 chunk ordinals, key k << 8 | y << 4 | x
     uint32_t tshift;
     Geom g;
     uint32_t K;
@@ -348,6 +350,11 @@ __device__ __forceinline__ uint64_t tile_of(const OutParams &p, uint64_t idx, ui
     uint64_t x = idx % g.nx, yz = idx / g.nx;
     uint64_t y = yz % g.ny, z = yz / g.ny;
     uint64_t bx = x / g.cx, by = y / g.cy, bz = z / g.cz;
+    if (p.fast2d) {
+        const uint64_t ord = bx + g.nbx * by;
+        *boxpos = (uint32_t)(((ord & 7u) << 8) | ((y & 15) << 4) | (x & 15));
+        return ord >> 3;
+    }
     if (p.fast3d) {
         uint64_t ord = bx + g.nbx * (by + g.nby * bz);
         *boxpos = (uint32_t)(((ord & ((1u << p.tshift) - 1u)) << 9) | ((z & 7) << 6) | ((y & 7) << 3) | (x & 7));
@@ -649,6 +656,7 @@ static int nsms() {
 
 struct RcLayout {
     bool fast3d;
+    bool fast2d;
     bool box;
     uint32_t K;
     uint64_t tiles_per_row, ntiles;
@@ -658,7 +666,8 @@ static RcLayout rc_layout(const Geom &g) {
     RcLayout L;
     uint64_t vol = g.cx * g.cy * g.cz;
     L.fast3d = g.cx == 8 && g.cy == 8 && g.cz == 8;
-    if (L.fast3d) {
+    L.fast2d = g.cx == 16 && g.cy == 16 && g.cz == 1 && g.nz == 1;
+    if (L.fast3d || L.fast2d) {
         L.box = true;
         L.K = 0;
         L.tiles_per_row = 0;
@@ -740,6 +749,7 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
         op.rec = outliers;
         op.n_out = n_out;
         op.fast3d = L.fast3d;
+        op.fast2d = L.fast2d;
         op.tshift = 3;
         op.g = g;
         op.K = L.K;
@@ -762,7 +772,7 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
             k_out_scatter<<<go, 256, 0, s>>>(op);
             LZB_LAUNCH_CHECK();
         }
-        if (L.fast3d) {
+        if (L.fast3d || L.fast2d) {
             R3Params r3;
             r3.codes = codes;
             r3.g = g;
@@ -783,7 +793,7 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
             // driver exposes the tensor-map encoder and no int64 copy is asked for
             CUtensorMap ymap;
             memset(&ymap, 0, sizeof(ymap));
-            bool tma = dtype == 0 && !prequant_out && r3.vec_ok && tma_encode() != nullptr;
+            bool tma = L.fast3d && dtype == 0 && !prequant_out && r3.vec_ok && tma_encode() != nullptr;
             if (tma) {
                 cuuint64_t dims[3] = {g.nx, g.ny, g.nz};
                 cuuint64_t strides[2] = {g.nx * 4, g.nx * g.ny * 4};
@@ -804,8 +814,22 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
                 LZB_LAUNCH_CHECK();
                 return LZB_OK;
             };
+            auto launch2d = [&](auto kern) -> int {
+                int per_sm = 0;
+                LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kR3Threads, 0));
+                if (per_sm < 1) per_sm = 1;
+                uint64_t grid = umin64((uint64_t)sm * per_sm, (L.ntiles + kR3Warps - 1) / kR3Warps);
+                kern<<<(unsigned)(grid ? grid : 1), kR3Threads, 0, s>>>(r3);
+                LZB_LAUNCH_CHECK();
+                return LZB_OK;
+            };
             int rc;
-            if (code_bytes == 2)
+            if (L.fast2d)
+                rc = code_bytes == 2 ? (dtype == 0 ? launch2d(k_reconstruct2d16<uint16_t, float>)
+                                                   : launch2d(k_reconstruct2d16<uint16_t, double>))
+                                     : (dtype == 0 ? launch2d(k_reconstruct2d16<uint32_t, float>)
+                                                   : launch2d(k_reconstruct2d16<uint32_t, double>));
+            else if (code_bytes == 2)
                 rc = dtype == 0 ? (tma ? launch(k_reconstruct3d8<uint16_t, float, true>)
                                        : launch(k_reconstruct3d8<uint16_t, float, false>))
                                 : launch(k_reconstruct3d8<uint16_t, double, false>);
