@@ -122,10 +122,12 @@ class Status:
 
     __slots__ = ("code", "detail", "u")
 
-    def __init__(self, raw: np.ndarray):
-        self.code = int(raw[:4].view(np.int32)[0])
-        self.detail = int(raw[4:8].view(np.int32)[0])
-        self.u = [int(v) for v in raw[8:56].view(np.uint64)]
+    def __init__(self, raw: np.ndarray | None = None, code: int = 0, detail: int = 0, u=None):
+        if raw is not None:
+            code = int(raw[:4].view(np.int32)[0])
+            detail = int(raw[4:8].view(np.int32)[0])
+            u = [int(v) for v in raw[8:56].view(np.uint64)]
+        self.code, self.detail, self.u = code, detail, u
 
     def f64(self, i: int) -> float:
         return float(np.array([self.u[i]], np.uint64).view(np.float64)[0])
@@ -178,9 +180,13 @@ def read_status(block) -> list[Status]:
         raise ValueError("status block larger than the read-back region")
     h = _pinned_stage(8192)
     check_rc(lib().lzb_copy_bytes(h.data_ptr(), block.data_ptr(), n, stream_ptr()), "copy")
-    torch.cuda.current_stream().synchronize()
-    raw = h[:n].numpy().copy().reshape(-1, STATUS_BYTES)
-    return [Status(r) for r in raw]
+    sync_current_stream()
+    rec = np.frombuffer(h.numpy(), _STATUS_DT, n // STATUS_BYTES)
+    return [Status(code=c, detail=d, u=u) for c, d, u in
+            zip(rec["code"].tolist(), rec["detail"].tolist(), rec["u"].tolist())]
+
+
+_STATUS_DT = np.dtype([("code", "<i4"), ("detail", "<i4"), ("u", "<u8", (6,)), ("pad", "V8")])
 
 
 def raise_for(st: Status, stage: str, corrupt_msg: str | None = None) -> None:
@@ -205,9 +211,26 @@ def raise_for(st: Status, stage: str, corrupt_msg: str | None = None) -> None:
 
 
 def stream_ptr() -> int:
+    """The current CUDA stream of the current device (raw cudaStream_t)."""
     import torch
 
-    return torch.cuda.current_stream().cuda_stream
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
+
+
+_SYNC = {}
+
+
+def sync_current_stream() -> None:
+    """Block until the current stream is idle (no torch.cuda.Stream object per call)."""
+    import torch
+
+    dev = torch._C._cuda_getDevice()
+    raw = torch._C._cuda_getCurrentRawStream(dev)
+    s = _SYNC.get((dev, raw))
+    if s is None:
+        s = _SYNC[(dev, raw)] = torch.cuda.ExternalStream(raw, device=dev) if raw \
+            else torch.cuda.default_stream(dev)
+    s.synchronize()
 
 
 def ptr(t) -> int:

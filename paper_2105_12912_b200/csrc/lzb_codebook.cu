@@ -434,8 +434,7 @@ extern "C" int lzb_codebook(const uint64_t *hist, uint32_t cap, uint8_t *lengths
     size_t smem = (size_t)np * 8 + (size_t)cap * 8 + (size_t)cap * 8 + (size_t)cap * 2;
     int use_smem = smem <= 160 * 1024;
     if (use_smem) {
-        LZB_CUDA_TRY(cudaFuncSetAttribute(k_codebook<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
+        LZB_CUDA_TRY(set_dyn_smem(k_codebook<true>, smem));
         k_codebook<true><<<1, kCbThreads, smem, s>>>((const unsigned long long *)hist, cap, lengths, codes,
                                                      st, c, np);
     } else {

@@ -5,6 +5,10 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "../../include/lzb.h"
 
 #define LZB_CUDA_TRY(expr)                                         \
@@ -16,6 +20,49 @@
 #define LZB_LAUNCH_CHECK() LZB_CUDA_TRY(cudaGetLastError())
 
 namespace lzb {
+
+// Host-side launch configuration cache.  cudaFuncSetAttribute (dynamic
+// shared memory opt-in) and the occupancy query cost microseconds per call,
+// which a small field would pay on every launch; both are per (device,
+// kernel[, block, shared memory]) constants, so they are asked once.
+struct LaunchCache {
+    std::mutex mu;
+    std::map<std::tuple<int, const void *>, size_t> smem;
+    std::map<std::tuple<int, const void *, int, size_t>, int> occ;
+};
+static inline LaunchCache &launch_cache() {
+    static LaunchCache c;
+    return c;
+}
+template <typename K>
+static inline cudaError_t set_dyn_smem(K kern, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    LaunchCache &c = launch_cache();
+    const auto key = std::make_tuple(dev, reinterpret_cast<const void *>(kern));
+    std::lock_guard<std::mutex> g(c.mu);
+    auto it = c.smem.find(key);
+    if (it != c.smem.end() && it->second >= bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) c.smem[key] = bytes;
+    return e;
+}
+template <typename K>
+static inline cudaError_t occupancy(int *per_sm, K kern, int threads, size_t smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    LaunchCache &c = launch_cache();
+    const auto key = std::make_tuple(dev, reinterpret_cast<const void *>(kern), threads, smem);
+    std::lock_guard<std::mutex> g(c.mu);
+    auto it = c.occ.find(key);
+    if (it != c.occ.end()) {
+        *per_sm = it->second;
+        return cudaSuccess;
+    }
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, smem);
+    if (e == cudaSuccess) c.occ[key] = *per_sm;
+    return e;
+}
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda);
 // a cached function pointer, nullptr if the driver lacks it.

@@ -1341,9 +1341,9 @@ static int huff_encode_w(const void *sym, uint64_t n, const uint8_t *lengths, co
     p.wwords = (32 * maxlen + 2 + 3) & ~3u;
     const size_t smem = (((size_t)cap * 8 + 15) & ~(size_t)15) + (size_t)kWWarps * kWTile * 2 +
                         (size_t)kWWarps * p.wwords * 4;
-    LZB_CUDA_TRY(cudaFuncSetAttribute(k_huff_encode_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LZB_CUDA_TRY(set_dyn_smem(k_huff_encode_w, smem));
     int per_sm = 0;
-    LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_huff_encode_w, kWWarps * 32, smem));
+    LZB_CUDA_TRY(occupancy(&per_sm, k_huff_encode_w, kWWarps * 32, smem));
     if (per_sm < 1) return LZB_E_ARG;
     uint64_t grid = (uint64_t)dev_sms() * per_sm;
     const uint64_t need = (ntw + kWWarps - 1) / kWWarps;
@@ -1410,9 +1410,9 @@ static int huff_encode_impl(const void *sym, int sym_bytes, uint64_t n, const ui
         if (shortc) kern = p.table_smem ? k_huff_encode<uint32_t, true, true> : k_huff_encode<uint32_t, true, false>;
         else kern = p.table_smem ? k_huff_encode<uint32_t, false, true> : k_huff_encode<uint32_t, false, false>;
     }
-    LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LZB_CUDA_TRY(set_dyn_smem(kern, smem));
     int per_sm = 0;
-    LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEThreads, smem));
+    LZB_CUDA_TRY(occupancy(&per_sm, kern, kEThreads, smem));
     uint64_t grid = (uint64_t)dev_sms() * (per_sm > 0 ? per_sm : 1);
     if (grid > nt) grid = nt;
     kern<<<(unsigned)grid, kEThreads, smem, s>>>(p);
@@ -1550,14 +1550,14 @@ static int dec_resolve_final(DecParams &p, const DecLayout &L, cudaStream_t s, i
     if (sym_bytes == 2 && cap <= 65536) {
         const size_t f9 = (size_t)kLutSize * (8 + 2 + 2 + 1) + (size_t)kF9Warps * kF9Stage +
                           (size_t)kF9Warps * 2 * kStgWords * 4;
-        LZB_CUDA_TRY(cudaFuncSetAttribute(k_dec_final9, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f9));
+        LZB_CUDA_TRY(set_dyn_smem(k_dec_final9, f9));
         const unsigned g9 = (unsigned)umin64((L.T + kF9Warps - 1) / kF9Warps, (uint64_t)sms);
         k_dec_final9<<<g9, kF9Warps * 32, f9, s>>>(p, cap);
     } else {
         const unsigned fg = (unsigned)umin64((L.T + kFThreads - 1) / kFThreads, (uint64_t)sms * 4);
         const size_t fsm = kLutSize * sizeof(uint64_t) + (size_t)(kFThreads / 32) * 32 * (kStage + 1) * sym_bytes;
         auto kern = sym_bytes == 2 ? k_dec_final<uint16_t> : k_dec_final<uint32_t>;
-        LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+        LZB_CUDA_TRY(set_dyn_smem(kern, fsm));
         kern<<<fg, kFThreads, fsm, s>>>(p);
     }
     LZB_LAUNCH_CHECK();
@@ -1640,7 +1640,7 @@ extern "C" int lzb_huff_decode(const uint8_t *bits, uint64_t bit_len, uint64_t c
     const int sms = dev_sms();
     const size_t f9 = (size_t)kLutSize * (8 + 2 + 2 + 1) + (size_t)kF9Warps * kF9Stage +
                       (size_t)kF9Warps * 2 * kStgWords * 4;
-    LZB_CUDA_TRY(cudaFuncSetAttribute(k_dec_final9, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f9));
+    LZB_CUDA_TRY(set_dyn_smem(k_dec_final9, f9));
     const unsigned g9 = (unsigned)umin64((p.T + kF9Warps - 1) / kF9Warps, (uint64_t)sms);
     k_dec_final9<<<g9, kF9Warps * 32, f9, s>>>(q, cap);
     LZB_LAUNCH_CHECK();

@@ -611,9 +611,9 @@ static int launch_quant(const QuantParams &qp, cudaStream_t s) {
     size_t smem = (BOX ? kTile * sizeof(int64_t) : 0) + kTile * sizeof(SymT) + kTile / 8 +
                   (qp.cap <= kSmemHistMaxCap ? qp.cap * sizeof(uint32_t) : 0);
     auto kern = k_quantize<InT, SymT, BOX>;
-    LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LZB_CUDA_TRY(set_dyn_smem(kern, smem));
     int per_sm = 0;
-    LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQThreads, smem));
+    LZB_CUDA_TRY(occupancy(&per_sm, kern, kQThreads, smem));
     if (per_sm < 1) per_sm = 1;
     uint64_t grid = (uint64_t)device_sms() * per_sm;
     if (grid > qp.ntiles) grid = qp.ntiles ? qp.ntiles : 1;
@@ -744,9 +744,9 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
                 return LZB_E_CUDA;
             const size_t tsm = (size_t)kT1Stages * kT1Tile + 1024 + (size_t)kT1Warps * 16 * 32 * 4 +
                                (size_t)kT1Warps * 512 * 2 + (size_t)cap * 4;
-            LZB_CUDA_TRY(cudaFuncSetAttribute(k_quantize3d8_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+            LZB_CUDA_TRY(set_dyn_smem(k_quantize3d8_tma, tsm));
             int per_sm = 0;
-            LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantize3d8_tma, kT1Threads, tsm));
+            LZB_CUDA_TRY(occupancy(&per_sm, k_quantize3d8_tma, kT1Threads, tsm));
             if (per_sm < 1) per_sm = 1;
             const uint64_t grid = umin64((uint64_t)device_sms() * per_sm, tp.nst);
             tp.step_q = (uint32_t)((grid ? grid : 1) / tp.tpr);
@@ -755,9 +755,9 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
             LZB_LAUNCH_CHECK();
         }
         auto launch = [&](auto kern) -> int {
-            LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            LZB_CUDA_TRY(set_dyn_smem(kern, smem));
             int per_sm = 0;
-            LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQ3Threads, smem));
+            LZB_CUDA_TRY(occupancy(&per_sm, kern, kQ3Threads, smem));
             if (per_sm < 1) per_sm = 1;
             uint64_t grid = umin64((uint64_t)device_sms() * per_sm, (q3.ntiles + kQ3Warps - 1) / kQ3Warps);
             kern<<<(unsigned)(grid ? grid : 1), kQ3Threads, smem, s>>>(q3);
@@ -766,9 +766,9 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
         };
         auto launch2d = [&](auto kern) -> int {
             const size_t sm2 = (size_t)kQ3Warps * 16 * 32 * 4 + (size_t)cap * 4;
-            LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+            LZB_CUDA_TRY(set_dyn_smem(kern, sm2));
             int per_sm = 0;
-            LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQ3Threads, sm2));
+            LZB_CUDA_TRY(occupancy(&per_sm, kern, kQ3Threads, sm2));
             if (per_sm < 1) per_sm = 1;
             uint64_t grid = umin64((uint64_t)device_sms() * per_sm, (q3.ntiles + kQ3Warps - 1) / kQ3Warps);
             kern<<<(unsigned)(grid ? grid : 1), kQ3Threads, sm2, s>>>(q3);

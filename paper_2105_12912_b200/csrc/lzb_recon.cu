@@ -805,9 +805,9 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
             }
             const size_t ysm = tma ? (size_t)kR3Warps * 4096 : 0;
             auto launch = [&](auto kern) -> int {
-                if (ysm) LZB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ysm));
+                if (ysm) LZB_CUDA_TRY(set_dyn_smem(kern, ysm));
                 int per_sm = 0;
-                LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kR3Threads, ysm));
+                LZB_CUDA_TRY(occupancy(&per_sm, kern, kR3Threads, ysm));
                 if (per_sm < 1) per_sm = 1;
                 uint64_t grid = umin64((uint64_t)sm * per_sm, (L.ntiles + kR3Warps - 1) / kR3Warps);
                 kern<<<(unsigned)(grid ? grid : 1), kR3Threads, ysm, s>>>(r3, ymap);
@@ -816,7 +816,7 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
             };
             auto launch2d = [&](auto kern) -> int {
                 int per_sm = 0;
-                LZB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kR3Threads, 0));
+                LZB_CUDA_TRY(occupancy(&per_sm, kern, kR3Threads, 0));
                 if (per_sm < 1) per_sm = 1;
                 uint64_t grid = umin64((uint64_t)sm * per_sm, (L.ntiles + kR3Warps - 1) / kR3Warps);
                 kern<<<(unsigned)(grid ? grid : 1), kR3Threads, 0, s>>>(r3);
