@@ -201,6 +201,52 @@ __device__ __forceinline__ void huffman_merge(const CbScratch &sc, uint32_t n) {
     }
 }
 
+// The u32 two-queue merge for books in shared memory, one thread, six-deep
+// register windows: L0..L5 = leaf weights li..li+5 (lw is padded with the
+// "none" marker past n), I0..I5 = internal weights ii..ii+5 (wi starts as
+// all "none", so an unwritten slot reads as an empty queue).  A step takes
+// both pops from L0/I0 and the first pop's survivors (X0 / Y0), shifts both
+// windows with selects, patches the new node into positions 0..3, and
+// reloads positions 4 and 5 -- which the next step reads only in its
+// selects, a full step after the load, so shared-memory latency never sits
+// on the compare -> select -> compare chain.
+__device__ __forceinline__ void huffman_merge32(const uint32_t *lw, uint32_t *wi, uint32_t *parent, uint32_t n) {
+    uint32_t L0 = lw[0], L1 = lw[1], L2 = lw[2], L3 = lw[3], L4 = lw[4], L5 = lw[5];
+    uint32_t I0 = wi[0], I1 = wi[1], I2 = wi[2], I3 = wi[3], I4 = wi[4], I5 = wi[5];
+    uint32_t li = 0, ii = 0;
+    for (uint32_t ni = 0; ni + 1 < n; ni++) {
+        const bool a = L0 <= I0;  // first pop: a leaf (ties go to leaves)
+        const uint32_t X0 = a ? L1 : L0, X1 = a ? L2 : L1, X2 = a ? L3 : L2, X3 = a ? L4 : L3, X4 = a ? L5 : L4;
+        const uint32_t Y0 = a ? I0 : I1, Y1 = a ? I1 : I2, Y2 = a ? I2 : I3, Y3 = a ? I3 : I4, Y4 = a ? I4 : I5;
+        const bool b = X0 <= Y0;  // second pop
+        const uint32_t nw = min(L0, I0) + min(X0, Y0);
+        const uint32_t pv = n + ni;
+        parent[a ? li : n + ii] = pv;
+        const uint32_t li1 = li + (uint32_t)a, ii1 = ii + (uint32_t)!a;
+        parent[b ? li1 : n + ii1] = pv;
+        wi[ni] = nw;
+        li = li1 + (uint32_t)b;
+        ii = ii1 + (uint32_t)!b;
+        L0 = b ? X1 : X0;
+        L1 = b ? X2 : X1;
+        L2 = b ? X3 : X2;
+        L3 = b ? X4 : X3;
+        I0 = b ? Y0 : Y1;
+        I1 = b ? Y1 : Y2;
+        I2 = b ? Y2 : Y3;
+        I3 = b ? Y3 : Y4;
+        const uint32_t pos = ni - ii;  // the new node's place in the internal window
+        I0 = pos == 0 ? nw : I0;
+        I1 = pos == 1 ? nw : I1;
+        I2 = pos == 2 ? nw : I2;
+        I3 = pos == 3 ? nw : I3;
+        L4 = lw[li + 4];
+        L5 = lw[li + 5];
+        I4 = wi[ii + 4];
+        I5 = wi[ii + 5];
+    }
+}
+
 // kSmem: small books, the whole tree lives in shared memory (the pointers
 // are derived from the shared array in this instantiation, so the compiler
 // emits LDS/STS instead of generic loads -- the serial merge is latency bound)
@@ -264,15 +310,25 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
         if (threadIdx.x == 0) lengths[sc.key[0] & 0xFFFFF] = 1;  // lone symbol -> 1 bit
     } else {
         // two-queue Huffman merge (sequential; n-1 steps) on thread 0; see
-        // huffman_merge for the register windows that keep shared-memory
-        // latency off the step's dependency chain
-        if (threadIdx.x == 0) {
-            if (s_tot < (1ull << 32) - 1)  // every weight below the u32 "none" marker
+        // huffman_merge32 / huffman_merge for the register windows that keep
+        // shared-memory latency off the step's dependency chain
+        const bool w32 = s_tot < (1ull << 32) - 1;  // every weight below the u32 "none" marker
+        if (kSmem && w32 && n + 8 <= 2 * cap) {  // wint holds 2 cap u32 slots
+            uint32_t *lw = reinterpret_cast<uint32_t *>(sc.depth + 2 * cap + 16 - ((2 * cap) & 15));
+            uint32_t *wi = reinterpret_cast<uint32_t *>(sc.wint);
+            for (uint32_t i = threadIdx.x; i < n + 8; i += blockDim.x) {
+                lw[i] = i < n ? (uint32_t)(sc.key[i] >> 20) : 0xFFFFFFFFu;
+                wi[i] = 0xFFFFFFFFu;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) huffman_merge32(lw, wi, sc.parent, n);
+        } else if (threadIdx.x == 0) {
+            if (w32)
                 huffman_merge<uint32_t>(sc, n);
             else
                 huffman_merge<uint64_t>(sc, n);
-            s_clk[1] = clock64() - t0;
         }
+        if (threadIdx.x == 0) s_clk[1] = clock64() - t0;
         __syncthreads();
         // depths (number of ancestors) of the 2n-1 nodes, root = node 2n-2
         const uint32_t nn = 2 * n - 1, root = nn - 1;
@@ -431,7 +487,8 @@ extern "C" int lzb_codebook(const uint64_t *hist, uint32_t cap, uint8_t *lengths
     c.depth = sc.take<uint8_t>(2 * cap);
     if (!c.depth) return LZB_E_ARG;
     LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
-    size_t smem = (size_t)np * 8 + (size_t)cap * 8 + (size_t)cap * 8 + (size_t)cap * 2;
+    // key | wint | parent | depth | (16-aligned) u32 leaf weights for the merge window
+    size_t smem = (size_t)np * 8 + (size_t)cap * 8 + (size_t)cap * 8 + (size_t)cap * 2 + 16 + ((size_t)cap + 16) * 4;
     int use_smem = smem <= 160 * 1024;
     if (use_smem) {
         LZB_CUDA_TRY(set_dyn_smem(k_codebook<true>, smem));
