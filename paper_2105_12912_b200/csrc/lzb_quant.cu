@@ -545,7 +545,8 @@ static bool box_mode_ok(const Geom &g, uint32_t *K) {
 struct QuantLayout {
     uint64_t ntiles;
     bool fast3d;
-    bool fast2d;  // ChunkSpec(16,16) on a 2D grid: k_quantize2d16
+    bool fast2d;  // ChunkSpec(16,16) on a 2D grid: k_quantize_r8<2>
+    bool fast1d;  // ChunkSpec(256) on a 1D grid: k_quantize_r8<1>
     bool box;
     uint32_t K;
     uint64_t tiles_per_row;
@@ -568,7 +569,8 @@ static QuantLayout quant_layout(const Geom &g) {
     L.nrows_chunk = g.nby * g.nbz;
     L.fast3d = g.cx == 8 && g.cy == 8 && g.cz == 8;
     L.fast2d = g.cx == 16 && g.cy == 16 && g.cz == 1 && g.nz == 1;
-    if (L.fast3d || L.fast2d) {
+    L.fast1d = g.cx == 256 && g.cy == 1 && g.cz == 1 && g.ny == 1 && g.nz == 1;
+    if (L.fast3d || L.fast2d || L.fast1d) {
         uint64_t nch = g.nbx * g.nby * g.nbz;
         uint64_t nt = (nch + kQ3TileChunks - 1) / kQ3TileChunks;
         if (nt > L.ntiles) L.ntiles = nt;
@@ -586,7 +588,7 @@ static void quant_scratch(S &s, const QuantLayout &L, uint64_t cap_out) {
     s.template take<uint64_t>(L.nrows_chunk);            // seg start
     s.template take<uint64_t>(L.nrows_chunk);            // seg end
     s.template take<uint64_t>((L.nrows_grid + 2047) / 2048 + 1);  // scan look-back
-    if (L.fast3d || L.fast2d) {
+    if (L.fast3d || L.fast2d || L.fast1d) {
         s.template take<uint64_t>(L.ntiles * 2 * kQ3Slot);  // record slots
         s.template take<uint32_t>(L.ntiles);                // tile counts
         s.template take<uint32_t>(L.ntiles);                // overflow list
@@ -657,7 +659,7 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
     if (!scan_lb) return LZB_E_ARG;
     uint64_t *slots = nullptr, *tile_off = nullptr, *slb = nullptr;
     uint32_t *tile_cnt = nullptr, *over_list = nullptr;
-    if (L.fast3d || L.fast2d) {
+    if (L.fast3d || L.fast2d || L.fast1d) {
         slots = sc.take<uint64_t>(L.ntiles * 2 * kQ3Slot);
         tile_cnt = sc.take<uint32_t>(L.ntiles);
         over_list = sc.take<uint32_t>(L.ntiles);
@@ -696,7 +698,7 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
     qp.tiles_per_row = L.tiles_per_row;
 
     int rc;
-    if ((L.fast3d || L.fast2d) && dtype != 2) {
+    if ((L.fast3d || L.fast2d || L.fast1d) && dtype != 2) {
         Q3Params q3;
         q3.x = x;
         q3.g = g;
@@ -723,6 +725,7 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
         q3.tile_off = tile_off;
         const size_t esz = dtype == 0 ? 4 : 8;
         q3.vec_ok = (g.nx % (16 / esz) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+        if (L.fast1d) q3.vec_ok = (reinterpret_cast<uintptr_t>(x) & 15) == 0;  // chunks start at 256 k
         size_t smem = (size_t)kQ3Warps * 2 * 32 * 16 * (dtype == 0 ? 4 : 8) +
                       (size_t)kQ3Warps * 512 * code_bytes + (size_t)kQ3Warps * 16 * 32 * 4 +
                       (size_t)cap * 4;
@@ -778,10 +781,15 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
         if (tma)
             rc = LZB_OK;
         else if (L.fast2d)
-            rc = dtype == 0 ? (code_bytes == 2 ? launch2d(k_quantize2d16<float, uint16_t>)
-                                               : launch2d(k_quantize2d16<float, uint32_t>))
-                            : (code_bytes == 2 ? launch2d(k_quantize2d16<double, uint16_t>)
-                                               : launch2d(k_quantize2d16<double, uint32_t>));
+            rc = dtype == 0 ? (code_bytes == 2 ? launch2d(k_quantize_r8<2, float, uint16_t>)
+                                               : launch2d(k_quantize_r8<2, float, uint32_t>))
+                            : (code_bytes == 2 ? launch2d(k_quantize_r8<2, double, uint16_t>)
+                                               : launch2d(k_quantize_r8<2, double, uint32_t>));
+        else if (L.fast1d)
+            rc = dtype == 0 ? (code_bytes == 2 ? launch2d(k_quantize_r8<1, float, uint16_t>)
+                                               : launch2d(k_quantize_r8<1, float, uint32_t>))
+                            : (code_bytes == 2 ? launch2d(k_quantize_r8<1, double, uint16_t>)
+                                               : launch2d(k_quantize_r8<1, double, uint32_t>));
         else if (dtype == 0)
             rc = code_bytes == 2 ? launch(k_quantize3d8<float, uint16_t>) : launch(k_quantize3d8<float, uint32_t>);
         else
@@ -796,13 +804,14 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
             k_q3_compact<<<(unsigned)umin64((q3.ntiles * 32 + 255) / 256, (uint64_t)sms * 16), 256, 0, s>>>(q3);
             LZB_LAUNCH_CHECK();
             size_t esm = (size_t)kQ3Warps * 512 * code_bytes;
-            if (L.fast2d) {
-                if (dtype == 0) {
-                    if (code_bytes == 2) k_q2_emit<float, uint16_t><<<sms, kQ3Threads, 0, s>>>(q3);
-                    else k_q2_emit<float, uint32_t><<<sms, kQ3Threads, 0, s>>>(q3);
+            if (L.fast2d || L.fast1d) {
+                auto emit = [&](auto kern) { kern<<<sms, kQ3Threads, 0, s>>>(q3); };
+                if (L.fast2d) {
+                    if (dtype == 0) code_bytes == 2 ? emit(k_q2_emit<2, float, uint16_t>) : emit(k_q2_emit<2, float, uint32_t>);
+                    else code_bytes == 2 ? emit(k_q2_emit<2, double, uint16_t>) : emit(k_q2_emit<2, double, uint32_t>);
                 } else {
-                    if (code_bytes == 2) k_q2_emit<double, uint16_t><<<sms, kQ3Threads, 0, s>>>(q3);
-                    else k_q2_emit<double, uint32_t><<<sms, kQ3Threads, 0, s>>>(q3);
+                    if (dtype == 0) code_bytes == 2 ? emit(k_q2_emit<1, float, uint16_t>) : emit(k_q2_emit<1, float, uint32_t>);
+                    else code_bytes == 2 ? emit(k_q2_emit<1, double, uint16_t>) : emit(k_q2_emit<1, double, uint32_t>);
                 }
             } else if (dtype == 0) {
                 if (code_bytes == 2) k_q3_emit<float, uint16_t><<<sms, kQ3Threads, esm, s>>>(q3);

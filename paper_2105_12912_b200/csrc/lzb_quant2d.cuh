@@ -1,15 +1,18 @@
-// K1 for 2D fields with ChunkSpec(16,16): one warp per 16x16 chunk, eight
-// consecutive chunk ordinals per warp task ("warp tile"), persistent CTAs.
+// K1 for 2D fields with ChunkSpec(16,16) and 1D fields with ChunkSpec(256):
+// one warp per 256-element chunk, eight per lane, eight consecutive chunk
+// ordinals per warp task ("warp tile"), persistent CTAs.
 // Included by lzb_quant.cu.  Semantics identical to the generic K1 and to the
 // reference (P/quantize.py:90-213, P/pipeline.py:102-105,
 // P/codebook.py:23-27); the outlier hand-off (per-tile slots, k_q3_scan,
 // k_q3_compact, overflow re-emission) is the 3D fast path's.
 //
-// Register layout: lane l owns row ly = l >> 1 of the chunk and the eight
-// x-elements xh = 8 * (l & 1) .. xh + 7.  The chunk's row-major stream
-// position of element j is then ly * ex + xh + j (8 l + j for a full chunk),
-// so a lane's eight codes are one 16-byte store and the warp's 256 codes one
-// contiguous 512-byte range.  The 2D Lorenzo delta is separable,
+// Register layout (D = 2): lane l owns row ly = l >> 1 of the chunk and the
+// eight x-elements xh = 8 * (l & 1) .. xh + 7; (D = 1) lane l owns elements
+// 8 l .. 8 l + 7.  The chunk's stream position of element j is then
+// ly * ex + xh + j, resp. 8 l + j (8 l + j for every full chunk), so a lane's
+// eight codes are one 16-byte store and the warp's 256 codes one contiguous
+// 512-byte range.  1D: d = q - (left neighbour), in-lane or lane l - 1's last
+// element.  2D: the Lorenzo delta is separable,
 //   d = dx(dy(q)):  dy needs the row above = lane l - 2 (shfl by 2),
 //                   dx the element to the left = in-lane, or the last
 //                   element of lane l - 1 for the right half (shfl by 1),
@@ -26,31 +29,56 @@ struct Q2Chunk {
     bool full;
 };
 
+template <int D>
 __device__ __forceinline__ Q2Chunk q2_chunk_of(const Geom &g, uint64_t c) {
     Q2Chunk k;
-    const uint64_t by = c / g.nbx, bx = c - by * g.nbx;
-    k.x0 = bx * 16;
-    k.y0 = by * 16;
-    k.ex = (uint32_t)umin64(16, g.nx - k.x0);
-    k.ey = (uint32_t)umin64(16, g.ny - k.y0);
-    k.full = k.ex == 16 && k.ey == 16;
-    k.base = g.nx * 16 * by + (uint64_t)k.ey * 16 * bx;  // rows above + full chunks to the left
+    if constexpr (D == 1) {
+        k.x0 = c * 256;
+        k.y0 = 0;
+        k.ex = (uint32_t)umin64(256, g.nx - k.x0);
+        k.ey = 1;
+        k.full = k.ex == 256;
+        k.base = k.x0;
+    } else {
+        const uint64_t by = c / g.nbx, bx = c - by * g.nbx;
+        k.x0 = bx * 16;
+        k.y0 = by * 16;
+        k.ex = (uint32_t)umin64(16, g.nx - k.x0);
+        k.ey = (uint32_t)umin64(16, g.ny - k.y0);
+        k.full = k.ex == 16 && k.ey == 16;
+        k.base = g.nx * 16 * by + (uint64_t)k.ey * 16 * bx;  // rows above + full chunks to the left
+    }
     return k;
 }
 
-// 2D Lorenzo deltas of the lane's eight values (int32 or int64)
-template <typename I>
+// global index / chunk stream position of the lane's first element
+template <int D>
+__device__ __forceinline__ uint64_t q2_lane_gi(const Q2Chunk &k, uint32_t lane, uint64_t nx) {
+    if constexpr (D == 1) return k.x0 + 8 * lane;
+    else return (k.x0 + 8 * (lane & 1)) + nx * (k.y0 + (lane >> 1));
+}
+template <int D>
+__device__ __forceinline__ uint32_t q2_lane_pos(const Q2Chunk &k, uint32_t lane) {
+    if constexpr (D == 1) return 8 * lane;
+    else return (lane >> 1) * k.ex + 8 * (lane & 1);
+}
+
+// Lorenzo deltas of the lane's eight values (int32 or int64)
+template <int D, typename I>
 __device__ __forceinline__ void q2_deltas(I (&v)[8], uint32_t lane) {
-    const bool top = lane < 2, right = lane & 1;
+    if constexpr (D == 2) {
+        const bool top = lane < 2;
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
-        const I up = __shfl_up_sync(f3::kFull, v[j], 2);
-        v[j] -= top ? (I)0 : up;
+        for (int j = 0; j < 8; j++) {
+            const I up = __shfl_up_sync(f3::kFull, v[j], 2);
+            v[j] -= top ? (I)0 : up;
+        }
     }
+    const bool has_left = D == 1 ? lane > 0 : (lane & 1) != 0;
     const I left = __shfl_up_sync(f3::kFull, v[7], 1);
 #pragma unroll
     for (int j = 7; j > 0; j--) v[j] -= v[j - 1];
-    v[0] -= right ? left : (I)0;
+    v[0] -= has_left ? left : (I)0;
 }
 
 // Outlier ranks in stream order: lanes in order, then x within the lane.
@@ -66,11 +94,11 @@ __device__ __forceinline__ uint32_t q2_rank(uint32_t om, uint32_t lane, uint32_t
     return inc - c;
 }
 
-template <typename I>
+template <int D, typename I>
 __device__ __forceinline__ void q2_records(const Q3Params &p, const Q2Chunk &k, uint32_t lane, uint32_t om,
                                            uint32_t rk, const I (&d)[8], uint64_t *stash, uint32_t wcount,
                                            bool emit, uint64_t emit_pos) {
-    const uint64_t gi0 = (k.x0 + 8 * (lane & 1)) + p.g.nx * (k.y0 + (lane >> 1));
+    const uint64_t gi0 = q2_lane_gi<D>(k, lane, p.g.nx);
 #pragma unroll
     for (int j = 0; j < 8; j++) {
         if (!((om >> j) & 1u)) continue;
@@ -79,7 +107,7 @@ __device__ __forceinline__ void q2_records(const Q3Params &p, const Q2Chunk &k, 
 }
 
 // codes of one chunk: store + histogram (not in emit mode)
-template <typename SymT>
+template <int D, typename SymT>
 __device__ __forceinline__ void q2_codes(const Q3Params &p, const Q2Chunk &k, uint32_t lane, uint32_t vmask,
                                          const uint32_t (&c)[8], uint32_t colbase, uint32_t hbase) {
     const uint32_t klo = p.cap >= 16 ? (uint32_t)(p.r - 8) : (uint32_t)(p.r + 16);
@@ -105,25 +133,26 @@ __device__ __forceinline__ void q2_codes(const Q3Params &p, const Q2Chunk &k, ui
             reinterpret_cast<uint4 *>(dst)[1] = make_uint4(c[4], c[5], c[6], c[7]);
         }
     } else {
-        const uint32_t pos0 = (lane >> 1) * k.ex + 8 * (lane & 1);
+        const uint32_t pos0 = q2_lane_pos<D>(k, lane);
 #pragma unroll
         for (int j = 0; j < 8; j++)
             if ((vmask >> j) & 1u) out[pos0 + j] = (SymT)c[j];
     }
 }
 
-// valid x-elements of the lane in chunk k
+// valid elements of the lane in chunk k
+template <int D>
 __device__ __forceinline__ uint32_t q2_vmask(const Q2Chunk &k, uint32_t lane) {
-    const uint32_t xh = 8 * (lane & 1), ly = lane >> 1;
+    const uint32_t xh = D == 1 ? 8 * lane : 8 * (lane & 1), ly = D == 1 ? 0u : lane >> 1;
     if (ly >= k.ey || xh >= k.ex) return 0u;
     const uint32_t w = k.ex - xh;
     return w >= 8 ? 0xFFu : ((1u << w) - 1u);
 }
 
-template <typename InT>
+template <int D, typename InT>
 __device__ __forceinline__ void q2_load(const Q3Params &p, const Q2Chunk &k, uint32_t lane, uint32_t vmask,
                                         InT (&x)[8]) {
-    const InT *in = static_cast<const InT *>(p.x) + (k.x0 + 8 * (lane & 1)) + p.g.nx * (k.y0 + (lane >> 1));
+    const InT *in = static_cast<const InT *>(p.x) + q2_lane_gi<D>(k, lane, p.g.nx);
     if (k.full && p.vec_ok) {
         if constexpr (sizeof(InT) == 4) {
             const float4 a = __ldg(reinterpret_cast<const float4 *>(in));
@@ -146,21 +175,21 @@ __device__ __forceinline__ void q2_load(const Q3Params &p, const Q2Chunk &k, uin
 
 // The exact int64 path (a value needs the reference's f64 division), out of
 // line: the whole chunk is redone from its input.
-template <typename InT, typename SymT>
+template <int D, typename InT, typename SymT>
 __device__ __noinline__ uint32_t q2_chunk_wide(const Q3Params *pp, uint64_t c, uint32_t lane, uint64_t *stash,
                                                uint32_t wcount, uint32_t colbase, uint32_t hbase, bool emit,
                                                uint64_t emit_pos, int *flags) {
     const Q3Params &p = *pp;
-    const Q2Chunk k = q2_chunk_of(p.g, c);
-    const uint32_t vm = q2_vmask(k, lane);
+    const Q2Chunk k = q2_chunk_of<D>(p.g, c);
+    const uint32_t vm = q2_vmask<D>(k, lane);
     InT x[8];
-    q2_load<InT>(p, k, lane, vm, x);
+    q2_load<D, InT>(p, k, lane, vm, x);
     int64_t d[8];
     int fl = 0;
 #pragma unroll
     for (int j = 0; j < 8; j++) d[j] = ((vm >> j) & 1u) ? f3::pq_exact((double)x[j], p.two_eb, p.slack, fl) : 0;
     if (!emit) *flags |= fl;
-    q2_deltas<int64_t>(d, lane);
+    q2_deltas<D, int64_t>(d, lane);
     uint32_t cc[8], om = 0;
 #pragma unroll
     for (int j = 0; j < 8; j++) {
@@ -171,17 +200,17 @@ __device__ __noinline__ uint32_t q2_chunk_wide(const Q3Params *pp, uint64_t c, u
     }
     uint32_t total;
     const uint32_t rk = q2_rank(om, lane, total);
-    if (om) q2_records<int64_t>(p, k, lane, om, rk, d, stash, wcount, emit, emit_pos);
-    if (!emit) q2_codes<SymT>(p, k, lane, vm, cc, colbase, hbase);
+    if (om) q2_records<D, int64_t>(p, k, lane, om, rk, d, stash, wcount, emit, emit_pos);
+    if (!emit) q2_codes<D, SymT>(p, k, lane, vm, cc, colbase, hbase);
     return total;
 }
 
 // One chunk from its (already loaded) values; returns the outlier count.
-template <typename InT, typename SymT>
+template <int D, typename InT, typename SymT>
 __device__ __forceinline__ uint32_t q2_chunk(const Q3Params &p, uint64_t c, const Q2Chunk &k, const InT (&x)[8],
                                              uint32_t lane, uint64_t *stash, uint32_t wcount, uint32_t colbase,
                                              uint32_t hbase, bool emit, uint64_t emit_pos, int &flags) {
-    const uint32_t vm = q2_vmask(k, lane);
+    const uint32_t vm = q2_vmask<D>(k, lane);
     int32_t d[8];
     bool ok = true;
 #pragma unroll
@@ -192,8 +221,8 @@ __device__ __forceinline__ uint32_t q2_chunk(const Q3Params &p, uint64_t c, cons
         d[j] = ((vm >> j) & 1u) ? v : 0;
     }
     if (!__all_sync(f3::kFull, ok))
-        return q2_chunk_wide<InT, SymT>(&p, c, lane, stash, wcount, colbase, hbase, emit, emit_pos, &flags);
-    q2_deltas<int32_t>(d, lane);
+        return q2_chunk_wide<D, InT, SymT>(&p, c, lane, stash, wcount, colbase, hbase, emit, emit_pos, &flags);
+    q2_deltas<D, int32_t>(d, lane);
     const int32_t r = p.r;
     uint32_t cc[8], om = 0;
 #pragma unroll
@@ -207,14 +236,14 @@ __device__ __forceinline__ uint32_t q2_chunk(const Q3Params &p, uint64_t c, cons
     uint32_t total = 0;
     if (any) {
         const uint32_t rk = q2_rank(om, lane, total);
-        if (om) q2_records<int32_t>(p, k, lane, om, rk, d, stash, wcount, emit, emit_pos);
+        if (om) q2_records<D, int32_t>(p, k, lane, om, rk, d, stash, wcount, emit, emit_pos);
     }
-    if (!emit) q2_codes<SymT>(p, k, lane, vm, cc, colbase, hbase);
+    if (!emit) q2_codes<D, SymT>(p, k, lane, vm, cc, colbase, hbase);
     return total;
 }
 
-template <typename InT, typename SymT>
-__global__ void __launch_bounds__(kQ3Threads, 4) k_quantize2d16(const __grid_constant__ Q3Params p) {
+template <int D, typename InT, typename SymT>
+__global__ void __launch_bounds__(kQ3Threads, 4) k_quantize_r8(const __grid_constant__ Q3Params p) {
     extern __shared__ __align__(16) unsigned char q2_smem[];
     // [s_col: warps x 16 bins x 32 lanes u32][s_hist: cap u32]
     uint32_t *s_col = reinterpret_cast<uint32_t *>(q2_smem);
@@ -238,8 +267,8 @@ __global__ void __launch_bounds__(kQ3Threads, 4) k_quantize2d16(const __grid_con
     Q2Chunk k{};
     InT x[8] = {};
     if (t < p.ntiles) {
-        k = q2_chunk_of(p.g, t * kQ3TileChunks);
-        q2_load<InT>(p, k, lane, q2_vmask(k, lane), x);
+        k = q2_chunk_of<D>(p.g, t * kQ3TileChunks);
+        q2_load<D, InT>(p, k, lane, q2_vmask<D>(k, lane), x);
     }
     while (t < p.ntiles) {
         const uint64_t c0 = t * kQ3TileChunks;
@@ -256,10 +285,10 @@ __global__ void __launch_bounds__(kQ3Threads, 4) k_quantize2d16(const __grid_con
             Q2Chunk kn = k;
             InT xn[8] = {};
             if (cn < p.nchunks) {
-                kn = q2_chunk_of(p.g, cn);
-                q2_load<InT>(p, kn, lane, q2_vmask(kn, lane), xn);
+                kn = q2_chunk_of<D>(p.g, cn);
+                q2_load<D, InT>(p, kn, lane, q2_vmask<D>(kn, lane), xn);
             }
-            wcount += q2_chunk<InT, SymT>(p, c, k, x, lane, slot, wcount, colbase, hbase, false, 0, flags);
+            wcount += q2_chunk<D, InT, SymT>(p, c, k, x, lane, slot, wcount, colbase, hbase, false, 0, flags);
             k = kn;
 #pragma unroll
             for (int j = 0; j < 8; j++) x[j] = xn[j];
@@ -287,7 +316,7 @@ __global__ void __launch_bounds__(kQ3Threads, 4) k_quantize2d16(const __grid_con
 
 // Tiles that overflowed their slots re-derive their outliers straight into
 // the final positions (noisy data only).
-template <typename InT, typename SymT>
+template <int D, typename InT, typename SymT>
 __global__ void __launch_bounds__(kQ3Threads) k_q2_emit(const __grid_constant__ Q3Params p) {
     const uint32_t lane = lane_id();
     const uint32_t nover = *p.n_over;
@@ -300,10 +329,10 @@ __global__ void __launch_bounds__(kQ3Threads) k_q2_emit(const __grid_constant__ 
         const uint64_t c1 = umin64(c0 + kQ3TileChunks, p.nchunks);
         uint64_t pos = p.tile_off[t];
         for (uint64_t c = c0; c < c1; c++) {
-            const Q2Chunk k = q2_chunk_of(p.g, c);
+            const Q2Chunk k = q2_chunk_of<D>(p.g, c);
             InT x[8];
-            q2_load<InT>(p, k, lane, q2_vmask(k, lane), x);
-            pos += q2_chunk<InT, SymT>(p, c, k, x, lane, nullptr, 0, 0, 0, true, pos, flags);
+            q2_load<D, InT>(p, k, lane, q2_vmask<D>(k, lane), x);
+            pos += q2_chunk<D, InT, SymT>(p, c, k, x, lane, nullptr, 0, 0, 0, true, pos, flags);
         }
     }
 }

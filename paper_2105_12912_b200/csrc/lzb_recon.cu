@@ -325,6 +325,7 @@ struct OutParams {
     uint64_t n_out;
     int fast3d;          // tiles = 2^tshift consecutive chunk ordinals (8: K6, 16: fused K5+K6)
     int fast2d;          // ChunkSpec(16,16): tiles of 8 chunk ordinals, key k << 8 | y << 4 | x
+    int fast1d;          // ChunkSpec(256) 1D: tiles of 8 chunks, key k << 8 | x mod 256
     uint32_t tshift;
     Geom g;
     uint32_t K;
@@ -350,6 +351,10 @@ __device__ __forceinline__ uint64_t tile_of(const OutParams &p, uint64_t idx, ui
     uint64_t x = idx % g.nx, yz = idx / g.nx;
     uint64_t y = yz % g.ny, z = yz / g.ny;
     uint64_t bx = x / g.cx, by = y / g.cy, bz = z / g.cz;
+    if (p.fast1d) {
+        *boxpos = (uint32_t)((((x >> 8) & 7u) << 8) | (x & 255));
+        return x >> 11;
+    }
     if (p.fast2d) {
         const uint64_t ord = bx + g.nbx * by;
         *boxpos = (uint32_t)(((ord & 7u) << 8) | ((y & 15) << 4) | (x & 15));
@@ -657,6 +662,7 @@ static int nsms() {
 struct RcLayout {
     bool fast3d;
     bool fast2d;
+    bool fast1d;
     bool box;
     uint32_t K;
     uint64_t tiles_per_row, ntiles;
@@ -667,7 +673,8 @@ static RcLayout rc_layout(const Geom &g) {
     uint64_t vol = g.cx * g.cy * g.cz;
     L.fast3d = g.cx == 8 && g.cy == 8 && g.cz == 8;
     L.fast2d = g.cx == 16 && g.cy == 16 && g.cz == 1 && g.nz == 1;
-    if (L.fast3d || L.fast2d) {
+    L.fast1d = g.cx == 256 && g.cy == 1 && g.cz == 1 && g.ny == 1 && g.nz == 1;
+    if (L.fast3d || L.fast2d || L.fast1d) {
         L.box = true;
         L.K = 0;
         L.tiles_per_row = 0;
@@ -750,6 +757,7 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
         op.n_out = n_out;
         op.fast3d = L.fast3d;
         op.fast2d = L.fast2d;
+        op.fast1d = L.fast1d;
         op.tshift = 3;
         op.g = g;
         op.K = L.K;
@@ -772,7 +780,7 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
             k_out_scatter<<<go, 256, 0, s>>>(op);
             LZB_LAUNCH_CHECK();
         }
-        if (L.fast3d || L.fast2d) {
+        if (L.fast3d || L.fast2d || L.fast1d) {
             R3Params r3;
             r3.codes = codes;
             r3.g = g;
@@ -789,6 +797,7 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
             r3.ticket = &tick[1];
             const size_t osz = dtype == 0 ? 4 : 8;
             r3.vec_ok = (g.nx % (16 / osz) == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
+            if (L.fast1d) r3.vec_ok = (reinterpret_cast<uintptr_t>(y) & 15) == 0;  // chunks start at 256 k
             // f32 output through TMA tensor stores (8x8x8 boxes) when the
             // driver exposes the tensor-map encoder and no int64 copy is asked for
             CUtensorMap ymap;
@@ -825,10 +834,15 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
             };
             int rc;
             if (L.fast2d)
-                rc = code_bytes == 2 ? (dtype == 0 ? launch2d(k_reconstruct2d16<uint16_t, float>)
-                                                   : launch2d(k_reconstruct2d16<uint16_t, double>))
-                                     : (dtype == 0 ? launch2d(k_reconstruct2d16<uint32_t, float>)
-                                                   : launch2d(k_reconstruct2d16<uint32_t, double>));
+                rc = code_bytes == 2 ? (dtype == 0 ? launch2d(k_reconstruct_r8<2, uint16_t, float>)
+                                                   : launch2d(k_reconstruct_r8<2, uint16_t, double>))
+                                     : (dtype == 0 ? launch2d(k_reconstruct_r8<2, uint32_t, float>)
+                                                   : launch2d(k_reconstruct_r8<2, uint32_t, double>));
+            else if (L.fast1d)
+                rc = code_bytes == 2 ? (dtype == 0 ? launch2d(k_reconstruct_r8<1, uint16_t, float>)
+                                                   : launch2d(k_reconstruct_r8<1, uint16_t, double>))
+                                     : (dtype == 0 ? launch2d(k_reconstruct_r8<1, uint32_t, float>)
+                                                   : launch2d(k_reconstruct_r8<1, uint32_t, double>));
             else if (code_bytes == 2)
                 rc = dtype == 0 ? (tma ? launch(k_reconstruct3d8<uint16_t, float, true>)
                                        : launch(k_reconstruct3d8<uint16_t, float, false>))
