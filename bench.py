@@ -703,14 +703,19 @@ def run_gpu(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize()
     clocks.mark("t0")
     t_c, t_d, profs = [], [], []
+    # inputs that fit in L2 (C1, C2): a 512 MB write evicts them before every timed step
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if nbytes < (512 << 20) else None
     for _ in range(args.steps):
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         prof = []
+        if flush is not None:
+            flush.zero_()
         e0.record()
         arc = lzb.compress_device(field, eb, prof=prof)
         e1.record()
-        pre = arc.data[: arc.header.symbols[0] + 32].cpu().numpy().tobytes()
-        y, _, _, _ = lzb.decompress_device(arc.data, raw_host=pre, prof=prof, out=ybuf)
+        # the device API's round trip: decompress takes the DeviceArchive
+        # compress returned (header known; no host read-back of the prefix)
+        y, _, _, _ = lzb.decompress_device(arc, prof=prof, out=ybuf)
         e2.record()
         torch.cuda.synchronize()
         t_c.append(e0.elapsed_time(e1) / 1e3)
@@ -884,7 +889,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "ms_per_step": round(t_step * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg["workload"], "elements": n, "bytes": nbytes,
-                   "workflow": hdr.workflow.name, "l2": "inputs 34 GB >> 126 MB L2 (no flush)",
+                   "workflow": hdr.workflow.name,
+                   "l2": "inputs >> 126 MB L2 (no flush)" if nbytes >= (512 << 20) else
+                         "L2 flushed (512 MB write) before every timed step",
+                   "decompress_input": "the DeviceArchive compress_device returned",
                    "parallelism": f"slab{world}" if world > 1 else "single"},
         "compress_gbs": round(nbytes / tc / 1e9, 3),
         "decompress_gbs": round(nbytes / td / 1e9, 3),

@@ -17,7 +17,7 @@ STAGES = {
     "K5_huff_decode": ("k_dec",),
     "K6_reconstruct": ("k_reconstruct3d8", "k_out_", "k_scan_tiles", "k_first_nonfinite", "k_rc_finish", "k_mm_init"),
 }
-TIME = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+TIME = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 rows = list(csv.reader(open(src)))
 hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
