@@ -698,7 +698,9 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
     qp.tiles_per_row = L.tiles_per_row;
 
     int rc;
-    if ((L.fast3d || L.fast2d || L.fast1d) && dtype != 2) {
+    // the register paths store codes with 16-byte vector stores
+    const bool codes_vec = (reinterpret_cast<uintptr_t>(codes) & 15) == 0;
+    if ((L.fast3d || L.fast2d || L.fast1d) && dtype != 2 && codes_vec) {
         Q3Params q3;
         q3.x = x;
         q3.g = g;

@@ -797,6 +797,7 @@ extern "C" int lzb_reconstruct(const void *codes, int code_bytes, const uint8_t 
             r3.ticket = &tick[1];
             const size_t osz = dtype == 0 ? 4 : 8;
             r3.vec_ok = (g.nx % (16 / osz) == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
+            r3.codes_vec = (reinterpret_cast<uintptr_t>(codes) & 15) == 0;
             if (L.fast1d) r3.vec_ok = (reinterpret_cast<uintptr_t>(y) & 15) == 0;  // chunks start at 256 k
             // f32 output through TMA tensor stores (8x8x8 boxes) when the
             // driver exposes the tensor-map encoder and no int64 copy is asked for

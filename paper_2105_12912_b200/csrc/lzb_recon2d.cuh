@@ -68,7 +68,7 @@ template <int D, typename SymT>
 __device__ __forceinline__ void r2_load(const R3Params &p, const R2Chunk &k, uint32_t lane, uint32_t vm,
                                         uint32_t (&c)[8]) {
     const SymT *cs = static_cast<const SymT *>(p.codes) + k.base;
-    if (k.full) {
+    if (k.full && p.codes_vec) {
         if constexpr (sizeof(SymT) == 2) {
             const uint4 a = __ldg(reinterpret_cast<const uint4 *>(cs + 8 * lane));
             const uint32_t w[4] = {a.x, a.y, a.z, a.w};
@@ -84,7 +84,7 @@ __device__ __forceinline__ void r2_load(const R3Params &p, const R2Chunk &k, uin
             c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
         }
     } else {
-        const uint32_t pos0 = D == 1 ? 8 * lane : (lane >> 1) * k.ex + 8 * (lane & 1);
+        const uint32_t pos0 = D == 1 ? 8 * lane : (lane >> 1) * k.ex + 8 * (lane & 1);  // full: 8 lane
 #pragma unroll
         for (int j = 0; j < 8; j++) c[j] = ((vm >> j) & 1u) ? (uint32_t)cs[pos0 + j] : 0u;
     }

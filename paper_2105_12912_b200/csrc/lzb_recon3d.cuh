@@ -35,6 +35,7 @@ struct R3Params {
     const uint64_t *brec;        // per record: [k << 9 | lz << 6 | ly << 3 | lx, delta]
     unsigned int *ticket;
     int vec_ok;
+    int codes_vec;  // the code stream is 16-byte aligned: vector / cp.async loads of full chunks
 };
 
 __device__ __forceinline__ unsigned long long r3_dkey(double v) {
@@ -233,7 +234,7 @@ __device__ __forceinline__ void r3_chunk(const R3Params &p, const f3::Chunk &ch,
     const uint32_t xmask = (1u << ch.ex) - 1u;
     const uint32_t m0 = (ly < ch.ey && lz0 < ch.ez) ? xmask : 0u;
     const uint32_t m1 = (ly < ch.ey && lz0 + 1 < ch.ez) ? xmask : 0u;
-    const bool fast = ch.full && ((ch.base & 7) == 0);
+    const bool fast = ch.full && ((ch.base & 7) == 0) && p.codes_vec;
     if (fast) {
 #pragma unroll
         for (int h = 0; h < 2; h++) {
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(kR3Threads, TMA ? 3 : 3)
         }
         uint64_t cbx = c0 % p.g.nbx, cby = (c0 / p.g.nbx) % p.g.nby, cbz = (c0 / p.g.nbx) / p.g.nby;
         f3::Chunk cur = f3::chunk_at(p.g, cbx, cby, cbz);
-        bool cur_pf = cur.full && (cur.base & 7) == 0;
+        bool cur_pf = cur.full && (cur.base & 7) == 0 && p.codes_vec;
         if (cur_pf) r3_prefetch<SymT>(p, cur, lane, stage_s);
         asm volatile("cp.async.commit_group;" ::: "memory");
         uint32_t sb = 0;
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(kR3Threads, TMA ? 3 : 3)
                     f3::chunk_step(p.g, cbx, cby, cbz);
                     nxt = f3::chunk_at(p.g, cbx, cby, cbz);
                 }
-                nxt_pf = nxt.full && (nxt.base & 7) == 0;
+                nxt_pf = nxt.full && (nxt.base & 7) == 0 && p.codes_vec;
                 if (nxt_pf) r3_prefetch<SymT>(p, nxt, lane, stage_s + (sb ^ 1) * kBuf);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");

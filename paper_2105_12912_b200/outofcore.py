@@ -1,0 +1,322 @@
+"""Block-by-block compression and decompression of fields larger than device
+memory (the spec's "block-by-block compression above a
+memory budget", which the reference leaves unimplemented).
+
+The field stays in host memory (a numpy array or ``np.memmap`` of a raw
+file); slabs of whole chunk layers along the slowest axis are moved through
+the GPU one at a time, so device memory holds one slab plus its codes.  The
+archive is the one ``compress`` writes for the whole field, byte for byte --
+the slabs play the part the ranks play in ``distributed.compress_sharded``:
+
+  pass A   each slab: K1 -> its code histogram and outlier count (the codes
+           are dropped); the histograms add up to the field's, which gives
+           the code book (K2) and the workflow decision exactly as compress;
+  pass B   each slab again: K1, then K3 at the slab's bit phase (its first
+           bit is the sum of the earlier slabs' bits) straight into the
+           archive's bit stream (the one byte shared with the previous slab
+           OR-merged), its outlier records at their offset.  RLE / RLE+VLE:
+           each slab's runs (K4) are stitched across slab boundaries with
+           ``distributed.plan_rle_stitch`` and the stitched run values are
+           Huffman-coded in pieces at their bit phases.
+
+Decompression goes the other way: the archive (compressed, so it normally
+fits) is put on the device; the dense bit stream is cut into ranges whose
+transfer maps (``lzb_huff_range_maps``) are chained from phase 0, and each
+slab decodes only the ranges that hold its symbols (``lzb_huff_range_decode``),
+reconstructs (K6) and goes back to host memory.  Run-length archives expand
+only the runs a slab overlaps.
+
+The per-slab work goes through the ``SlabOps`` of ``distributed`` (device
+kernels in production; the tests drive the same logic with a CPU stand-in).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import distributed as D
+from .errors import DataError
+from .grid import ChunkSpec, Dims
+
+_MAX_RUN = 0xFFFFFFFF
+_DEFAULT_BLOCK = 4 << 30  # bytes of field per slab
+
+
+def _host(x) -> np.ndarray:
+    return D._host_bytes(x)
+
+
+def _lens_u8(x) -> np.ndarray:
+    """code lengths as host uint8 (device tensor or numpy array of any int type)"""
+    if hasattr(x, "cpu"):
+        return x.cpu().numpy().astype(np.uint8)
+    return np.asarray(x).astype(np.uint8)
+
+
+def _plane(dims: Dims) -> int:
+    return dims.count // dims.as_tuple()[dims.ndim - 1]
+
+
+def _slabs(dims: Dims, chunk: ChunkSpec, field_bytes: int, block_bytes: int):
+    """Slab bounds along the slowest axis: whole chunk layers, about
+    block_bytes of field each."""
+    nb = max(1, math.ceil(field_bytes / max(1, block_bytes)))
+    out = [D.slab_bounds(dims, chunk, k, nb) for k in range(nb)]
+    return [(lo, hi) for lo, hi in out if hi > lo]
+
+
+class _Dev:
+    """Host block -> what the ops take (a device tensor, or the array itself)."""
+
+    def __init__(self, ops):
+        self.device = getattr(ops, "device", None)
+
+    def __call__(self, a: np.ndarray):
+        if self.device is None:
+            return np.ascontiguousarray(a)
+        import torch
+
+        return torch.from_numpy(np.ascontiguousarray(a)).to(self.device, non_blocking=False)
+
+
+def _check_decode(ops) -> None:
+    st = getattr(ops, "_decode_status", None)
+    if st is not None:
+        from . import _native as N
+
+        (s,) = N.read_status(st)
+        N.raise_for(s, "decode", "bit stream does not decode to its declared symbols")
+        ops._decode_status = None
+
+
+def field_range(values: np.ndarray, block_elems: int = 1 << 28) -> tuple[float, float]:
+    """min / max of a host field, block by block; non-finite values are a
+    DataError (P/grid.py:155-202)."""
+    vmin, vmax = math.inf, -math.inf
+    for a in range(0, values.size, block_elems):
+        b = np.asarray(values[a: a + block_elems])
+        if not np.isfinite(b).all():
+            bad = a + int(np.flatnonzero(~np.isfinite(b))[0])
+            raise DataError(f"non-finite value at flat offset {bad}")
+        vmin, vmax = min(vmin, float(b.min())), max(vmax, float(b.max()))
+    return vmin, vmax
+
+
+def compress_blocks(values: np.ndarray, dims: Dims, eb: float, eb_mode: str = "rel", cap: int = 1024,
+                    workflow=None, chunk: ChunkSpec | None = None, select_mode: str = "exact",
+                    vmin: float | None = None, vmax: float | None = None,
+                    block_bytes: int = _DEFAULT_BLOCK, ops=None) -> bytes:
+    """Archive bytes of a host field compressed slab by slab (same arguments
+    and same bytes as ``compress``); device memory holds one slab at a time."""
+    import torch
+
+    from .pipeline import _check_cfg, _resolve_eb, resolve_workflow
+    from .smoothness import RLE_THRESHOLD_BITS, Workflow, estimate_bits
+
+    values = values.reshape(-1)
+    if values.size != dims.count:
+        raise DataError(f"field has {values.size} values, dims need {dims.count}")
+    if values.dtype not in (np.float32, np.float64):
+        raise DataError(f"unsupported dtype {values.dtype}")
+    chunk = chunk or ChunkSpec.default_for(dims.ndim)
+    if vmin is None or vmax is None:
+        vmin, vmax = field_range(values)
+    eb_abs = _resolve_eb(eb_mode, eb, vmin, vmax)
+    _check_cfg(eb_abs, cap)
+    if select_mode not in ("exact", "estimate"):
+        raise DataError(f"unknown selection mode {select_mode!r}")
+    if ops is None:
+        ops = D.DeviceSlabOps(torch.device("cuda", torch.cuda.current_device()))
+    up = _Dev(ops)
+    plane = _plane(dims)
+    slabs = _slabs(dims, chunk, values.nbytes, block_bytes)
+    dtype_code = 0 if values.dtype == np.float32 else 1
+
+    def slab(lo, hi):
+        sd = D.slab_dims(dims, lo, hi)
+        return sd, ops.quantize(up(values[lo * plane: hi * plane]), sd, chunk, eb_abs, cap)
+
+    # ---- pass A: histograms and outlier counts ----
+    hists, outs = [], []
+    total = None
+    for lo, hi in slabs:
+        _, (codes, hist, n_out, recs) = slab(lo, hi)
+        del codes, recs
+        hists.append(hist)
+        outs.append(int(n_out))
+        h = ops.to_tensor(hist).to(torch.int64)
+        total = h.clone() if total is None else total + h
+    chosen = resolve_workflow(workflow)
+    book = None
+    if chosen is None:
+        if select_mode == "exact":
+            book = ops.codebook(total, cap)
+            b = float(np.float64(book[3]) / np.float64(dims.count))  # P/codebook.py:110-115
+        else:
+            b = estimate_bits(total.cpu().numpy())
+        chosen = Workflow.RLE_VLE if b <= RLE_THRESHOLD_BITS else Workflow.HUFFMAN
+    meta = dict(dims=dims, chunk=chunk, cap=cap, eb=eb, eb_mode=eb_mode, vmin=vmin, vmax=vmax,
+                dtype_code=dtype_code, total_out=sum(outs))
+    rec_off = np.concatenate([[0], np.cumsum(outs)]).astype(np.int64)
+
+    def put_records(blob, lay, k, lo, recs, n_out):
+        if n_out:
+            r = _host(ops.offset_records(recs, n_out, D.slab_index_offset(dims, lo)))[: 16 * n_out]
+            o = lay["out_off"] + 16 * int(rec_off[k])
+            blob[o: o + len(r)] = r
+
+    if chosen is Workflow.HUFFMAN:
+        lengths, words, maxlen, total_bits = book if book is not None else ops.codebook(total, cap)
+        bits = [ops.local_bits(h, lengths) for h in hists]
+        assert sum(bits) == total_bits
+        meta.update(workflow="HUFFMAN", total_bits=total_bits)
+        lay = D.archive_layout(meta)
+        blob = _start_blob(meta, lay, _lens_u8(lengths))
+        data = blob[lay["data_off"]: lay["data_off"] + lay["nbytes"]]
+        pos = 0
+        for k, (lo, hi) in enumerate(slabs):  # ---- pass B ----
+            sd, (codes, _, n_out, recs) = slab(lo, hi)
+            if bits[k]:
+                sl = _host(ops.encode_at(codes, sd.count, lengths, words, cap, maxlen, pos % 8, bits[k]))
+                a = pos // 8
+                end = min(lay["nbytes"], a + len(sl))
+                data[a:end] |= sl[: end - a]
+            put_records(blob, lay, k, lo, recs, n_out)
+            pos += bits[k]
+        return blob.tobytes()
+
+    # ---- RLE / RLE+VLE: per-slab runs, stitched across slabs ----
+    runs, infos, recs_all = [], [], []
+    for lo, hi in slabs:
+        sd, (codes, _, n_out, recs) = slab(lo, hi)
+        vals, lens, r_k, info = ops.rle_local(codes, sd.count, _MAX_RUN)
+        runs.append((vals, lens))
+        infos.append(tuple(int(v) for v in info))
+        recs_all.append((recs, n_out))
+    keep, grp, emitted = D.plan_rle_stitch(infos, _MAX_RUN)
+    ev, el = [], []
+    for k in range(len(slabs)):
+        if emitted[k]:
+            v, ln = ops.rle_emit(runs[k][0], runs[k][1], keep[k][0], keep[k][1], grp[k], _MAX_RUN)
+            ev.append(_host(v)[: 4 * emitted[k]].view(np.uint32))
+            el.append(_host(ln)[: 4 * emitted[k]].view(np.uint32))
+    V = np.concatenate(ev) if ev else np.empty(0, np.uint32)
+    Lr = np.concatenate(el) if el else np.empty(0, np.uint32)
+    R = len(V)
+    if chosen is Workflow.RLE:
+        meta.update(workflow="RLE", total_bits=0, n_runs=R)
+        lay = D.archive_layout(meta)
+        blob = _start_blob(meta, lay, None)
+        blob[lay["vals_off"]: lay["vals_off"] + 4 * R] = V.view(np.uint8)
+    else:
+        vh = np.bincount(V.astype(np.int64), minlength=cap)[:cap].astype(np.int64)
+        lengths, words, maxlen, vbits = ops.codebook(ops.to_tensor(vh), cap)
+        meta.update(workflow="RLE_VLE", total_bits=vbits, n_runs=R)
+        lay = D.archive_layout(meta)
+        blob = _start_blob(meta, lay, _lens_u8(lengths))
+        data = blob[lay["data_off"]: lay["data_off"] + lay["nbytes"]]
+        lens_host = _lens_u8(lengths)[:cap].astype(np.int64)
+        piece = max(1, block_bytes // 8)
+        pos = 0
+        for a in range(0, R, piece):  # the run values, in pieces at their bit phases
+            pv = V[a: a + piece]
+            nb = int(lens_host[pv].sum())
+            if nb:
+                sl = _host(ops.encode_at(up(pv.view(np.int32)) if up.device is not None else pv, len(pv),
+                                         lengths, words, cap, maxlen, pos % 8, nb, sym_bytes=4))
+                s = pos // 8
+                end = min(lay["nbytes"], s + len(sl))
+                data[s:end] |= sl[: end - s]
+            pos += nb
+        assert pos == vbits
+    blob[lay["lens_off"]: lay["lens_off"] + 4 * R] = Lr.view(np.uint8)
+    for k, (lo, _) in enumerate(slabs):
+        put_records(blob, lay, k, lo, *recs_all[k])
+    return blob.tobytes()
+
+
+def _start_blob(meta: dict, lay: dict, lengths: np.ndarray | None) -> np.ndarray:
+    blob = np.zeros(lay["total"], np.uint8)
+    hdr = D.archive_header(meta, lay)
+    blob[: len(hdr)] = np.frombuffer(hdr, np.uint8)
+    if lay["cb_len"]:
+        blob[lay["cb_off"]: lay["cb_off"] + meta["cap"]] = lengths[: meta["cap"]]
+    pre = D.archive_prefix(meta, lay)
+    blob[lay["sym_off"]: lay["sym_off"] + len(pre)] = np.frombuffer(pre, np.uint8)
+    return blob
+
+
+def decompress_blocks(archive, out: np.ndarray | None = None, block_bytes: int = _DEFAULT_BLOCK,
+                      ops=None) -> np.ndarray:
+    """The field of an archive, decoded slab by slab into host memory (``out``,
+    or a new array); same values as ``decompress``."""
+    import torch
+
+    from .pipeline import Workflow, code_bytes_for, parse_header
+
+    raw = bytes(archive) if not isinstance(archive, (bytes, bytearray)) else archive
+    hdr = parse_header(raw)
+    dims, chunk, cap = hdr.dims, hdr.chunk, hdr.cap
+    if ops is None:
+        ops = D.DeviceSlabOps(torch.device("cuda", torch.cuda.current_device()))
+    dev = getattr(ops, "device", None)
+    arc = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev) if dev is not None else raw
+    dt = np.float32 if hdr.dtype == "f32" else np.float64
+    if out is None:
+        out = np.empty(dims.count, dt)
+    out = out.reshape(-1)
+    if out.size != dims.count or out.dtype != dt:
+        raise DataError("output array does not match the archive's grid / dtype")
+    eb_abs = hdr.eb_abs
+    plane = _plane(dims)
+    itemsize = np.dtype(dt).itemsize
+    slabs = _slabs(dims, chunk, dims.count * itemsize, block_bytes)
+    dtype_code = 0 if dt == np.float32 else 1
+    cb = code_bytes_for(cap)
+
+    huff = hdr.workflow is Workflow.HUFFMAN
+    if huff:
+        bit_len, count, maxlen = ops.stream_info(arc, hdr)
+        nr = max(1, math.ceil(count * cb / max(1, block_bytes // 2)))
+        ranges = D.stream_ranges(bit_len, nr)
+        maps = []
+        for lo, hi in ranges:
+            if hi > lo:
+                fm = ops.range_maps(arc, hdr, bit_len, lo, hi, maxlen)
+            else:
+                fm = np.arange(maxlen, dtype=np.int64)
+            maps.append(np.asarray(fm.cpu() if hasattr(fm, "cpu") else fm, np.int64).reshape(-1))
+        chain = D.chain_ranges(maps, ranges, count)
+        cache: dict[int, object] = {}
+
+        def symbols(a: int, b: int):
+            """Symbols [a, b) of the stream from the ranges that hold them."""
+            parts = []
+            for k, (e, x, first, n) in enumerate(chain):
+                if n == 0 or first + n <= a or first >= b:
+                    continue
+                if k not in cache:
+                    cache.clear()  # ranges are visited in order: keep the last one only
+                    lo, hi = ranges[k]
+                    # the range decode runs on the tables its range-map call
+                    # left in the shared scratch (lzb.h): rebuild them first
+                    ops.range_maps(arc, hdr, bit_len, lo, hi, maxlen)
+                    cache[k] = ops.range_decode(arc, hdr, bit_len, lo, hi, maxlen, e, x, n)
+                    _check_decode(ops)
+                s = cache[k]
+                i0, i1 = max(a, first) - first, min(b, first + n) - first
+                parts.append(s[i0 * cb: i1 * cb] if dev is not None else np.asarray(s)[i0:i1])
+            if dev is not None:  # a fresh (aligned) tensor either way
+                return torch.cat(parts) if len(parts) > 1 else parts[0].clone()
+            return np.concatenate(parts) if len(parts) > 1 else parts[0]
+
+    for lo, hi in slabs:
+        sd = D.slab_dims(dims, lo, hi)
+        a, b = D.slab_index_offset(dims, lo), D.slab_index_offset(dims, hi)
+        codes = symbols(a, b) if huff else ops.rle_slab_codes(arc, hdr, a, b)
+        recs, n_out = ops.slab_records(arc, hdr, a, b)
+        y = ops.reconstruct(codes, sd, chunk, eb_abs, cap, recs, n_out, dtype_code)
+        out[lo * plane: hi * plane] = y.cpu().numpy() if hasattr(y, "cpu") else np.asarray(y).reshape(-1)
+    return out

@@ -392,3 +392,31 @@ def test_fast_prequant_exhaustive_f32(cuda):
         N.check_rc(L.lzb_prequant_verify(eb, 12345, 1 << 28, 1, st.data_ptr(), N.stream_ptr()), "verify")
         (s,) = N.read_status(st)
         assert s.u[0] == 0, (eb, "f64", s.u[0])
+
+
+@pytest.mark.parametrize("shape", [(24, 40, 64), (100, 70), (30000,)])
+def test_reconstruct_unaligned_code_stream(cuda, shape):
+    """K6's register paths load full chunks with 16-byte vectors only from an
+    aligned code stream; a stream at an odd 2-byte offset takes the scalar
+    loads and gives the same values."""
+    import torch
+
+    import paper_2105_12912_b200 as lzb
+    from helpers import smooth
+    from paper_2105_12912_b200 import ChunkSpec
+    from paper_2105_12912_b200 import distributed as D
+
+    vals = smooth(shape).astype(np.float32)
+    f = lzb.Field.from_array(vals)
+    d = f.dims
+    chunk = ChunkSpec.default_for(d.ndim)
+    ops = D.DeviceSlabOps(torch.device("cuda"))
+    x = torch.from_numpy(vals.reshape(-1)).cuda()
+    eb_abs = 1e-4 * float(vals.max() - vals.min())
+    codes, _, n_out, recs = ops.quantize(x, d, chunk, eb_abs, 1024)
+    buf = torch.zeros(codes.numel() + 2, dtype=torch.uint8, device="cuda")
+    buf[2:].copy_(codes)
+    rec = ops.local_records(recs, n_out, 0) if n_out else None
+    y0 = ops.reconstruct(codes, d, chunk, eb_abs, 1024, rec, n_out, 0)
+    y1 = ops.reconstruct(buf[2:], d, chunk, eb_abs, 1024, rec, n_out, 0)
+    assert torch.equal(y0, y1)
