@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kR3Threads, TMA ? 3 : 3)
                 vmin = mmv[0];
                 vmax = mmv[1];
             } else {
-                const bool tma = TMA && __any_sync(f3::kFull, cur.full);
+                const bool tma = TMA && p.codes_vec && __any_sync(f3::kFull, cur.full);  // = r3_chunk's fast
                 uint32_t yb = 0;
                 if (tma) {
                     yb = ybase_s + (nb & 1u) * 2048;

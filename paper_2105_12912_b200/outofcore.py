@@ -68,17 +68,28 @@ def _slabs(dims: Dims, chunk: ChunkSpec, field_bytes: int, block_bytes: int):
 
 
 class _Dev:
-    """Host block -> what the ops take (a device tensor, or the array itself)."""
+    """Host block -> what the ops take: a device tensor (staged through one
+    reusable pinned buffer, so a read-only memory map is never wrapped and the
+    copy runs at DMA speed), or the array itself for host ops."""
 
     def __init__(self, ops):
         self.device = getattr(ops, "device", None)
+        self._pin = None
 
     def __call__(self, a: np.ndarray):
         if self.device is None:
             return np.ascontiguousarray(a)
         import torch
 
-        return torch.from_numpy(np.ascontiguousarray(a)).to(self.device, non_blocking=False)
+        a = np.asarray(a).reshape(-1)
+        if self._pin is None or self._pin.numel() < a.nbytes:
+            self._pin = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+        host = self._pin[: a.nbytes]
+        host.numpy().view(a.dtype)[:] = a
+        dev = host.to(self.device, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()  # the stage is reused by the next block
+        return dev.view(torch.float32 if a.dtype == np.float32 else
+                        torch.float64 if a.dtype == np.float64 else torch.int32)
 
 
 def _check_decode(ops) -> None:

@@ -108,3 +108,25 @@ def test_analyze_matches_reference_csv(golden, cuda, tmp_path, capsys):
     capsys.readouterr()
     assert _run(["analyze", "-d", dims, "-t", "f32", "-e", f"rel:{eb}", "--dmax", "10", str(src)]) == 0
     assert capsys.readouterr().out.startswith("stage,kind,distance,variance")
+
+
+def test_out_of_core_blocks_match_whole_field(cuda, tmp_path, capsys):
+    """--block-mb: the raw file is memory-mapped and pushed through the GPU in
+    slabs; the archive equals the whole-field one and decodes to the same file."""
+    from helpers import smooth
+
+    data = smooth((24, 96, 128)).astype(np.float32)  # 1.2 MB -> three slabs of <= 0.5 MB... 1 MB
+    path = tmp_path / "f.f32"
+    path.write_bytes(data.tobytes())
+    whole, blocks = tmp_path / "w.lz", tmp_path / "b.lz"
+    dims = "128,96,24"
+    assert _run(["compress", "-d", dims, "-t", "f32", "-e", "rel:1e-4", str(path), str(whole)]) == 0
+    assert _run(["compress", "-d", dims, "-t", "f32", "-e", "rel:1e-4", "--block-mb", "1", str(path),
+                 str(blocks)]) == 0
+    line = capsys.readouterr().out.strip().splitlines()[-1]
+    assert line.startswith("workflow=HUFFMAN") and "max_abs_err=" in line
+    assert blocks.read_bytes() == whole.read_bytes()
+    y0, y1 = tmp_path / "y0.f32", tmp_path / "y1.f32"
+    assert _run(["decompress", str(whole), str(y0)]) == 0
+    assert _run(["decompress", "--block-mb", "1", str(whole), str(y1)]) == 0
+    assert y0.read_bytes() == y1.read_bytes()
