@@ -684,6 +684,22 @@ def run_gpu(args, cfg, rank, world, local_rank):
         y, hdr, _, _ = lzb.decompress_device(arc, prof=prof, out=out)
         return arc, y
 
+    # field construction (reported separately): the device range
+    # pass behind Field.from_array (lzb_field_range: min / max + first non-finite)
+    fc = []
+    for k in range(args.warmup + args.steps):
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        lzb.Field.from_array(x.reshape(shape))
+        f1.record()
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            fc.append(f0.elapsed_time(f1) / 1e3)
+    t_fc = statistics.mean(fc)
+    field_construction = {"ms": round(t_fc * 1e3, 3), "gbs": round(nbytes / t_fc / 1e9, 1),
+                          "what": "Field.from_array of the device field: lzb_field_range "
+                                  "(min / max / first non-finite), outside the step"}
+
     ybuf = torch.empty(n, dtype=x.dtype, device=dev)
     for _ in range(args.warmup):
         arc, y = step(out=ybuf)
@@ -913,6 +929,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "bound_ok": bool(bound_ok), "max_abs_err": err, "eb_abs": hdr.eb_abs,
         "gpu_launches": launches_per_step(hdr) * args.steps,
         "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
+        "field_construction": field_construction,
     }
     print(json.dumps(line), flush=True)
 
