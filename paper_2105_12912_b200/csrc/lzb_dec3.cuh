@@ -79,18 +79,23 @@ __device__ __forceinline__ void d3_stage_wait() {
     __syncwarp();
 }
 
-// Bit window over a staged subsequence (raw big-endian stream words).
+// Bit window over a staged subsequence (raw big-endian stream words), read
+// through 32-bit shared addresses (lds32): a generic pointer made the
+// compiler rebuild the shared window base (S2UR + ULEA) at every refill.
 struct SWin {
-    const uint32_t *s;
-    uint32_t i, sh;      // word of w0, bit offset inside w0
+    uint32_t base;       // shared address of the stage
+    uint32_t ad;         // shared address of the word after w2
+    uint32_t sh;         // bit offset inside w0
     uint32_t w0, w1, w2;
-    __device__ __forceinline__ void init(const uint32_t *st, uint32_t a) {  // a: stage bit
-        s = st;
-        i = a >> 5;
+    __device__ __forceinline__ void init(const uint32_t *st, uint32_t a) { init_s(smem_addr(st), a); }
+    __device__ __forceinline__ void init_s(uint32_t b, uint32_t a) {  // a: stage bit
+        base = b;
+        const uint32_t wa = b + ((a >> 5) << 2);
         sh = a & 31;
-        w0 = bswap32(s[i]);
-        w1 = bswap32(s[i + 1]);
-        w2 = bswap32(s[i + 2]);
+        w0 = bswap32(lds32(wa));
+        w1 = bswap32(lds32(wa + 4));
+        w2 = bswap32(lds32(wa + 8));
+        ad = wa + 12;
     }
     __device__ __forceinline__ uint32_t peek12() const { return __funnelshift_l(w1, w0, sh) >> (32 - kLutBits); }
     __device__ __forceinline__ uint64_t peek64() const {
@@ -100,15 +105,15 @@ struct SWin {
         sh += L;
         if (sh >= 32) {
             sh -= 32;
-            i++;
             w0 = w1;
             w1 = w2;
-            w2 = bswap32(s[i + 2]);
+            w2 = bswap32(lds32(ad));
+            ad += 4;
         }
     }
     __device__ __forceinline__ void skip(uint32_t L) {  // any L <= 64
         if (L <= 32) consume(L);
-        else init(s, i * 32 + sh + L);
+        else init_s(base, (ad - 12 - base) * 8 + sh + L);
     }
 };
 
