@@ -605,12 +605,19 @@ __global__ void __launch_bounds__(kF9Warps * 32, 1) k_dec_final9(DecParams p, ui
                     n -= __popc(hs);
                     adv = hs ? (uint32_t)(__ffs(hs) - 1) : adv;
                 }
-                asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(lo));
-                if (n > 1) asm volatile("st.shared.u8 [%0+1], %1;" ::"r"(a), "r"(lo >> 8));
-                if (n > 2) asm volatile("st.shared.u8 [%0+2], %1;" ::"r"(a), "r"(lo >> 16));
-                if (n > 3) asm volatile("st.shared.u8 [%0+3], %1;" ::"r"(a), "r"(lo >> 24));
-                if (n > 4) asm volatile("st.shared.u8 [%0+4], %1;" ::"r"(a), "r"(hi));
-                if (n > 5) asm volatile("st.shared.u8 [%0+5], %1;" ::"r"(a), "r"(hi >> 8));
+                // predicated (not branched) byte stores: one per decoded symbol
+                asm volatile(
+                    "{\n\t.reg .pred q1, q2, q3, q4, q5;\n\t"
+                    "setp.gt.u32 q1, %3, 1;\n\tsetp.gt.u32 q2, %3, 2;\n\tsetp.gt.u32 q3, %3, 3;\n\t"
+                    "setp.gt.u32 q4, %3, 4;\n\tsetp.gt.u32 q5, %3, 5;\n\t"
+                    "st.shared.u8 [%0], %1;\n\t"
+                    "@q1 st.shared.u8 [%0+1], %4;\n\t"
+                    "@q2 st.shared.u8 [%0+2], %5;\n\t"
+                    "@q3 st.shared.u8 [%0+3], %6;\n\t"
+                    "@q4 st.shared.u8 [%0+4], %2;\n\t"
+                    "@q5 st.shared.u8 [%0+5], %7;\n\t}"
+                    ::"r"(a), "r"(lo), "r"(hi), "r"(n), "r"(lo >> 8), "r"(lo >> 16), "r"(lo >> 24), "r"(hi >> 8)
+                    : "memory");
                 a += n;
                 rel += adv;
                 r.skip(adv);
