@@ -599,8 +599,13 @@ __global__ void __launch_bounds__(kF9Warps * 32, 1) k_dec_final9(DecParams p, ui
                     } else {
                         lo = (uint32_t)d;
                     }
-                    n = 1;
-                } else if (mstop - rel < (uint32_t)kLutBits) {  // code words must start before mstop
+                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(lo) : "memory");
+                    a += 1;
+                    rel += adv;
+                    r.skip(adv);  // a long code word may exceed 32 bits
+                    continue;
+                }
+                if (mstop - rel < (uint32_t)kLutBits) {  // code words must start before mstop
                     const uint32_t hs = (uint32_t)s_st[pk] & (0xFFFu << (mstop - rel));
                     n -= __popc(hs);
                     adv = hs ? (uint32_t)(__ffs(hs) - 1) : adv;
@@ -620,7 +625,7 @@ __global__ void __launch_bounds__(kF9Warps * 32, 1) k_dec_final9(DecParams p, ui
                     : "memory");
                 a += n;
                 rel += adv;
-                r.skip(adv);
+                r.consume(adv);  // <= 12 bits from the LUT
             }
         }
         if (__any_sync(kD3Full, wide) && !__any_sync(kD3Full, bad)) {
