@@ -809,7 +809,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
         # The field upload of step k+2 and the result download of step k
         # share the host link in M chunk pairs: upload chunk j waits for
-        # download chunk j.  Unpaced, the upload takes ~48 of the ~92 GB/s
+        # download chunk j-1.  Unpaced, the upload takes ~48 of the ~92 GB/s
         # duplex and finishes early while the download -- the critical path
         # (the next decompress waits for ybuf) -- crawls at ~36 GB/s.
         M = 8
@@ -824,8 +824,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
                     up.wait_event(xfree[b])  # the compress that read this buffer is done
                 mark(up, k, "up0")
                 for j in range(M):
-                    if pace is not None:
-                        up.wait_event(pace[j])
+                    if pace is not None and j > 0:  # chunk 0 goes at once; then one behind the download
+                        up.wait_event(pace[j - 1])
                     xds[b][bounds[j]: bounds[j + 1]].copy_(xh[bounds[j]: bounds[j + 1]], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(up)
