@@ -106,7 +106,9 @@ int lzb_prequant_verify(double eb_abs, uint64_t lo, uint64_t count, int dtype, l
  * outlier gather, emitting the CHUNK-MAJOR symbol stream.
  * Replaces prequantize + construct_grid + gather_chunk_major + histogram
  * (P/quantize.py:90-213, P/pipeline.py:102-105, P/codebook.py:23-27).
- *   codes     : n symbols, chunk-major, width code_bytes
+ *   codes     : n symbols, chunk-major, width code_bytes (naturally aligned;
+ *               a 16-byte aligned buffer enables the register fast paths
+ *               for ChunkSpec 8x8x8 / 16x16 / 256, else the generic path)
  *   hist      : cap x u64, OVERWRITTEN with the stream histogram
  *   outliers  : out_capacity records of {u64 index, i64 delta}, sorted by
  *               global row-major index (the archive's outlier section)
@@ -287,7 +289,8 @@ int lzb_rle_decode(const uint8_t *values_le, const uint8_t *lengths_le, uint64_t
  * reconstruction + dequantization + range/finiteness.  Replaces
  * scatter_chunk_major + _decode_outliers validation + reconstruct_grid +
  * dequantize (P/pipeline.py:108-117, 306-315, P/reconstruct.py:22-88).
- *   codes    : chunk-major symbols
+ *   codes    : chunk-major symbols (naturally aligned; full chunks of a
+ *              16-byte aligned stream are read with vector loads)
  *   outliers : n_out 16-byte LE records {u64 index, i64 delta}, any alignment
  *   y        : n values (dtype) in grid (row-major) order
  * st->u[0]/u[1] = vmin/vmax (f64 bits), u[2] = first non-finite offset.
