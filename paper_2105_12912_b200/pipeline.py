@@ -24,6 +24,7 @@ no CPU fallback: without a CUDA device the compute entry points raise.
 from __future__ import annotations
 
 import math
+import os
 import struct
 from dataclasses import dataclass
 
@@ -158,8 +159,12 @@ def _dev(t):
     return t.data_ptr()
 
 
+_NVTX = bool(os.environ.get("LZB_NVTX"))  # named ranges per stage for nsys / ncu --nvtx
+
+
 class _Stage:
-    """CUDA-event bracket around one stage when profiling (bench.py); no-op otherwise."""
+    """CUDA-event bracket around one stage when profiling (bench.py), and an
+    NVTX range when LZB_NVTX is set; no-op otherwise."""
 
     __slots__ = ("prof", "name", "ev")
 
@@ -167,17 +172,24 @@ class _Stage:
         self.prof, self.name, self.ev = prof, name, None
 
     def __enter__(self):
-        if self.prof is not None:
+        if self.prof is not None or _NVTX:
             import torch
 
-            self.ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            self.ev[0].record()
+            if _NVTX:
+                torch.cuda.nvtx.range_push(f"lzb.{self.name}")
+            if self.prof is not None:
+                self.ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                self.ev[0].record()
         return self
 
     def __exit__(self, *exc):
         if self.prof is not None and exc[0] is None:
             self.ev[1].record()
             self.prof.append((self.name, self.ev[0], self.ev[1]))
+        if _NVTX:
+            import torch
+
+            torch.cuda.nvtx.range_pop()
         return False
 
 
