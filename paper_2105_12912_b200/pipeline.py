@@ -139,6 +139,7 @@ class _Pool:
 
     def __init__(self):
         self.bufs = {}
+        self.gen = 0  # bumped whenever a buffer is (re)allocated: invalidates cached launch plans
 
     def get(self, name: str, nbytes: int, device):
         import torch
@@ -149,6 +150,7 @@ class _Pool:
             self.bufs[(name, str(device))] = None
             t = torch.empty(nbytes, dtype=torch.uint8, device=device)
             self.bufs[(name, str(device))] = t
+            self.gen += 1
         return t
 
 
@@ -252,6 +254,48 @@ def compress_device(field: Field, eb: float, eb_mode: str = "rel", cap: int = 10
     return _compress_staged(field, eb, eb_mode, eb_abs, cap, workflow, chunk, select_mode, values, prof)
 
 
+class _SSPlan:
+    """Buffers and sizes of one single-sync compress shape, valid while the
+    pool generation is unchanged (small fields: the Python setup is a
+    measurable part of a call)."""
+
+    __slots__ = ("gen", "g", "codes", "hist", "lengths", "cwords", "st", "cb_scr", "cap_out", "outl", "qs",
+                 "q_scr", "sym_off", "worst", "big", "es", "e_scr")
+
+
+_SS_PLANS: dict = {}
+
+
+def _ss_plan(dims: Dims, chunk: ChunkSpec, cap: int, dev) -> _SSPlan:
+    sdev = str(dev)
+    key = (dims.as_tuple(), chunk.as_tuple(), cap, sdev, _pool.bufs.get(("outcap", sdev), 0))
+    pl = _SS_PLANS.get(key)
+    if pl is not None and pl.gen == _pool.gen:
+        return pl
+    L = N.lib()
+    n = dims.count
+    pl = _SSPlan()
+    pl.g = N.geom(dims.as_tuple(), chunk.as_tuple())
+    pl.codes = _pool.get("codes", n * 2, dev)
+    pl.hist = _pool.get("hist", cap * 8, dev)
+    pl.lengths = _pool.get("lengths", cap, dev)
+    pl.cwords = _pool.get("cwords", cap * 8, dev)
+    pl.st = _pool.get("status", 8 * N.STATUS_BYTES, dev)
+    pl.cb_scr = _pool.get("cb_scratch", L.lzb_codebook_scratch_bytes(cap), dev)
+    pl.cap_out = int(_pool.bufs.get(("outcap", sdev), 0) or min(n, n // 128 + 4096))
+    pl.outl = _pool.get("outliers", pl.cap_out * 16, dev)
+    pl.qs = L.lzb_quantize_scratch_bytes(pl.g, pl.cap_out)
+    pl.q_scr = _pool.get("q_scratch", pl.qs, dev)
+    pl.sym_off = _a8(_SECTION_BASE + cap)
+    pl.worst = pl.sym_off + 16 + 4 * n + 8 + 16 * pl.cap_out  # code words <= 32 bits on this path
+    pl.big = _pool.get("arc_stage", pl.worst, dev)
+    pl.es = L.lzb_huff_encode_scratch_bytes(n)
+    pl.e_scr = _pool.get("e_scratch", pl.es, dev)
+    pl.gen = _pool.gen
+    _SS_PLANS[key] = pl
+    return pl
+
+
 def _compress_single_sync(field: Field, eb, eb_mode, eb_abs, cap, chosen, chunk, values, prof):
     """K1, K2, K3 and lzb_archive_finalize_huff back to back; one read-back.
     Returns None when the staged path must run instead."""
@@ -262,23 +306,11 @@ def _compress_single_sync(field: Field, eb, eb_mode, eb_abs, cap, chosen, chunk,
     dev = x.device
     L = N.lib()
     sp = N.stream_ptr()
-    g = N.geom(dims.as_tuple(), chunk.as_tuple())
-    codes = _pool.get("codes", n * 2, dev)
-    hist = _pool.get("hist", cap * 8, dev)
-    lengths = _pool.get("lengths", cap, dev)
-    cwords = _pool.get("cwords", cap * 8, dev)
-    st = _pool.get("status", 8 * N.STATUS_BYTES, dev)
+    pl = _ss_plan(dims, chunk, cap, dev)
+    g, codes, hist, lengths, cwords, st = pl.g, pl.codes, pl.hist, pl.lengths, pl.cwords, pl.st
     stp = _dev(st)
-    cb_scr = _pool.get("cb_scratch", L.lzb_codebook_scratch_bytes(cap), dev)
-    cap_out = int(_pool.bufs.get(("outcap", str(dev)), 0) or min(n, n // 128 + 4096))
-    outl = _pool.get("outliers", cap_out * 16, dev)
-    qs = L.lzb_quantize_scratch_bytes(g, cap_out)
-    q_scr = _pool.get("q_scratch", qs, dev)
-    sym_off = _a8(_SECTION_BASE + cap)
-    worst = sym_off + 16 + 4 * n + 8 + 16 * cap_out  # code words <= 32 bits on this path
-    big = _pool.get("arc_stage", worst, dev)
-    es = L.lzb_huff_encode_scratch_bytes(n)
-    e_scr = _pool.get("e_scratch", es, dev)
+    cb_scr, cap_out, outl, qs, q_scr = pl.cb_scr, pl.cap_out, pl.outl, pl.qs, pl.q_scr
+    sym_off, worst, big, es, e_scr = pl.sym_off, pl.worst, pl.big, pl.es, pl.e_scr
     with _Stage(prof, "K1_quantize"):
         N.check_rc(L.lzb_quantize(_dev(x), _DTYPE_CODES[dt], g, eb_abs, cap, _dev(codes), 2, _dev(hist),
                                   _dev(outl), cap_out, stp, _dev(q_scr), qs, sp), "quantize")
