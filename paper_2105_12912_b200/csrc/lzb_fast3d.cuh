@@ -56,6 +56,23 @@ __device__ __forceinline__ int32_t pq_fast_f32(float x, float inv_hi, float inv_
     return __float_as_int(t) - 0x4B400000;  // integer value of k
 }
 
+// The same with the magnitude guard folded into a running maximum: the
+// caller tests |ph|max < 2^22 once for all its elements (one FMNMX per
+// element instead of a compare and a predicate merge).  NaN / inf inputs
+// still fail the tie test (f is NaN), so `ok` keeps its meaning.
+__device__ __forceinline__ int32_t pq_fast_f32m(float x, float inv_hi, float inv_lo, bool &ok, float &amax) {
+    const float M = 12582912.0f;  // 1.5 * 2^23
+    float ph = __fmul_rn(x, inv_hi);
+    float pe = __fmaf_rn(x, inv_hi, -ph);
+    float pl = __fmaf_rn(x, inv_lo, pe);
+    float t = __fadd_rn(ph, M);
+    float k = __fsub_rn(t, M);
+    float f = __fadd_rn(__fsub_rn(ph, k), pl);
+    ok = ok && (fabsf(f) < 0.4999847412109375f);
+    amax = fmaxf(amax, fabsf(ph));
+    return __float_as_int(t) - 0x4B400000;
+}
+
 // exact reference prequantization; flags: 1 overflow, 2 assert
 __device__ __forceinline__ int64_t pq_exact(double v, double two_eb, double slack, int &flags) {
     double s = __ddiv_rn(v, two_eb);

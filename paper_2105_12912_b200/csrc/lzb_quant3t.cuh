@@ -190,11 +190,13 @@ __global__ void __launch_bounds__(kT1Threads, 1)
             }
             int32_t d0[8], d1[8];
             bool ok = true;
+            float amax = 0.0f;
 #pragma unroll
             for (int j = 0; j < 8; j++) {
-                d0[j] = f3::pq_fast_f32(x0[j], p.inv_hi, p.inv_lo, ok);
-                d1[j] = f3::pq_fast_f32(x1[j], p.inv_hi, p.inv_lo, ok);
+                d0[j] = f3::pq_fast_f32m(x0[j], p.inv_hi, p.inv_lo, ok, amax);
+                d1[j] = f3::pq_fast_f32m(x1[j], p.inv_hi, p.inv_lo, ok, amax);
             }
+            ok = ok && amax < 4194304.0f;
             if (!__all_sync(f3::kFull, ok)) {
                 // rare: an element near a rounding tie (exact f64 division for
                 // it), or values beyond the int32 fast path (exact chunk path)
