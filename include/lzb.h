@@ -123,6 +123,15 @@ int lzb_quantize(const void *x, int dtype, const lzb_geom *g, double eb_abs, uin
                  uint64_t out_capacity, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
                  void *stream);
 
+/* lzb_quantize that also records `hist_event` (a cudaEvent_t; may be NULL)
+ * on the stream as soon as `hist` is final -- before the outlier compaction
+ * and ordering launches -- so the code book (K2) can be built on a second
+ * stream while they run. */
+int lzb_quantize_ev(const void *x, int dtype, const lzb_geom *g, double eb_abs, uint32_t cap,
+                    void *codes, int code_bytes, uint64_t *hist, uint64_t *outliers,
+                    uint64_t out_capacity, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
+                    void *stream, void *hist_event);
+
 /* ---------------------------------------------------------------------
  * Histogram of a symbol stream (P/codebook.py:23-27).  hist (cap x u64) is
  * overwritten.  code = LZB_E_DATA if a symbol >= cap (u[0] = that symbol).

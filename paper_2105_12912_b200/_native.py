@@ -44,6 +44,7 @@ SIGNATURES = {
     "lzb_prequant_verify": (_I, [_D, _U64, _U64, _I, _P, _P]),
     "lzb_quantize_scratch_bytes": (_SZ, [_GP, _U64]),
     "lzb_quantize": (_I, [_P, _I, _GP, _D, _U32, _P, _I, _P, _P, _U64, _P, _P, _SZ, _P]),
+    "lzb_quantize_ev": (_I, [_P, _I, _GP, _D, _U32, _P, _I, _P, _P, _U64, _P, _P, _SZ, _P, _P]),
     "lzb_histogram": (_I, [_P, _I, _U64, _U32, _P, _P, _P]),
     "lzb_codebook_scratch_bytes": (_SZ, [_U32]),
     "lzb_codebook": (_I, [_P, _U32, _P, _P, _P, _P, _SZ, _P]),

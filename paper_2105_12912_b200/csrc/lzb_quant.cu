@@ -635,10 +635,31 @@ extern "C" size_t lzb_quantize_scratch_bytes(const lzb_geom *g, uint64_t out_cap
     return s.bytes();
 }
 
+static int quantize_impl(const void *x, int dtype, const lzb_geom *gg, double eb_abs, uint32_t cap, void *codes,
+                         int code_bytes, uint64_t *hist, uint64_t *outliers, uint64_t out_capacity,
+                         lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream,
+                         cudaEvent_t hist_ev);
+
 extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double eb_abs,
                             uint32_t cap, void *codes, int code_bytes, uint64_t *hist,
                             uint64_t *outliers, uint64_t out_capacity, lzb_dstatus *st,
                             void *scratch, size_t scratch_bytes, void *stream) {
+    return quantize_impl(x, dtype, gg, eb_abs, cap, codes, code_bytes, hist, outliers, out_capacity, st, scratch,
+                         scratch_bytes, stream, nullptr);
+}
+
+extern "C" int lzb_quantize_ev(const void *x, int dtype, const lzb_geom *gg, double eb_abs, uint32_t cap,
+                               void *codes, int code_bytes, uint64_t *hist, uint64_t *outliers,
+                               uint64_t out_capacity, lzb_dstatus *st, void *scratch, size_t scratch_bytes,
+                               void *stream, void *hist_event) {
+    return quantize_impl(x, dtype, gg, eb_abs, cap, codes, code_bytes, hist, outliers, out_capacity, st, scratch,
+                         scratch_bytes, stream, static_cast<cudaEvent_t>(hist_event));
+}
+
+static int quantize_impl(const void *x, int dtype, const lzb_geom *gg, double eb_abs, uint32_t cap, void *codes,
+                         int code_bytes, uint64_t *hist, uint64_t *outliers, uint64_t out_capacity,
+                         lzb_dstatus *st, void *scratch, size_t scratch_bytes, void *stream,
+                         cudaEvent_t hist_ev) {
     if (!gg || !x || !codes || !hist || !st || dtype < 0 || dtype > 2) return LZB_E_ARG;
     if (code_bytes != 2 && code_bytes != 4) return LZB_E_ARG;
     if (cap < 4 || (cap & (cap - 1)) || (code_bytes == 2 && cap > 65536)) return LZB_E_ARG;
@@ -797,6 +818,7 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
         else
             rc = code_bytes == 2 ? launch(k_quantize3d8<double, uint16_t>) : launch(k_quantize3d8<double, uint32_t>);
         if (rc) return rc;
+        if (hist_ev) LZB_CUDA_TRY(cudaEventRecord(hist_ev, s));  // the histogram is final
         // phase 2: tile offsets, slot compaction, overflow re-emission
         const int sms = device_sms();
         k_q3_scan<<<(unsigned)umin64((q3.ntiles + 2047) / 2048, (uint64_t)sms * 4), 256, 0, s>>>(
@@ -851,6 +873,7 @@ extern "C" int lzb_quantize(const void *x, int dtype, const lzb_geom *gg, double
                                  : launch_quant<double, uint32_t, false>(qp, s);
     }
     if (rc) return rc;
+    if (hist_ev) LZB_CUDA_TRY(cudaEventRecord(hist_ev, s));  // the histogram is final
 order:
     if (!outliers || out_capacity == 0) return LZB_OK;
 

@@ -296,6 +296,25 @@ def _ss_plan(dims: Dims, chunk: ChunkSpec, cap: int, dev) -> _SSPlan:
     return pl
 
 
+_SIDE: dict = {}
+
+
+def _side_stream(dev):
+    """(second stream, histogram-final event, code-book-done event) per device:
+    K2 runs beside K1's outlier compaction / ordering launches."""
+    import torch
+
+    key = str(dev)
+    v = _SIDE.get(key)
+    if v is None:
+        side = torch.cuda.Stream(device=dev)
+        ev_hist, ev_book = torch.cuda.Event(), torch.cuda.Event()
+        ev_hist.record()  # create the handles (torch events are created lazily)
+        ev_book.record()
+        v = _SIDE[key] = (side, ev_hist, ev_book)
+    return v
+
+
 def _compress_single_sync(field: Field, eb, eb_mode, eb_abs, cap, chosen, chunk, values, prof):
     """K1, K2, K3 and lzb_archive_finalize_huff back to back; one read-back.
     Returns None when the staged path must run instead."""
@@ -311,12 +330,25 @@ def _compress_single_sync(field: Field, eb, eb_mode, eb_abs, cap, chosen, chunk,
     stp = _dev(st)
     cb_scr, cap_out, outl, qs, q_scr = pl.cb_scr, pl.cap_out, pl.outl, pl.qs, pl.q_scr
     sym_off, worst, big, es, e_scr = pl.sym_off, pl.worst, pl.big, pl.es, pl.e_scr
-    with _Stage(prof, "K1_quantize"):
-        N.check_rc(L.lzb_quantize(_dev(x), _DTYPE_CODES[dt], g, eb_abs, cap, _dev(codes), 2, _dev(hist),
-                                  _dev(outl), cap_out, stp, _dev(q_scr), qs, sp), "quantize")
-    with _Stage(prof, "K2_codebook"):
+    if prof is None:  # K2 on a second stream as soon as the histogram is final
+        import torch
+
+        side, ev_hist, ev_book = _side_stream(dev)
+        N.check_rc(L.lzb_quantize_ev(_dev(x), _DTYPE_CODES[dt], g, eb_abs, cap, _dev(codes), 2, _dev(hist),
+                                     _dev(outl), cap_out, stp, _dev(q_scr), qs, sp, ev_hist.cuda_event),
+                   "quantize")
+        side.wait_event(ev_hist)
         N.check_rc(L.lzb_codebook(_dev(hist), cap, _dev(lengths), _dev(cwords), stp + N.STATUS_BYTES,
-                                  _dev(cb_scr), cb_scr.numel(), sp), "codebook")
+                                  _dev(cb_scr), cb_scr.numel(), side.cuda_stream), "codebook")
+        ev_book.record(side)
+        torch.cuda.current_stream(dev).wait_event(ev_book)
+    else:  # stage timing: one stream
+        with _Stage(prof, "K1_quantize"):
+            N.check_rc(L.lzb_quantize(_dev(x), _DTYPE_CODES[dt], g, eb_abs, cap, _dev(codes), 2, _dev(hist),
+                                      _dev(outl), cap_out, stp, _dev(q_scr), qs, sp), "quantize")
+        with _Stage(prof, "K2_codebook"):
+            N.check_rc(L.lzb_codebook(_dev(hist), cap, _dev(lengths), _dev(cwords), stp + N.STATUS_BYTES,
+                                      _dev(cb_scr), cb_scr.numel(), sp), "codebook")
     with _Stage(prof, "K3_huff_encode"):
         N.check_rc(L.lzb_huff_encode(_dev(codes), 2, n, _dev(lengths), _dev(cwords), cap, N.LZB_MAXLEN_DEVICE,
                                      _dev(big) + sym_off + 16, worst - sym_off - 16, stp + 2 * N.STATUS_BYTES,
