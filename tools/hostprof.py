@@ -20,7 +20,11 @@ ybuf = torch.empty_like(x)
 for _ in range(10):
     lzb.decompress_device(lzb.compress_device(field, cfg["eb"]), out=ybuf)
 torch.cuda.synchronize()
-for what, fn in (("compress", lambda: lzb.compress_device(field, cfg["eb"])),):
+arc0 = lzb.compress_device(field, cfg["eb"])
+which = sys.argv[3] if len(sys.argv) > 3 else "compress"
+calls = {"compress": lambda: lzb.compress_device(field, cfg["eb"]),
+         "decompress": lambda: lzb.decompress_device(arc0, out=ybuf)}
+for what, fn in ((which, calls[which]),):
     t = time.perf_counter()
     for _ in range(reps):
         fn()
