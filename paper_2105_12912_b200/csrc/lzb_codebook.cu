@@ -80,6 +80,57 @@ __device__ void bitonic_sort_u64(uint64_t *a, uint32_t n) {  // n power of two, 
     }
 }
 
+// Ascending sort of np (a power of two) keys a[0..np) with one CTA: 32-key
+// runs sorted in registers per warp (bitonic over shuffles), then
+// log2(np/32) merge levels where every key finds its place by a binary
+// search in the partner run (ties -- the ~0 padding -- resolved left run
+// first, so every slot is written once).  Ping-pongs between
+// a and b; returns the buffer holding the result.  About a dozen block
+// barriers instead of the bitonic network's 55.
+__device__ uint64_t *sort_u64_merge(uint64_t *a, uint64_t *b, uint32_t np, uint32_t nbuf) {
+    const uint32_t lane = threadIdx.x & 31u;
+    for (uint32_t i0 = threadIdx.x & ~31u; i0 < np; i0 += blockDim.x) {
+        const uint32_t i = i0 + lane;
+        uint64_t v = i < nbuf ? a[i] : ~0ull;
+#pragma unroll
+        for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                const uint64_t o = __shfl_xor_sync(0xffffffffu, v, j);
+                const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+                v = keep_min ? (v < o ? v : o) : (v < o ? o : v);
+            }
+        }
+        if (i < np) a[i] = v;
+    }
+    __syncthreads();
+    for (uint32_t run = 32; run < np; run <<= 1) {
+        for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+            const uint64_t v = a[i];
+            const uint32_t r = i / run, pos = i - r * run;
+            const uint32_t pb = (r ^ 1u) * run;  // partner run
+            const bool left = (r & 1u) == 0;
+            uint32_t lo = 0, cnt = run;
+            while (cnt > 0) {  // partner keys before v: below it (left run) / not above it (right run)
+                const uint32_t half = cnt >> 1;
+                const uint64_t x = a[pb + lo + half];
+                if (left ? x < v : x <= v) {
+                    lo += half + 1;
+                    cnt -= half + 1;
+                } else {
+                    cnt = half;
+                }
+            }
+            b[(r & ~1u) * run + pos + lo] = v;
+        }
+        __syncthreads();
+        uint64_t *t = a;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
 // Canonical code words from lengths (P/codebook.py:179-190) + Kraft check
 // (P/codebook.py:125-140).  Block-wide; returns a LZB code (0 ok).
 __device__ int canonical_from_lengths(const uint8_t *lengths, uint32_t cap, uint64_t *codes,
@@ -303,7 +354,16 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
     {  // keys past n are ~0: sorting the power-of-two prefix covering n suffices
         uint32_t np = 1;
         while (np < n) np <<= 1;
-        bitonic_sort_u64(sc.key, np);
+        if (kSmem && np <= cap) {
+            // merge sort ping-ponging with wint (cap x u64, unused until the merge)
+            uint64_t *sorted = sort_u64_merge(sc.key, sc.wint, np, npow2);
+            if (sorted != sc.key) {  // equal-sized arrays: swap the roles
+                sc.wint = sc.key;
+                sc.key = sorted;
+            }
+        } else {
+            bitonic_sort_u64(sc.key, np);
+        }
     }
     if (threadIdx.x == 0) s_clk[0] = clock64() - t0;
     if (n == 1) {
