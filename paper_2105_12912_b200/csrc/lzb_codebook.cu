@@ -314,6 +314,12 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
         sc.parent = reinterpret_cast<uint32_t *>(sc.wint + cap);
         sc.depth = reinterpret_cast<uint8_t *>(sc.parent + 2 * cap);
     }
+    // code lengths: a shared copy for the small-book instantiation (the
+    // canonical pass and the stats read them back), copied out once at the end
+    uint8_t *len = lengths;
+    if constexpr (kSmem)
+        len = reinterpret_cast<uint8_t *>(reinterpret_cast<uint32_t *>(sc.depth + 2 * cap + 16 - ((2 * cap) & 15)) +
+                                          cap + 16);
     __shared__ uint32_t s_n;
     __shared__ uint32_t s_cnt[65];
     __shared__ uint64_t s_first[66];
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
     for (uint32_t s0 = 0; s0 < cap; s0 += blockDim.x) {  // warp-aggregated compaction
         const uint32_t s = s0 + threadIdx.x;
         const uint64_t f = s < cap ? hist[s] : 0ull;
-        if (s < cap) lengths[s] = 0;
+        if (s < cap) len[s] = 0;
         if (f >= (1ull << 44)) s_err = 1;
         unsigned long long fs = f;
 #pragma unroll
@@ -367,7 +373,7 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
     }
     if (threadIdx.x == 0) s_clk[0] = clock64() - t0;
     if (n == 1) {
-        if (threadIdx.x == 0) lengths[sc.key[0] & 0xFFFFF] = 1;  // lone symbol -> 1 bit
+        if (threadIdx.x == 0) len[sc.key[0] & 0xFFFFF] = 1;  // lone symbol -> 1 bit
     } else {
         // two-queue Huffman merge (sequential; n-1 steps) on thread 0; see
         // huffman_merge32 / huffman_merge for the register windows that keep
@@ -440,7 +446,7 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
                 s_err = 1;
                 d = 64;
             }
-            lengths[sc.key[i] & 0xFFFFF] = (uint8_t)d;
+            len[sc.key[i] & 0xFFFFF] = (uint8_t)d;
         }
     }
     __syncthreads();
@@ -449,7 +455,10 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
         return;
     }
     if (threadIdx.x == 0) s_clk[2] = clock64() - t0;
-    int rc = canonical_from_lengths(lengths, cap, codes, s_cnt, s_first, s_misc, false);
+    if constexpr (kSmem) {
+        for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) lengths[i] = len[i];
+    }
+    int rc = canonical_from_lengths(len, cap, codes, s_cnt, s_first, s_misc, false);
     if (rc) {
         if (threadIdx.x == 0) set_status(st, LZB_E_DATA);
         return;
@@ -458,7 +467,7 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const unsigned long lon
     unsigned long long sum = 0;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {  // the n used symbols, from the sorted keys
         const uint64_t k = sc.key[i];
-        sum += (k >> 20) * lengths[k & 0xFFFFF];
+        sum += (k >> 20) * len[k & 0xFFFFF];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);  // warp sums first
@@ -547,8 +556,8 @@ extern "C" int lzb_codebook(const uint64_t *hist, uint32_t cap, uint8_t *lengths
     c.depth = sc.take<uint8_t>(2 * cap);
     if (!c.depth) return LZB_E_ARG;
     LZB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(lzb_dstatus), s));
-    // key | wint | parent | depth | (16-aligned) u32 leaf weights for the merge window
-    size_t smem = (size_t)np * 8 + (size_t)cap * 8 + (size_t)cap * 8 + (size_t)cap * 2 + 16 + ((size_t)cap + 16) * 4;
+    // key | wint | parent | depth | (16-aligned) u32 leaf weights for the merge window | lengths
+    size_t smem = (size_t)np * 8 + (size_t)cap * 8 + (size_t)cap * 8 + (size_t)cap * 2 + 16 + ((size_t)cap + 16) * 4 + (size_t)cap;
     int use_smem = smem <= 160 * 1024;
     if (use_smem) {
         LZB_CUDA_TRY(set_dyn_smem(k_codebook<true>, smem));
