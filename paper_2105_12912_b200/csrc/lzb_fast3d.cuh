@@ -73,6 +73,29 @@ __device__ __forceinline__ int32_t pq_fast_f32m(float x, float inv_hi, float inv
     return __float_as_int(t) - 0x4B400000;
 }
 
+// Four-instruction form (K1 TMA path): the magic-number add is fused with
+// the product, t = RN(x * inv_hi + M), so k = t - M is the integer nearest
+// to the exact product x * inv_hi; the remainder against k is
+// f = RN(x * inv_lo + RN(x * inv_hi - k)), within 2^-24 of x * inv - k for
+// |k| < 2^22 (the inner FMA's argument is below 1 in magnitude: rounding
+// 2^-26; the outer sum below 1: 2^-25), so the same |f| < 0.5 - 2^-16
+// acceptance proves k = round-half-away(x / 2eb) exactly as above.  The
+// magnitude guard is |k| < 2^22 through the running maximum `kmax` (NaN
+// inputs fail the remainder test, infinities both).  Returns the BIASED
+// integer float_as_int(t) = 0x4B400000 + k: the Lorenzo differences cancel
+// the bias everywhere but at a chunk's origin element, which the caller
+// corrects once (kPqBias).
+constexpr int32_t kPqBias = 0x4B400000;
+__device__ __forceinline__ int32_t pq_fast_f32b(float x, float inv_hi, float inv_lo, bool &ok, float &kmax) {
+    const float M = 12582912.0f;  // 1.5 * 2^23
+    const float t = __fmaf_rn(x, inv_hi, M);
+    const float k = __fsub_rn(t, M);
+    const float f = __fmaf_rn(x, inv_lo, __fmaf_rn(x, inv_hi, -k));
+    ok = ok && (fabsf(f) < 0.4999847412109375f);
+    kmax = fmaxf(kmax, fabsf(k));
+    return __float_as_int(t);
+}
+
 // exact reference prequantization; flags: 1 overflow, 2 assert
 __device__ __forceinline__ int64_t pq_exact(double v, double two_eb, double slack, int &flags) {
     double s = __ddiv_rn(v, two_eb);

@@ -190,21 +190,18 @@ __global__ void __launch_bounds__(kT1Threads, 1)
             }
             int32_t d0[8], d1[8];
             bool ok = true;
-            float amax = 0.0f;
+            float kmax = 0.0f;
+            // biased integers (f3::pq_fast_f32b): the deltas cancel the bias
+            // everywhere but at the chunk origin, corrected after them
 #pragma unroll
             for (int j = 0; j < 8; j++) {
-                d0[j] = f3::pq_fast_f32m(x0[j], p.inv_hi, p.inv_lo, ok, amax);
-                d1[j] = f3::pq_fast_f32m(x1[j], p.inv_hi, p.inv_lo, ok, amax);
+                d0[j] = f3::pq_fast_f32b(x0[j], p.inv_hi, p.inv_lo, ok, kmax);
+                d1[j] = f3::pq_fast_f32b(x1[j], p.inv_hi, p.inv_lo, ok, kmax);
             }
-            ok = ok && amax < 4194304.0f;
-            if (!__all_sync(f3::kFull, ok)) {
+            const bool big = !(kmax < 4194304.0f);  // |k| >= 2^22 (or an infinity)
+            if (!__all_sync(f3::kFull, ok && !big)) {
                 // rare: an element near a rounding tie (exact f64 division for
                 // it), or values beyond the int32 fast path (exact chunk path)
-                bool big = false;
-#pragma unroll
-                for (int j = 0; j < 8; j++)
-                    big |= fabsf(__fmul_rn(x0[j], p.inv_hi)) >= 4194304.0f ||
-                           fabsf(__fmul_rn(x1[j], p.inv_hi)) >= 4194304.0f;
                 if (__any_sync(f3::kFull, big)) {
                     slow = true;
                 } else if (!ok) {
@@ -213,10 +210,12 @@ __global__ void __launch_bounds__(kT1Threads, 1)
                         const uint32_t j = b & 7;
                         const float xv = b < 8 ? t1_pick(x0, j) : t1_pick(x1, j);
                         bool e = true;
-                        (void)f3::pq_fast_f32(xv, p.inv_hi, p.inv_lo, e);
+                        float km = 0.0f;
+                        (void)f3::pq_fast_f32b(xv, p.inv_hi, p.inv_lo, e, km);
                         if (!e) {
                             int fl = 0;
-                            const int32_t v = (int32_t)f3::pq_exact((double)xv, p.two_eb, p.slack, fl);
+                            const int32_t v =
+                                (int32_t)f3::pq_exact((double)xv, p.two_eb, p.slack, fl) + f3::kPqBias;
                             flags |= fl;
                             if (b < 8) t1_put(d0, j, v);
                             else t1_put(d1, j, v);
@@ -226,6 +225,7 @@ __global__ void __launch_bounds__(kT1Threads, 1)
             }
             if (!slow) {
                 f3::deltas<int32_t>(d0, d1, lane);
+                d0[0] -= lane == 0 ? f3::kPqBias : 0;
                 uint32_t c0[8], c1[8];
                 uint32_t o0 = 0, o1 = 0;
 #pragma unroll
