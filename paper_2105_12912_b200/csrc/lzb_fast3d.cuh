@@ -39,55 +39,35 @@ __device__ __forceinline__ int32_t pq_fast(double x, double inv, bool &ok) {
 }
 
 // f32-input fast path in FP32 arithmetic (2x the FP64 rate, no conversions):
-// q = x * (inv_hi + inv_lo) as a double-single product (relative error
-// ~2^-46), the nearest integer from a magic-number add.  Accepted only for
-// |q| < 2^22 and q at least 2^-16 away from a half-integer, where the
-// absolute error (< 2^-23) cannot change round-half-away(x / 2eb) nor the
-// reference's debug assert.
+// q = x * (inv_hi + inv_lo) with inv_hi + inv_lo = 1/(2eb) to ~2^-46.  The
+// magic-number add is fused with the product, t = RN(x * inv_hi + M), so
+// k = t - M is the integer nearest to the exact product x * inv_hi; the
+// remainder against k is f = RN(x * inv_lo + RN(x * inv_hi - k)), within
+// 2^-24 of x * inv - k for |k| < 2^22 (the inner FMA's argument is below 1/2
+// in magnitude: rounding 2^-26; the outer sum below 1: 2^-25; the split of
+// 1/(2eb): 2^-24).  Accepted only for |k| < 2^22 and |f| < 1/2 - 2^-16, where
+// the error cannot change round-half-away(x / 2eb) nor the reference's debug
+// assert; NaN inputs fail the remainder
+// test, infinities both.  lzb_prequant_verify checks exactly this function
+// against the exact rule over all 2^32 f32 bit patterns.
 __device__ __forceinline__ int32_t pq_fast_f32(float x, float inv_hi, float inv_lo, bool &ok) {
     const float M = 12582912.0f;  // 1.5 * 2^23
-    float ph = __fmul_rn(x, inv_hi);
-    float pe = __fmaf_rn(x, inv_hi, -ph);  // exact error of ph
-    float pl = __fmaf_rn(x, inv_lo, pe);
-    float t = __fadd_rn(ph, M);
-    float k = __fsub_rn(t, M);             // nearest integer to ph
-    float f = __fadd_rn(__fsub_rn(ph, k), pl);
-    ok = ok && (fabsf(ph) < 4194304.0f) && (fabsf(f) < 0.4999847412109375f);
+    const float t = __fmaf_rn(x, inv_hi, M);
+    const float k = __fsub_rn(t, M);
+    const float f = __fmaf_rn(x, inv_lo, __fmaf_rn(x, inv_hi, -k));
+    ok = ok && (fabsf(k) < 4194304.0f) && (fabsf(f) < 0.4999847412109375f);
     return __float_as_int(t) - 0x4B400000;  // integer value of k
 }
 
-// The same with the magnitude guard folded into a running maximum: the
-// caller tests |ph|max < 2^22 once for all its elements (one FMNMX per
-// element instead of a compare and a predicate merge).  NaN / inf inputs
-// still fail the tie test (f is NaN), so `ok` keeps its meaning.
-__device__ __forceinline__ int32_t pq_fast_f32m(float x, float inv_hi, float inv_lo, bool &ok, float &amax) {
-    const float M = 12582912.0f;  // 1.5 * 2^23
-    float ph = __fmul_rn(x, inv_hi);
-    float pe = __fmaf_rn(x, inv_hi, -ph);
-    float pl = __fmaf_rn(x, inv_lo, pe);
-    float t = __fadd_rn(ph, M);
-    float k = __fsub_rn(t, M);
-    float f = __fadd_rn(__fsub_rn(ph, k), pl);
-    ok = ok && (fabsf(f) < 0.4999847412109375f);
-    amax = fmaxf(amax, fabsf(ph));
-    return __float_as_int(t) - 0x4B400000;
-}
-
-// Four-instruction form (K1 TMA path): the magic-number add is fused with
-// the product, t = RN(x * inv_hi + M), so k = t - M is the integer nearest
-// to the exact product x * inv_hi; the remainder against k is
-// f = RN(x * inv_lo + RN(x * inv_hi - k)), within 2^-24 of x * inv - k for
-// |k| < 2^22 (the inner FMA's argument is below 1 in magnitude: rounding
-// 2^-26; the outer sum below 1: 2^-25), so the same |f| < 0.5 - 2^-16
-// acceptance proves k = round-half-away(x / 2eb) exactly as above.  The
-// magnitude guard is |k| < 2^22 through the running maximum `kmax` (NaN
-// inputs fail the remainder test, infinities both).  Returns the BIASED
+// The same arithmetic for the K1 TMA path: the magnitude guard is folded
+// into a running maximum `kmax` (the caller tests kmax < 2^22 once; NaN
+// inputs still fail the remainder test), and the result is the BIASED
 // integer float_as_int(t) = 0x4B400000 + k: the Lorenzo differences cancel
 // the bias everywhere but at a chunk's origin element, which the caller
-// corrects once (kPqBias).
+// corrects once (kPqBias).  Accepted exactly when pq_fast_f32 accepts.
 constexpr int32_t kPqBias = 0x4B400000;
 __device__ __forceinline__ int32_t pq_fast_f32b(float x, float inv_hi, float inv_lo, bool &ok, float &kmax) {
-    const float M = 12582912.0f;  // 1.5 * 2^23
+    const float M = 12582912.0f;
     const float t = __fmaf_rn(x, inv_hi, M);
     const float k = __fsub_rn(t, M);
     const float f = __fmaf_rn(x, inv_lo, __fmaf_rn(x, inv_hi, -k));
