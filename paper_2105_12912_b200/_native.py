@@ -15,7 +15,8 @@ import numpy as np
 from .errors import CompressionError, CorruptArchiveError, DataError, QuantOverflowError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "liblzb.so")
+# LZB_LIB: another build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("LZB_LIB") or os.path.join(_HERE, "_lib", "liblzb.so")
 
 LZB_OK, LZB_E_ARG, LZB_E_DATA, LZB_E_OVERFLOW = 0, 1, 2, 3
 LZB_E_CORRUPT, LZB_E_CUDA, LZB_E_ASSERT, LZB_E_CAPACITY = 4, 5, 6, 7

@@ -490,6 +490,10 @@ __global__ void __launch_bounds__(kF9Warps * 32, 1) k_dec_final9(DecParams p, ui
     if (p.st->code) return;  // corrupt stream: leave the output untouched
     const DecCanon *tab = &s_can;
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    // table addresses held in registers (otherwise the shared window base is
+    // rebuilt from SR_CgaCtaId inside the decode loop: 4 instructions a step)
+    const uint32_t lut_s = smem_addr(s_lut), st_s = smem_addr(s_st), s1_s = smem_addr(s_s1),
+                   l1_s = smem_addr(s_l1);
     const int32_t base8 = (int32_t)(cap / 2) - 128;
     const uint32_t b2 = ((uint32_t)base8 & 0xFFFFu) * 0x00010001u;  // per-halfword widening addend
     uint8_t *wout = s_out + warp * kF9Stage;
@@ -573,16 +577,16 @@ __global__ void __launch_bounds__(kF9Warps * 32, 1) k_dec_final9(DecParams p, ui
             r.init(stg, rel + p.head);
             while (rel < mstop) {
                 const uint32_t pk = r.peek12();
-                const uint64_t en = s_lut[pk];
-                uint32_t n = (uint32_t)(en >> 48) & 7u, adv = (uint32_t)(en >> 51) & 15u;
-                uint32_t lo = (uint32_t)en, hi = (uint32_t)(en >> 32);
+                uint32_t lo, hi;
+                asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(lut_s + 8 * pk));
+                uint32_t n = (hi >> 16) & 7u, adv = (hi >> 19) & 15u;
                 if (n == 0) {  // long code word, out-of-byte symbol, or invalid prefix
-                    const uint32_t l1 = s_l1[pk];
+                    const uint32_t l1 = lds8(l1_s + pk);
                     uint32_t sym = 0;
                     if (l1 & 0x80u) adv = dsym_long(tab, p.syms, r.peek64(), l1 & 0x7Fu, sym);
                     else if (l1) {
                         adv = l1;
-                        sym = s_s1[pk];
+                        sym = lds16(s1_s + 2 * pk);
                     } else {
                         adv = 0;
                     }
@@ -606,7 +610,7 @@ __global__ void __launch_bounds__(kF9Warps * 32, 1) k_dec_final9(DecParams p, ui
                     continue;
                 }
                 if (mstop - rel < (uint32_t)kLutBits) {  // code words must start before mstop
-                    const uint32_t hs = (uint32_t)s_st[pk] & (0xFFFu << (mstop - rel));
+                    const uint32_t hs = lds16(st_s + 2 * pk) & (0xFFFu << (mstop - rel));
                     n -= __popc(hs);
                     adv = hs ? (uint32_t)(__ffs(hs) - 1) : adv;
                 }

@@ -165,6 +165,11 @@ __device__ __forceinline__ uint32_t lds8(uint32_t a) {
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
 }
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 // A shared address held in a register (the compiler may otherwise rebuild it
 // from the CTA's shared window base inside hot loops).
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
