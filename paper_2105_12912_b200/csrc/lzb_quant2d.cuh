@@ -257,10 +257,12 @@ __global__ void __launch_bounds__(kQ3Threads, 4) k_quantize_r8(const __grid_cons
         ? (uint32_t)__cvta_generic_to_shared(s_col + warp * 16 * 32) + lane * 4
         : 0xFFFFFFFFu;
     int flags = 0;
+    // tiles from the end of the stream first (partial chunks; see k_quantize3d8)
     auto claim = [&]() -> uint64_t {
         uint64_t t = 0;
         if (lane == 0) t = atomicAdd(p.ticket, 1u);
-        return __shfl_sync(f3::kFull, t, 0);
+        t = __shfl_sync(f3::kFull, t, 0);
+        return t < p.ntiles ? p.ntiles - 1 - t : p.ntiles;
     };
     // the next chunk's values are loaded while the current one is processed
     uint64_t t = claim();

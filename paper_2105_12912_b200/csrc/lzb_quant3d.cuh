@@ -517,10 +517,15 @@ __global__ void __launch_bounds__(kQ3Threads, 2) k_quantize3d8(const __grid_cons
     w.flags = 0;
     // Tiles are claimed one ahead so the first chunk of the next tile is
     // prefetched while the last chunk of the current one is processed.
+    // Tickets hand out tiles from the END of the stream: the last chunk
+    // layer / row ends are the partial chunks (exact path, several times
+    // slower), so they start first and the run ends on full tiles instead of
+    // a tail of a few warps on partial ones.  Tiles are independent.
     auto claim = [&]() -> uint64_t {
         uint64_t t = 0;
         if (lane == 0) t = atomicAdd(p.ticket, 1u);
-        return __shfl_sync(f3::kFull, t, 0);
+        t = __shfl_sync(f3::kFull, t, 0);
+        return t < p.ntiles ? p.ntiles - 1 - t : p.ntiles;
     };
     uint64_t t = claim();
     uint64_t t_next = t < p.ntiles ? claim() : p.ntiles;

@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(kR3Threads, 4) k_reconstruct_r8(const __grid_c
         if (lane == 0) t = atomicAdd(p.ticket, 1u);
         t = __shfl_sync(f3::kFull, t, 0);
         if (t >= p.ntiles) break;
+        t = p.ntiles - 1 - t;  // tiles from the end first (partial chunks; see k_quantize3d8)
         const uint64_t c0 = t * kR3TileChunks;
         const uint64_t c1 = umin64(c0 + kR3TileChunks, p.nchunks);
         const uint64_t r0 = p.tile_start[t], r1 = p.tile_start[t + 1];
