@@ -672,7 +672,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         import torch.distributed as dist
 
     shape = cfg["shape"]
-    if world > 1:
+    if world > 1 or args.sharded:
         return run_sharded(args, cfg, rank, world, dev, local_rank)
 
     x = gen_field_device(cfg, dev)
@@ -986,6 +986,8 @@ def main():
     ap.add_argument("--ref-sample-elems", type=int, default=2048 * 2048 * 16)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N>1 (gloo only for one-GPU debugging)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="check: run the N>1 slab path (process group, NCCL collectives) even at N=1")
     ap.add_argument("--same-device", action="store_true",
                     help="debug: put every rank on cuda:0 (with --backend gloo)")
     args = ap.parse_args()
@@ -995,7 +997,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = CONFIGS[args.config]
-    if world > 1:
+    use_pg = world > 1 or (args.sharded and args.impl != "reference")
+    if use_pg:
         import torch
         import torch.distributed as dist
 
@@ -1011,7 +1014,7 @@ def main():
         else:
             run_gpu(args, cfg, rank, world, local_rank)
     finally:
-        if world > 1:
+        if use_pg:
             import torch.distributed as dist
 
             dist.barrier()
