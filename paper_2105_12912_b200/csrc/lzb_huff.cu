@@ -1283,7 +1283,11 @@ int d4_plan(const uint8_t *bits, uint32_t bit_phase, uint64_t bit_len, uint64_t 
     k_dec_luts<<<kLutSize / 1024, 1024, 0, s>>>(const_cast<DecTables *>(p.tab), p.syms, cap, st);
     LZB_LAUNCH_CHECK();
     const int sms = dev_sms();
-    k_dec4_count<<<(unsigned)umin64((p.T + kD4Warps - 1) / kD4Warps, (uint64_t)sms * 8), kD4Warps * 32, 0, s>>>(p);
+    // 32 CTAs per SM requested, ~5 resident: later CTAs fill in behind the
+    // slow subsequences (measured: 8 / 16 / 32 / 64 per SM -> K5 3.67 / 3.61 /
+    // 3.59 / 3.58 ms on C5q, C3 5.09 -> 4.94 ms at 32; sized to the resident
+    // CTAs exactly: 3.77 ms)
+    k_dec4_count<<<(unsigned)umin64((p.T + kD4Warps - 1) / kD4Warps, (uint64_t)sms * 32), kD4Warps * 32, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
     k_dec4_resolve<<<(unsigned)umin64(ntl, (uint64_t)sms * 4), kD4ResolveThreads, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
@@ -1345,11 +1349,13 @@ static int huff_encode_w(const void *sym, uint64_t n, const uint8_t *lengths, co
     int per_sm = 0;
     LZB_CUDA_TRY(occupancy(&per_sm, k_huff_encode_w, kWWarps * 32, smem));
     if (per_sm < 1) return LZB_E_ARG;
-    uint64_t grid = (uint64_t)dev_sms() * per_sm;
+    // 4x the resident CTAs: the later waves even out the warps' tile loads
+    // (C5q encode 1.47 -> 1.40 ms; count pass likewise at 32 CTAs per SM)
+    uint64_t grid = (uint64_t)dev_sms() * per_sm * 4;
     const uint64_t need = (ntw + kWWarps - 1) / kWWarps;
     if (grid > need) grid = need;
     const int sms = dev_sms();
-    k_huff_count_w<<<(unsigned)umin64((ntw + 7) / 8, (uint64_t)sms * 8), 256, 0, s>>>(p);
+    k_huff_count_w<<<(unsigned)umin64((ntw + 7) / 8, (uint64_t)sms * 32), 256, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
     k_huff_scan_w<<<(unsigned)nscan, 256, 0, s>>>(p);
     LZB_LAUNCH_CHECK();
